@@ -1,0 +1,156 @@
+/*
+ * qmsort_gpu.h -- C-ABI of the B200-native QuickMergesort replacement.
+ *
+ * Drop-in boundary for the reference entry point
+ *     template <class It, class Less = std::less<>>
+ *     Metrics qmsort::sort(It first, It last, const SortConfig& cfg = {},
+ *                          Less less = {}, SortObserver* obs = nullptr);
+ *   (/root/reference/proj/core/include/qmsort/sort.hpp:215-226)
+ * and its counted twin sort_range_counted (sort.hpp:207-211).  The reference is
+ * a header-only C++ template library; a foreign caller (ctypes, a C++ shim,
+ * JNI ...) binds the plain-C functions below.  No torch or CUDA types appear in
+ * the signatures: device buffers and streams are passed as void*.
+ *
+ * Every entry point returns QMSORT_OK (0) or a QMSORT_E* code and never
+ * throws; qmsort_gpu_last_error() describes the last failure of the calling
+ * thread.  There is no CPU fallback: without a usable sm_100 device every
+ * compute call fails with QMSORT_ECUDA.
+ */
+#ifndef QMSORT_GPU_H
+#define QMSORT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (SURVEY.md 8(b) "Errors") ---------------------------- */
+#define QMSORT_OK 0
+#define QMSORT_EINVAL 1    /* bad dtype / comparator / n / config          */
+#define QMSORT_ENOWS 2     /* caller workspace smaller than required       */
+#define QMSORT_ECUDA 3     /* CUDA runtime error (see last_error)          */
+#define QMSORT_ENCCL 4     /* collective failure (sharded path)            */
+#define QMSORT_EINTERNAL 5 /* internal capacity overflow                   */
+
+/* ---- element types: the five BASELINE.json configs --------------------- */
+typedef enum {
+    QMSORT_DT_I32 = 0,   /* int32_t                                        */
+    QMSORT_DT_U32 = 1,   /* uint32_t                                       */
+    QMSORT_DT_U64 = 2,   /* uint64_t                                       */
+    QMSORT_DT_F64 = 3,   /* double, NaN-free, no -0.0                       */
+    QMSORT_DT_REC32 = 4  /* 4 x uint64_t, lexicographic over w0..w3         */
+} qmsort_dtype;
+
+/* ---- comparator: the reference's Less template argument ---------------- */
+typedef enum {
+    QMSORT_LESS = 0,    /* std::less<>    (ascending)                      */
+    QMSORT_GREATER = 1  /* std::greater<> (descending, test_sort.cpp:356)  */
+} qmsort_cmp;
+
+/* ---- SortConfig as C scalars (sort.hpp:17-34, merge.hpp:14-31) --------- */
+typedef struct {
+    int variant;                     /* Variant: 0 qms 1 qmqs 2 momqms 3 hqms       */
+    int pivot;                       /* PivotStrategy: 0 median_of_3,
+                                        1 median_of_sqrt_n, 2 mom_of_thirds,
+                                        3 hybrid                                   */
+    int base_case_kind;              /* BaseCase: 0 insertion 1 hardcoded_small
+                                        2 clever_quicksort                         */
+    uint64_t base_case_size_threshold; /* BaseCasePolicy::size_threshold (10)     */
+    int base_case_use_levels;        /* BaseCasePolicy::use_levels                 */
+    double beta;                     /* 0.5                                        */
+    double delta;                    /* 1/16                                       */
+    int side;                        /* MergesortSide: 0 smaller_always,
+                                        1 larger_when_feasible (ignored on GPU)     */
+    int three_way;                   /* always on for equal splitters on the GPU    */
+    uint64_t block;                  /* partition block hint (kDefaultBlock 128)    */
+    /* GPU knobs (GpuSortOptions): not in the reference SortConfig */
+    int algorithm;                   /* 0 samplesort (default), 1 mergesort          */
+    uint64_t seed;                   /* sampling seed                                */
+    int max_levels;                  /* partition levels before the merge fallback   */
+} qmsort_gpu_config;
+
+/* ---- Metrics (metrics.hpp:14-24) plus GPU pass ledger ------------------- */
+typedef struct {
+    uint64_t comparisons; /* not instrumented on the GPU: 0                 */
+    uint64_t moves;       /* not instrumented on the GPU: 0                 */
+    uint64_t max_depth;   /* partition levels used                          */
+    uint64_t elapsed_ns;  /* device time of the sort (CUDA events)          */
+    uint64_t alg_bytes;   /* B_alg: key bytes credited per executed pass     */
+    uint32_t levels;      /* samplesort partition levels                    */
+    uint32_t merge_passes;/* merge-path passes (fallback / mergesort)       */
+    uint32_t kernel_launches; /* kernels launched by this call              */
+    uint32_t host_syncs;  /* host synchronisations inside the sort          */
+} qmsort_gpu_metrics;
+
+/* Presets qms() / qmqs() / momqms() / hqms() (sort.hpp:37-66). */
+void qmsort_gpu_config_init(qmsort_gpu_config* cfg, int variant);
+
+/* Bytes of device workspace qmsort_gpu_sort needs for n elements. */
+size_t qmsort_gpu_workspace_bytes(int dtype, size_t n, const qmsort_gpu_config* cfg);
+
+/* Sort d_data[0..n) in place on the device.  Replaces qmsort::sort
+ * (sort.hpp:215-226) for device-resident ranges.  d_ws may be NULL (the
+ * library allocates and frees it); otherwise ws_bytes must be at least
+ * qmsort_gpu_workspace_bytes().  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  The call returns after the sort completed. */
+int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu_config* cfg,
+                    void* d_ws, size_t ws_bytes, qmsort_gpu_metrics* metrics, void* stream);
+
+/* Host-array drop-in: copies h_data[0..n) to the device, sorts, copies back.
+ * Same contract as qmsort::sort(v.begin(), v.end(), cfg, less) on a
+ * contiguous host range.  Device buffers are cached per thread. */
+int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
+                         qmsort_gpu_metrics* metrics);
+
+/* Description of the last failure on the calling thread ("" if none). */
+const char* qmsort_gpu_last_error(void);
+
+/* Size in bytes of one element of dtype (0 for an unknown dtype). */
+size_t qmsort_gpu_dtype_size(int dtype);
+
+/* ---- sharded samplesort building blocks ---------------- */
+/* In-place order-preserving transform into / out of the unsigned key domain
+ * (inverse = 0 forward, 1 back).  After the forward transform, (I32,*) data is
+ * sorted as (U32, LESS), (F64,*) as (U64, LESS), (*, GREATER) as LESS. */
+int qmsort_gpu_transform(int dtype, int cmp, void* d_data, size_t n, int inverse, void* stream);
+
+/* Core key dtype for a caller dtype: I32->U32, F64->U64, others unchanged. */
+int qmsort_gpu_core_dtype(int dtype);
+
+/* Gather s seeded random keys of d_data[0..n) (core dtype) into d_out. */
+int qmsort_gpu_sample(int core_dtype, const void* d_data, size_t n, size_t s, uint64_t seed,
+                      void* d_out, void* stream);
+
+/* One partition level with caller-given sorted splitters (core dtype):
+ * bucket b = #{splitters < key} (b in [0, nsplit]); writes d_in permuted so
+ * that buckets are contiguous and ascending into d_out and the bucket sizes
+ * into d_counts[0..nsplit] (uint64).  nsplit <= 1023.  Uses d_ws (see
+ * qmsort_gpu_partition_workspace_bytes) or allocates if NULL. */
+size_t qmsort_gpu_partition_workspace_bytes(int core_dtype, size_t n);
+int qmsort_gpu_partition(int core_dtype, const void* d_in, size_t n, const void* d_splitters,
+                         uint32_t nsplit, void* d_out, uint64_t* d_counts, void* d_ws,
+                         size_t ws_bytes, void* stream);
+
+/* ---- harness (K9 generators, verification) ----------------------------- */
+/* kind: 0 u32 uniform, 1 u64 uniform, 2 rec32, 10..14 f64 sorted / reverse /
+ * 16-distinct / gaussian / organ-pipe.  Element i is global element start+i
+ * of an array of `total` elements (SURVEY.md 8(d) recipes). */
+int qmsort_gpu_generate(int kind, void* d_out, size_t n, uint64_t seed, uint64_t start,
+                        uint64_t total, void* stream);
+
+/* out3[0] = adjacent order violations under (dtype, cmp) (if check_order),
+ * out3[1] = sum, out3[2] = xor of a per-element fingerprint (multiset hash).
+ * Synchronises the stream. */
+int qmsort_gpu_check(int dtype, int cmp, const void* d_data, size_t n, int check_order,
+                     uint64_t* out3, void* stream);
+
+/* Library build identification (e.g. "qmsort-b200 sm_100a"). */
+const char* qmsort_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QMSORT_GPU_H */

@@ -1,0 +1,279 @@
+"""qmsort-b200: a B200-native drop-in for the reference QuickMergesort entry point.
+
+Python mirror of the reference API (``/root/reference/proj/core/include/qmsort``):
+
+=====================================  ============================================
+reference (C++)                        here
+=====================================  ============================================
+``enum class Variant`` (sort.hpp:17)   :class:`Variant`
+``enum class PivotStrategy`` (:19)     :class:`PivotStrategy`
+``enum class BaseCase`` (merge.hpp:14) :class:`BaseCase`
+``BaseCasePolicy`` (merge.hpp:26-31)   :class:`BaseCasePolicy`
+``SortConfig`` (sort.hpp:25-34)        :class:`SortConfig` (+ GPU knobs)
+``qms/qmqs/momqms/hqms`` (:37-66)      :func:`qms` :func:`qmqs` :func:`momqms` :func:`hqms`
+``Metrics`` (metrics.hpp:14-24)        :class:`Metrics`
+``qmsort::sort(first, last, cfg,       :func:`sort` (device tensor in place, or host
+  less)`` (sort.hpp:215-226)             array through the host drop-in call)
+``sort_range_counted`` (:207-211)      :func:`sort_range_counted`
+=====================================  ============================================
+
+All compute goes through the CUDA library (``libqmsort_gpu.so``) via the C-ABI
+in ``include/qmsort_gpu.h``; nothing here sorts on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import dataclasses
+import enum
+from typing import Any
+
+from . import _lib
+from ._lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64, GREATER, LESS, QmsortError
+
+__all__ = [
+    "Variant", "PivotStrategy", "BaseCase", "MergesortSide", "BaseCasePolicy", "SortConfig",
+    "Metrics", "qms", "qmqs", "momqms", "hqms", "sort", "sort_range_counted", "QmsortError",
+    "DT_I32", "DT_U32", "DT_U64", "DT_F64", "DT_REC32", "LESS", "GREATER",
+    "workspace_bytes", "generate", "check", "dtype_of",
+]
+
+
+class Variant(enum.IntEnum):
+    qms = 0
+    qmqs = 1
+    momqms = 2
+    hqms = 3
+
+
+class PivotStrategy(enum.IntEnum):
+    median_of_3 = 0
+    median_of_sqrt_n = 1
+    mom_of_thirds = 2
+    hybrid = 3
+
+
+class BaseCase(enum.IntEnum):
+    insertion = 0
+    hardcoded_small = 1
+    clever_quicksort = 2
+
+
+class MergesortSide(enum.IntEnum):
+    smaller_always = 0
+    larger_when_feasible = 1
+
+
+@dataclasses.dataclass
+class BaseCasePolicy:
+    """merge.hpp:26-31.  On the GPU every kind maps to the block sorter (K5)."""
+
+    kind: BaseCase = BaseCase.hardcoded_small
+    size_threshold: int = 10
+    use_levels: bool = False
+
+
+class Algorithm(enum.IntEnum):
+    samplesort = 0  # sampled multi-splitter partition + block sort (default)
+    mergesort = 1   # block sort + merge-path passes only
+
+
+@dataclasses.dataclass
+class SortConfig:
+    """SortConfig (sort.hpp:25-34) plus the GPU-only knobs (GpuSortOptions)."""
+
+    variant: Variant = Variant.qms
+    pivot: PivotStrategy = PivotStrategy.median_of_3
+    base_case: BaseCasePolicy = dataclasses.field(default_factory=BaseCasePolicy)
+    beta: float = 0.5
+    delta: float = 1.0 / 16.0
+    side: MergesortSide = MergesortSide.larger_when_feasible
+    three_way: bool = False
+    block: int = 128
+    # GPU knobs
+    algorithm: Algorithm = Algorithm.samplesort
+    seed: int = 42
+    max_levels: int = 8
+
+    def to_c(self) -> _lib.GpuConfig:
+        c = _lib.GpuConfig()
+        c.variant = int(self.variant)
+        c.pivot = int(self.pivot)
+        c.base_case_kind = int(self.base_case.kind)
+        c.base_case_size_threshold = int(self.base_case.size_threshold)
+        c.base_case_use_levels = int(bool(self.base_case.use_levels))
+        c.beta = float(self.beta)
+        c.delta = float(self.delta)
+        c.side = int(self.side)
+        c.three_way = int(bool(self.three_way))
+        c.block = int(self.block)
+        c.algorithm = int(self.algorithm)
+        c.seed = int(self.seed) & ((1 << 64) - 1)
+        c.max_levels = int(self.max_levels)
+        return c
+
+
+def qms() -> SortConfig:
+    """Median-of-3 pivots, hard-coded small base case (sort.hpp:37)."""
+    return SortConfig()
+
+
+def qmqs() -> SortConfig:
+    """sort.hpp:41-48."""
+    return SortConfig(variant=Variant.qmqs,
+                      base_case=BaseCasePolicy(BaseCase.clever_quicksort, 16, True))
+
+
+def momqms() -> SortConfig:
+    """sort.hpp:52-57."""
+    return SortConfig(variant=Variant.momqms, pivot=PivotStrategy.mom_of_thirds)
+
+
+def hqms() -> SortConfig:
+    """sort.hpp:61-66."""
+    return SortConfig(variant=Variant.hqms, pivot=PivotStrategy.hybrid)
+
+
+@dataclasses.dataclass
+class Metrics:
+    """metrics.hpp:14-24.  comparisons/moves are not instrumented on the GPU (0);
+    max_depth = partition levels; elapsed_ns = device time (CUDA events)."""
+
+    comparisons: int = 0
+    moves: int = 0
+    max_depth: int = 0
+    elapsed_ns: int = 0
+    # GPU pass ledger
+    alg_bytes: int = 0
+    levels: int = 0
+    merge_passes: int = 0
+    kernel_launches: int = 0
+    host_syncs: int = 0
+
+    @classmethod
+    def from_c(cls, m: _lib.GpuMetrics) -> "Metrics":
+        return cls(**{f.name: int(getattr(m, f.name)) for f in dataclasses.fields(cls)})
+
+
+def _cmp_code(less: Any) -> int:
+    if less in (None, "less", LESS):
+        return LESS
+    if less in ("greater", GREATER):
+        return GREATER
+    raise ValueError(f"unsupported comparator {less!r}: use 'less' or 'greater'")
+
+
+def dtype_of(data: Any) -> int:
+    """Map a torch tensor / numpy array to a qmsort dtype code.
+
+    int32 -> I32, uint32 -> U32, uint64 -> U64, float64 -> F64, and an (n, 4)
+    array of 64-bit words -> REC32 (records compared lexicographically).
+    """
+    name = str(data.dtype).replace("torch.", "")
+    shape = tuple(data.shape)
+    if len(shape) == 2 and shape[1] == 4 and name in ("uint64", "int64"):
+        return DT_REC32
+    if len(shape) != 1:
+        raise ValueError(f"expected a 1-D array or an (n, 4) record array, got shape {shape}")
+    table = {"int32": DT_I32, "uint32": DT_U32, "uint64": DT_U64, "float64": DT_F64}
+    if name not in table:
+        raise ValueError(f"unsupported dtype {name}")
+    return table[name]
+
+
+def _is_torch_cuda(x: Any) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def _stream_ptr(stream: Any) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+def workspace_bytes(dtype: int, n: int, cfg: SortConfig | None = None) -> int:
+    lib = _lib.load()
+    c = (cfg or SortConfig()).to_c()
+    return int(lib.qmsort_gpu_workspace_bytes(dtype, n, ctypes.byref(c)))
+
+
+def sort(data: Any, cfg: SortConfig | None = None, less: Any = "less", *, workspace: Any = None,
+         stream: Any = None) -> Metrics:
+    """Sort ``data`` ascending under ``less`` in place and return the Metrics.
+
+    * CUDA torch tensor: sorted on its device (``qmsort_gpu_sort``); the
+      optional ``workspace`` is a uint8 CUDA tensor of at least
+      :func:`workspace_bytes`.
+    * numpy array / CPU tensor (C-contiguous): the host drop-in call
+      ``qmsort_gpu_sort_host`` copies it to the GPU, sorts and copies back.
+    """
+    lib = _lib.load()
+    cfg = cfg or SortConfig()
+    c = cfg.to_c()
+    m = _lib.GpuMetrics()
+    dt = dtype_of(data)
+    cmp = _cmp_code(less)
+    n = int(data.shape[0])
+    if _is_torch_cuda(data):
+        if not data.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        ws_ptr, ws_bytes = None, 0
+        if workspace is not None:
+            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        rc = lib.qmsort_gpu_sort(dt, cmp, data.data_ptr(), n, ctypes.byref(c), ws_ptr, ws_bytes,
+                                 ctypes.byref(m), _stream_ptr(stream))
+        _lib.check(rc, "qmsort_gpu_sort")
+    else:
+        ptr = _host_ptr(data)
+        rc = lib.qmsort_gpu_sort_host(dt, cmp, ptr, n, ctypes.byref(c), ctypes.byref(m))
+        _lib.check(rc, "qmsort_gpu_sort_host")
+    return Metrics.from_c(m)
+
+
+def sort_range_counted(data: Any, cfg: SortConfig, metrics: Metrics, less: Any = "less") -> None:
+    """sort.hpp:207-211: sort and accumulate into a caller-owned Metrics."""
+    r = sort(data, cfg, less)
+    metrics.elapsed_ns += r.elapsed_ns
+    metrics.max_depth = max(metrics.max_depth, r.max_depth)
+    metrics.alg_bytes += r.alg_bytes
+    metrics.levels += r.levels
+    metrics.merge_passes += r.merge_passes
+    metrics.kernel_launches += r.kernel_launches
+    metrics.host_syncs += r.host_syncs
+
+
+def _host_ptr(data: Any) -> int:
+    if type(data).__module__.startswith("torch"):
+        if not data.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return data.data_ptr()
+    if not data.flags["C_CONTIGUOUS"] or not data.flags["WRITEABLE"]:
+        raise ValueError("array must be C-contiguous and writeable")
+    return data.ctypes.data
+
+
+# ---------------------------------------------------------------------------
+# Harness helpers (K9 generators and verification), used by bench.py / tests.
+# ---------------------------------------------------------------------------
+GEN_U32, GEN_U64, GEN_REC32 = 0, 1, 2
+GEN_F64_SORTED, GEN_F64_REVERSE, GEN_F64_DISTINCT16, GEN_F64_GAUSS, GEN_F64_ORGAN = 10, 11, 12, 13, 14
+
+
+def generate(kind: int, out: Any, seed: int, start: int = 0, total: int | None = None,
+             stream: Any = None) -> None:
+    """Fill CUDA tensor ``out`` with global elements [start, start+n) of a seeded config."""
+    lib = _lib.load()
+    n = int(out.shape[0])
+    rc = lib.qmsort_gpu_generate(kind, out.data_ptr(), n, seed, start, total or n,
+                                 _stream_ptr(stream))
+    _lib.check(rc, "qmsort_gpu_generate")
+
+
+def check(data: Any, less: Any = "less", order: bool = True, stream: Any = None) -> tuple[int, int, int]:
+    """(order violations, multiset sum fingerprint, multiset xor fingerprint) of a CUDA tensor."""
+    lib = _lib.load()
+    out = (ctypes.c_uint64 * 3)()
+    rc = lib.qmsort_gpu_check(dtype_of(data), _cmp_code(less), data.data_ptr(), int(data.shape[0]),
+                              int(order), out, _stream_ptr(stream))
+    _lib.check(rc, "qmsort_gpu_check")
+    return int(out[0]), int(out[1]), int(out[2])

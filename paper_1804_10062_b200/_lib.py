@@ -1,0 +1,132 @@
+"""ctypes binding of the C-ABI in include/qmsort_gpu.h.
+
+The shared library ``libqmsort_gpu.so`` is built in-tree by
+``__graft_entry__.build()`` (nvcc, sm_100a).  There is no CPU fallback: if the
+library is missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqmsort_gpu.so")
+
+QMSORT_OK = 0
+QMSORT_EINVAL = 1
+QMSORT_ENOWS = 2
+QMSORT_ECUDA = 3
+QMSORT_ENCCL = 4
+QMSORT_EINTERNAL = 5
+
+DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32 = 0, 1, 2, 3, 4
+LESS, GREATER = 0, 1
+
+
+class GpuConfig(ctypes.Structure):
+    """qmsort_gpu_config (mirrors SortConfig, sort.hpp:25-34)."""
+
+    _fields_ = [
+        ("variant", ctypes.c_int),
+        ("pivot", ctypes.c_int),
+        ("base_case_kind", ctypes.c_int),
+        ("base_case_size_threshold", ctypes.c_uint64),
+        ("base_case_use_levels", ctypes.c_int),
+        ("beta", ctypes.c_double),
+        ("delta", ctypes.c_double),
+        ("side", ctypes.c_int),
+        ("three_way", ctypes.c_int),
+        ("block", ctypes.c_uint64),
+        ("algorithm", ctypes.c_int),
+        ("seed", ctypes.c_uint64),
+        ("max_levels", ctypes.c_int),
+    ]
+
+
+class GpuMetrics(ctypes.Structure):
+    """qmsort_gpu_metrics (Metrics, metrics.hpp:14-24, plus the pass ledger)."""
+
+    _fields_ = [
+        ("comparisons", ctypes.c_uint64),
+        ("moves", ctypes.c_uint64),
+        ("max_depth", ctypes.c_uint64),
+        ("elapsed_ns", ctypes.c_uint64),
+        ("alg_bytes", ctypes.c_uint64),
+        ("levels", ctypes.c_uint32),
+        ("merge_passes", ctypes.c_uint32),
+        ("kernel_launches", ctypes.c_uint32),
+        ("host_syncs", ctypes.c_uint32),
+    ]
+
+
+EXPORTED = [
+    "qmsort_gpu_config_init",
+    "qmsort_gpu_workspace_bytes",
+    "qmsort_gpu_sort",
+    "qmsort_gpu_sort_host",
+    "qmsort_gpu_last_error",
+    "qmsort_gpu_dtype_size",
+    "qmsort_gpu_transform",
+    "qmsort_gpu_core_dtype",
+    "qmsort_gpu_sample",
+    "qmsort_gpu_partition_workspace_bytes",
+    "qmsort_gpu_partition",
+    "qmsort_gpu_generate",
+    "qmsort_gpu_check",
+    "qmsort_gpu_version",
+]
+
+_lib = None
+
+
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load (once) and type the C-ABI library; raises if it is absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"qmsort-b200 CUDA library not built: {p} is missing "
+            "(run `python -c 'import __graft_entry__ as g; g.build()'`)"
+        )
+    lib = ctypes.CDLL(p)
+    vp, sz, u64, i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int
+    cfgp, mp = ctypes.POINTER(GpuConfig), ctypes.POINTER(GpuMetrics)
+    sig = {
+        "qmsort_gpu_config_init": (None, [cfgp, i]),
+        "qmsort_gpu_workspace_bytes": (sz, [i, sz, cfgp]),
+        "qmsort_gpu_sort": (i, [i, i, vp, sz, cfgp, vp, sz, mp, vp]),
+        "qmsort_gpu_sort_host": (i, [i, i, vp, sz, cfgp, mp]),
+        "qmsort_gpu_last_error": (ctypes.c_char_p, []),
+        "qmsort_gpu_dtype_size": (sz, [i]),
+        "qmsort_gpu_transform": (i, [i, i, vp, sz, i, vp]),
+        "qmsort_gpu_core_dtype": (i, [i]),
+        "qmsort_gpu_sample": (i, [i, vp, sz, sz, u64, vp, vp]),
+        "qmsort_gpu_partition_workspace_bytes": (sz, [i, sz]),
+        "qmsort_gpu_partition": (i, [i, vp, sz, vp, ctypes.c_uint32, vp, vp, vp, sz, vp]),
+        "qmsort_gpu_generate": (i, [i, vp, sz, u64, u64, u64, vp]),
+        "qmsort_gpu_check": (i, [i, i, vp, sz, i, ctypes.POINTER(u64), vp]),
+        "qmsort_gpu_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+class QmsortError(RuntimeError):
+    """A nonzero C-ABI status, like the reference harness's runtime_error (trial.hpp:116)."""
+
+    def __init__(self, code: int, where: str):
+        msg = load().qmsort_gpu_last_error().decode(errors="replace")
+        super().__init__(f"{where} failed with status {code}: {msg}")
+        self.code = code
+
+
+def check(code: int, where: str) -> None:
+    if code != QMSORT_OK:
+        raise QmsortError(code, where)

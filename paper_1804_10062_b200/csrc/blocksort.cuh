@@ -1,0 +1,175 @@
+// blocksort.cuh -- K5: shared-memory block sort of register-resident tiles.
+//
+// Replaces the reference's base case X (small_sort / insertion_sort /
+// clever_quicksort, reference small_sort.hpp:13-111, clever.hpp:21-53) and the
+// bottom levels of the merge recursion (mergesort_into, merge.hpp:103-119):
+// instead of handing blocks below 10 elements to a straight-line sorter, every
+// bucket that fits one CTA is sorted entirely on chip:
+//   1. each thread sorts ITEMS keys in registers with Batcher's odd-even merge
+//      network (compile-time unrolled, no local memory);
+//   2. log2(T) merge-path rounds in shared memory double the run length; each
+//      thread locates its output diagonal by binary search (merge path) and
+//      merges ITEMS outputs serially -- the same "take run1 on ties" rule as
+//      swap_merge (merge.hpp:76), so the merge is stable.
+// The tile is loaded once from HBM and written once (2 n w bytes per pass).
+#pragma once
+#include <utility>
+
+#include "common.cuh"
+
+namespace qmsort_b200 {
+
+// Batcher odd-even merge sort network on N register-resident keys.  The
+// comparator list is computed at compile time and applied through a fold
+// expression, so every register index is a constant (no local memory).
+template <int N>
+struct OddEvenNet {
+    static constexpr int count() {
+        int c = 0;
+        for (int p = 1; p < N; p <<= 1)
+            for (int q = p; q >= 1; q >>= 1)
+                for (int j = q % p; j + q < N; j += 2 * q)
+                    for (int i = 0; i < q; ++i)
+                        if (i + j + q < N && (i + j) / (2 * p) == (i + j + q) / (2 * p)) ++c;
+        return c;
+    }
+    static constexpr int kCount = count();
+    struct Pairs {
+        int a[kCount > 0 ? kCount : 1];
+        int b[kCount > 0 ? kCount : 1];
+    };
+    static constexpr Pairs make() {
+        Pairs r{};
+        int c = 0;
+        for (int p = 1; p < N; p <<= 1)
+            for (int q = p; q >= 1; q >>= 1)
+                for (int j = q % p; j + q < N; j += 2 * q)
+                    for (int i = 0; i < q; ++i)
+                        if (i + j + q < N && (i + j) / (2 * p) == (i + j + q) / (2 * p)) {
+                            r.a[c] = i + j;
+                            r.b[c] = i + j + q;
+                            ++c;
+                        }
+        return r;
+    }
+    static constexpr Pairs kPairs = make();
+};
+
+template <class K, int N, size_t... I>
+__device__ __forceinline__ void apply_net(K (&k)[N], std::index_sequence<I...>) {
+    (KeyTraits<K>::cas(k[OddEvenNet<N>::kPairs.a[I]], k[OddEvenNet<N>::kPairs.b[I]]), ...);
+}
+
+template <class K, int N>
+__device__ __forceinline__ void register_sort(K (&k)[N]) {
+    if constexpr (OddEvenNet<N>::kCount > 0)
+        apply_net<K, N>(k, std::make_index_sequence<OddEvenNet<N>::kCount>{});
+}
+
+// Merge-path split on shared memory: the number of elements taken from run A
+// among the first `diag` outputs of merge(A, B) when ties take A first.
+template <class K>
+__device__ __forceinline__ int merge_path_smem(const K* s, int a0, int alen, int b0, int blen,
+                                               int diag) {
+    using P = SmemPad<K>;
+    int lo = diag > blen ? diag - blen : 0;
+    int hi = diag < alen ? diag : alen;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        // A[mid] goes first unless B[diag-1-mid] < A[mid]
+        if (!KeyTraits<K>::lt(s[P::idx(b0 + diag - 1 - mid)], s[P::idx(a0 + mid)]))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Serially merge ITEMS outputs from positions (ai in A, bi in B) of two sorted
+// shared-memory runs [a0,a0+alen) and [b0,b0+blen) into registers.
+template <class K, int ITEMS>
+__device__ __forceinline__ void serial_merge_smem(const K* s, int ai, int aend, int bi, int bend,
+                                                  K (&out)[ITEMS]) {
+    using P = SmemPad<K>;
+    using KT = KeyTraits<K>;
+    K ka = ai < aend ? s[P::idx(ai)] : KT::max_key();
+    K kb = bi < bend ? s[P::idx(bi)] : KT::max_key();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool take_b = (bi < bend) && ((ai >= aend) || KT::lt(kb, ka));
+        out[i] = take_b ? kb : ka;
+        if (take_b) {
+            ++bi;
+            if (bi < bend) kb = s[P::idx(bi)];
+        } else {
+            ++ai;
+            if (ai < aend) ka = s[P::idx(ai)];
+        }
+    }
+}
+
+template <class K, int T, int ITEMS>
+struct BlockSorter {
+    static constexpr int kThreads = T;
+    static constexpr int kItems = ITEMS;
+    static constexpr int kCap = T * ITEMS;
+    static constexpr int kSmemElems = SmemPad<K>::elems(kCap);
+    static constexpr size_t kSmemBytes = sizeof(K) * kSmemElems;
+    using P = SmemPad<K>;
+    using KT = KeyTraits<K>;
+
+    // Coalesced (striped) load of m <= kCap keys into shared memory, padding
+    // the tail with the maximum key.
+    __device__ __forceinline__ static void load_striped(const K* __restrict__ src, int m, K* s) {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < kCap; i += T) s[P::idx(i)] = i < m ? src[i] : KT::max_key();
+    }
+    __device__ __forceinline__ static void store_blocked(const K (&k)[ITEMS], K* s) {
+        const int base = threadIdx.x * ITEMS;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) s[P::idx(base + i)] = k[i];
+    }
+    __device__ __forceinline__ static void load_blocked(K (&k)[ITEMS], const K* s) {
+        const int base = threadIdx.x * ITEMS;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) k[i] = s[P::idx(base + i)];
+    }
+    __device__ __forceinline__ static void store_striped(K* __restrict__ dst, int m, const K* s) {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < m; i += T) dst[i] = s[P::idx(i)];
+    }
+
+    // Sort the kCap keys held in registers (blocked arrangement).  On return
+    // the sorted tile sits in shared memory s (padded indexing).  Must be
+    // called by all T threads; s must not be in use.
+    __device__ __forceinline__ static void sort(K (&k)[ITEMS], K* s) {
+        register_sort<K, ITEMS>(k);
+#pragma unroll 1
+        for (int run = ITEMS; run < kCap; run <<= 1) {
+            store_blocked(k, s);
+            __syncthreads();
+            const int out = threadIdx.x * ITEMS;
+            const int pair = out & ~(2 * run - 1);
+            const int diag = out - pair;
+            const int a0 = pair, b0 = pair + run;
+            const int a = merge_path_smem<K>(s, a0, run, b0, run, diag);
+            serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + run, b0 + diag - a, b0 + run, k);
+            __syncthreads();
+        }
+        store_blocked(k, s);
+        __syncthreads();
+    }
+
+    // Whole tile: global src (m keys) -> sorted -> global dst.  src may alias dst.
+    __device__ __forceinline__ static void sort_tile(const K* src, K* dst, int m, K* s) {
+        load_striped(src, m, s);
+        __syncthreads();
+        K k[ITEMS];
+        load_blocked(k, s);
+        __syncthreads();
+        sort(k, s);
+        store_striped(dst, m, s);
+    }
+};
+
+}  // namespace qmsort_b200

@@ -1,0 +1,152 @@
+// common.cuh -- key types, orderings and small device helpers shared by every
+// qmsort-b200 kernel.
+//
+// The sort core works on three UNSIGNED key types whose natural order is the
+// sort order: uint32 (C1/C2 after the order-preserving transform), uint64
+// (C3/C4) and Rec32 = four uint64 words compared lexicographically (C5, the
+// rec32 comparator of SURVEY.md 8(d)).  The reference's comparator `less`
+// (sort.hpp:215-217) is folded into an order-preserving bijection applied on
+// the way in and out (transform.cuh), so one kernel family serves every
+// (dtype, less/greater) pair bit-exactly.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qmsort_b200 {
+
+struct alignas(16) Rec32 {
+    uint64_t w[4];
+};
+
+template <class K>
+struct KeyTraits;
+
+template <>
+struct KeyTraits<uint32_t> {
+    static constexpr int kBytes = 4;
+    __device__ __forceinline__ static uint32_t max_key() { return 0xFFFFFFFFu; }
+    __device__ __forceinline__ static bool lt(uint32_t a, uint32_t b) { return a < b; }
+    __device__ __forceinline__ static bool eq(uint32_t a, uint32_t b) { return a == b; }
+    // compare-and-swap: a <- min, b <- max
+    __device__ __forceinline__ static void cas(uint32_t& a, uint32_t& b) {
+        uint32_t lo = min(a, b), hi = max(a, b);
+        a = lo;
+        b = hi;
+    }
+    __device__ __forceinline__ static uint64_t hash(uint32_t a) { return a; }
+};
+
+template <>
+struct KeyTraits<uint64_t> {
+    static constexpr int kBytes = 8;
+    __device__ __forceinline__ static uint64_t max_key() { return ~0ull; }
+    __device__ __forceinline__ static bool lt(uint64_t a, uint64_t b) { return a < b; }
+    __device__ __forceinline__ static bool eq(uint64_t a, uint64_t b) { return a == b; }
+    __device__ __forceinline__ static void cas(uint64_t& a, uint64_t& b) {
+        bool s = b < a;
+        uint64_t lo = s ? b : a, hi = s ? a : b;
+        a = lo;
+        b = hi;
+    }
+    __device__ __forceinline__ static uint64_t hash(uint64_t a) { return a; }
+};
+
+template <>
+struct KeyTraits<Rec32> {
+    static constexpr int kBytes = 32;
+    __device__ __forceinline__ static Rec32 max_key() {
+        Rec32 r;
+        r.w[0] = r.w[1] = r.w[2] = r.w[3] = ~0ull;
+        return r;
+    }
+    __device__ __forceinline__ static bool lt(const Rec32& a, const Rec32& b) {
+        // lexicographic over (w0,w1,w2,w3) as unsigned 64-bit words
+        if (a.w[0] != b.w[0]) return a.w[0] < b.w[0];
+        if (a.w[1] != b.w[1]) return a.w[1] < b.w[1];
+        if (a.w[2] != b.w[2]) return a.w[2] < b.w[2];
+        return a.w[3] < b.w[3];
+    }
+    __device__ __forceinline__ static bool eq(const Rec32& a, const Rec32& b) {
+        return a.w[0] == b.w[0] && a.w[1] == b.w[1] && a.w[2] == b.w[2] && a.w[3] == b.w[3];
+    }
+    __device__ __forceinline__ static void cas(Rec32& a, Rec32& b) {
+        bool s = lt(b, a);
+        Rec32 lo, hi;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            lo.w[i] = s ? b.w[i] : a.w[i];
+            hi.w[i] = s ? a.w[i] : b.w[i];
+        }
+        a = lo;
+        b = hi;
+    }
+    __device__ __forceinline__ static uint64_t hash(const Rec32& a) {
+        return a.w[0] * 0x9E3779B97F4A7C15ull ^ a.w[1] * 0xBF58476D1CE4E5B9ull ^
+               a.w[2] * 0x94D049BB133111EBull ^ a.w[3];
+    }
+};
+
+// Shared-memory padding: one spare element every 128 bytes so that a thread
+// that owns ITEMS consecutive keys ("blocked" arrangement) can store them
+// without bank conflicts when ITEMS*sizeof(K) is a multiple of 128 bytes.
+template <class K>
+struct SmemPad {
+    static constexpr int kPer = (128 / KeyTraits<K>::kBytes) > 0 ? (128 / KeyTraits<K>::kBytes) : 1;
+    __device__ __forceinline__ static int idx(int i) { return i + i / kPer; }
+    static constexpr int elems(int n) { return n + n / kPer + 1; }
+};
+
+// SplitMix64 finaliser (reference rng.hpp:14-19) -- also used as a hash.
+__host__ __device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+// Block-wide exclusive scan of `n` uint32 counters held in shared memory
+// (in place).  Returns the total.  All threads of the block must call it.
+// `warp_sums` needs blockDim.x/32 entries.
+template <int T>
+__device__ __forceinline__ uint32_t block_exclusive_scan_smem(uint32_t* data, int n,
+                                                              uint32_t* warp_sums) {
+    constexpr int kWarps = T / 32;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (n + T - 1) / T;  // consecutive items per thread
+    const int beg = tid * per;
+    uint32_t local = 0;
+    for (int i = 0; i < per; ++i)
+        if (beg + i < n) local += data[beg + i];
+    // warp inclusive scan
+    uint32_t x = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < kWarps ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < kWarps) warp_sums[lane] = w;  // inclusive warp totals
+    }
+    __syncthreads();
+    uint32_t excl = x - local + (wid > 0 ? warp_sums[wid - 1] : 0);
+    const uint32_t total = warp_sums[kWarps - 1];
+    for (int i = 0; i < per; ++i) {
+        if (beg + i < n) {
+            uint32_t v = data[beg + i];
+            data[beg + i] = excl;
+            excl += v;
+        }
+    }
+    __syncthreads();
+    return total;
+}
+
+}  // namespace qmsort_b200

@@ -1,0 +1,784 @@
+// qmsort_gpu.cu -- host orchestration and the C-ABI (include/qmsort_gpu.h).
+//
+// Maps the reference QuickXsort driver (detail::quickmergesort_impl,
+// sort.hpp:128-201) onto B200 kernels:
+//   reference step                         B200 replacement
+//   pivot (median_of_3 / median_of_sqrt)   K1 sample_kernel: K-1 sampled splitters
+//   block_partition (two sides)            K2-K4 count / plan / scatter (K buckets)
+//   "continue on the other side" loop      level loop over device segment lists
+//   mergesort_with_temp + base case X      K5 block sort of every bucket <= cap
+//   swap_merge recursion (large ranges)    K6/K7 merge-path passes (fallback and
+//                                          algorithm = mergesort)
+// Buffers: the caller's array A and a workspace array B of the same size are
+// used ping-pong.  Every scatter writes each bucket at its FINAL offset, so the
+// two buffers share one coordinate system and the sorted result always ends
+// in A.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/qmsort_gpu.h"
+#include "aux_kernels.cuh"
+#include "blocksort.cuh"
+#include "common.cuh"
+#include "mergepass.cuh"
+#include "samplesort.cuh"
+
+namespace qmsort_b200 {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define QCK(x)                                                                               \
+    do {                                                                                     \
+        cudaError_t e_ = (x);                                                                \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(QMSORT_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+#define QCK_LAUNCH(led)                                                                      \
+    do {                                                                                     \
+        ++(led).launches;                                                                    \
+        cudaError_t e_ = cudaGetLastError();                                                 \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(QMSORT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+#define QTRY(x)                      \
+    do {                             \
+        int r_ = (x);                \
+        if (r_ != QMSORT_OK) return r_; \
+    } while (0)
+
+// Per-key-type tile shapes.  Class c of the block sorter sorts buckets of up to
+// C_cT * C_cI keys with C_cT threads.
+template <class K>
+struct Tune;
+template <>
+struct Tune<uint32_t> {
+    static constexpr int LOGKMAX = 10;
+    static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
+    static constexpr int ST = 512, SI = 16;  // sampler
+    static constexpr int XT = 512, XI = 16;  // scatter tile
+    static constexpr int CT = 512;           // count
+    static constexpr int MT = 512, MI = 16;  // merge pass
+};
+template <>
+struct Tune<uint64_t> {
+    static constexpr int LOGKMAX = 10;
+    static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
+    static constexpr int ST = 512, SI = 16;
+    static constexpr int XT = 512, XI = 8;
+    static constexpr int CT = 512;
+    static constexpr int MT = 512, MI = 16;
+};
+template <>
+struct Tune<Rec32> {
+    static constexpr int LOGKMAX = 8;
+    static constexpr int C0T = 64, C0I = 8, C1T = 256, C1I = 8, C2T = 512, C2I = 8;
+    static constexpr int ST = 512, SI = 8;
+    static constexpr int XT = 256, XI = 8;
+    static constexpr int CT = 256;
+    static constexpr int MT = 512, MI = 8;
+};
+
+struct Ledger {
+    uint64_t alg_bytes = 0;
+    uint32_t launches = 0, syncs = 0, levels = 0, merge_passes = 0;
+};
+
+// Raise the dynamic shared-memory limit of a kernel once per process.
+static cudaError_t allow_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_set<const void*> done;
+    if (bytes <= 48 * 1024) return cudaSuccess;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.count(fn)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.insert(fn);
+    return e;
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct WsLayout {
+    size_t b_off = 0, segs_off[2] = {0, 0}, chunks_off[2] = {0, 0}, cnt_off[2] = {0, 0};
+    size_t tree_off[2] = {0, 0}, sorted_off[2] = {0, 0};
+    size_t hist_off = 0, tasks_off = 0, fills_off = 0, misc_off = 0, total = 0;
+    uint32_t seg_cap = 0, chunk_cap = 0, split_cap = 0, task_cap = 0, fill_cap = 0, hist_cap = 0;
+    uint64_t chunk_elems = 0;
+};
+
+template <class K>
+static WsLayout make_layout(size_t n) {
+    using TU = Tune<K>;
+    constexpr uint64_t cap = (uint64_t)TU::C2T * TU::C2I;
+    constexpr uint64_t target = cap / 2;
+    constexpr uint64_t tile = (uint64_t)TU::XT * TU::XI;
+    WsLayout L;
+    // ~8 chunks per SM on a 148-SM part at level 0
+    uint64_t ch = (n + 1183) / 1184;
+    ch = std::max<uint64_t>(tile, align_up(ch, tile));
+    L.chunk_elems = ch;
+    L.seg_cap = (uint32_t)(n / cap + 2);
+    L.chunk_cap = (uint32_t)(L.seg_cap + n / ch + 2);
+    L.split_cap = (uint32_t)(2 * n / target + 2 * (uint64_t)L.seg_cap + 2 * (1u << TU::LOGKMAX) + 64);
+    L.task_cap = 2 * L.split_cap + 64;
+    L.fill_cap = L.split_cap;
+    L.hist_cap = (uint32_t)(2ull * (1u << TU::LOGKMAX) * (n / ch + 2) + 2ull * L.split_cap);
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        size_t at = o;
+        o = align_up(o + bytes, 256);
+        return at;
+    };
+    L.b_off = take(n * sizeof(K));
+    for (int i = 0; i < 2; ++i) {
+        L.segs_off[i] = take(sizeof(SegDesc) * L.seg_cap);
+        L.chunks_off[i] = take(sizeof(ChunkDesc) * L.chunk_cap);
+        L.cnt_off[i] = take(sizeof(LevelCounters));
+        L.tree_off[i] = take(sizeof(K) * L.split_cap);
+        L.sorted_off[i] = take(sizeof(K) * L.split_cap);
+    }
+    L.hist_off = take(sizeof(uint32_t) * (size_t)L.hist_cap);
+    L.tasks_off = take(sizeof(SortTask) * (size_t)kNumClasses * L.task_cap);
+    L.fills_off = take(sizeof(FillTask) * (size_t)L.fill_cap);
+    L.misc_off = take(4096);
+    L.total = o;
+    return L;
+}
+
+template <class K, int T, int I>
+static int launch_tiles(const K* src, K* dst, uint64_t off, uint64_t len, cudaStream_t st,
+                        Ledger& led) {
+    using BS = BlockSorter<K, T, I>;
+    if (len == 0) return QMSORT_OK;
+    auto fn = blocksort_tiles_kernel<K, T, I>;
+    QCK(allow_smem((const void*)fn, BS::kSmemBytes));
+    const uint64_t tiles = (len + BS::kCap - 1) / BS::kCap;
+    fn<<<(unsigned)tiles, T, BS::kSmemBytes, st>>>(src, dst, off, len);
+    QCK_LAUNCH(led);
+    led.alg_bytes += 2 * len * sizeof(K);
+    return QMSORT_OK;
+}
+
+// Sort [off, off+len) with len <= class-2 capacity: one CTA of the smallest class.
+template <class K>
+static int blocksort_one(const K* src, K* dst, uint64_t off, uint64_t len, cudaStream_t st,
+                         Ledger& led) {
+    using TU = Tune<K>;
+    if (len <= (uint64_t)TU::C0T * TU::C0I) return launch_tiles<K, TU::C0T, TU::C0I>(src, dst, off, len, st, led);
+    if (len <= (uint64_t)TU::C1T * TU::C1I) return launch_tiles<K, TU::C1T, TU::C1I>(src, dst, off, len, st, led);
+    return launch_tiles<K, TU::C2T, TU::C2I>(src, dst, off, len, st, led);
+}
+
+// Block-sort tiles + merge-path passes over [off, off+len); the range currently
+// lives in X (A or B); the result lands in A.
+template <class K>
+static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStream_t st,
+                           Ledger& led) {
+    using TU = Tune<K>;
+    constexpr uint64_t C = (uint64_t)TU::C2T * TU::C2I;
+    constexpr uint64_t MC = (uint64_t)TU::MT * TU::MI;
+    static_assert(MC <= 2 * C, "merge tile must fit in one run pair");
+    if (len <= C) return blocksort_one<K>(X, A, off, len, st, led);
+    const uint64_t tiles = (len + C - 1) / C;
+    const uint32_t passes = ceil_log2_u64(tiles);
+    K* Y = (passes % 2 == 0) ? A : B;
+    QTRY((launch_tiles<K, TU::C2T, TU::C2I>(X, Y, off, len, st, led)));
+    using BS = BlockSorter<K, TU::MT, TU::MI>;
+    auto fn = merge_pass_kernel<K, TU::MT, TU::MI>;
+    QCK(allow_smem((const void*)fn, BS::kSmemBytes));
+    K* s = Y;
+    K* d = (Y == A) ? B : A;
+    for (uint64_t run = C; run < len; run *= 2) {
+        fn<<<(unsigned)((len + MC - 1) / MC), TU::MT, BS::kSmemBytes, st>>>(s + off, d + off, len, run);
+        QCK_LAUNCH(led);
+        led.alg_bytes += 2 * len * sizeof(K);
+        ++led.merge_passes;
+        std::swap(s, d);
+    }
+    if (s != A) return fail(QMSORT_EINTERNAL, "merge passes ended outside the caller buffer");
+    return QMSORT_OK;
+}
+
+template <class K>
+static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
+                      const WsLayout& L, cudaStream_t st, Ledger& led) {
+    using TU = Tune<K>;
+    constexpr uint32_t cap = (uint32_t)TU::C2T * TU::C2I;
+    PlanParams p;
+    p.chunk_elems = L.chunk_elems;
+    p.cap = cap;
+    p.target = cap / 2;
+    p.log_kmax = TU::LOGKMAX;
+    p.class_cap[0] = (uint32_t)TU::C0T * TU::C0I;
+    p.class_cap[1] = (uint32_t)TU::C1T * TU::C1I;
+    p.class_cap[2] = cap;
+    p.task_cap = L.task_cap;
+    p.fill_cap = L.fill_cap;
+    p.dst_is_a = 0;
+
+    LevelBufs lv[2];
+    K* tree[2];
+    K* sorted[2];
+    for (int i = 0; i < 2; ++i) {
+        lv[i].segs = reinterpret_cast<SegDesc*>(ws + L.segs_off[i]);
+        lv[i].chunks = reinterpret_cast<ChunkDesc*>(ws + L.chunks_off[i]);
+        lv[i].cnt = reinterpret_cast<LevelCounters*>(ws + L.cnt_off[i]);
+        lv[i].seg_cap = L.seg_cap;
+        lv[i].chunk_cap = L.chunk_cap;
+        lv[i].split_cap = L.split_cap;
+        lv[i].hist_cap = L.hist_cap;
+        tree[i] = reinterpret_cast<K*>(ws + L.tree_off[i]);
+        sorted[i] = reinterpret_cast<K*>(ws + L.sorted_off[i]);
+    }
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
+    SortTask* tasks = reinterpret_cast<SortTask*>(ws + L.tasks_off);
+    FillTask* fills = reinterpret_cast<FillTask*>(ws + L.fills_off);
+
+    QCK(cudaMemsetAsync(lv[0].cnt, 0, sizeof(LevelCounters), st));
+    init_level_kernel<<<1, 32, 0, st>>>(lv[0], n, p);
+    QCK_LAUNCH(led);
+
+    using BSS = BlockSorter<K, TU::ST, TU::SI>;
+    auto sample_fn = sample_kernel<K, TU::ST, TU::SI>;
+    QCK(allow_smem((const void*)sample_fn, BSS::kSmemBytes));
+    using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
+    auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
+    QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
+    using B0 = BlockSorter<K, TU::C0T, TU::C0I>;
+    using B1 = BlockSorter<K, TU::C1T, TU::C1I>;
+    using B2 = BlockSorter<K, TU::C2T, TU::C2I>;
+    auto bs0 = blocksort_tasks_kernel<K, TU::C0T, TU::C0I>;
+    auto bs1 = blocksort_tasks_kernel<K, TU::C1T, TU::C1I>;
+    auto bs2 = blocksort_tasks_kernel<K, TU::C2T, TU::C2I>;
+    QCK(allow_smem((const void*)bs0, B0::kSmemBytes));
+    QCK(allow_smem((const void*)bs1, B1::kSmemBytes));
+    QCK(allow_smem((const void*)bs2, B2::kSmemBytes));
+
+    uint32_t nsegs = 1;
+    uint32_t nchunks = (uint32_t)((n + L.chunk_elems - 1) / L.chunk_elems);
+    int cur = 0;
+    K* src = A;
+    K* dst = B;
+    const int max_levels = cfg.max_levels > 0 ? cfg.max_levels : 8;
+    for (int level = 0; nsegs > 0; ++level) {
+        const int nxt = cur ^ 1;
+        if (level >= max_levels) {
+            // K8 fallback: the remaining oversized buckets are merge-sorted.
+            std::vector<SegDesc> h(nsegs);
+            QCK(cudaMemcpyAsync(h.data(), lv[cur].segs, sizeof(SegDesc) * nsegs,
+                                cudaMemcpyDeviceToHost, st));
+            QCK(cudaStreamSynchronize(st));
+            ++led.syncs;
+            for (const SegDesc& d : h) QTRY(mergesort_range<K>(src, A, B, d.off, d.len, st, led));
+            break;
+        }
+        p.dst_is_a = (dst == A) ? 1 : 0;
+        const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
+        sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur], sorted[cur], seed);
+        QCK_LAUNCH(led);
+        count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
+            lv[cur].segs, lv[cur].chunks, src, tree[cur], sorted[cur], hist);
+        QCK_LAUNCH(led);
+        QCK(cudaMemsetAsync(lv[nxt].cnt, 0, sizeof(LevelCounters), st));
+        plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(lv[cur].segs, hist, lv[nxt], p,
+                                                                 tasks, fills, lv[cur].cnt);
+        QCK_LAUNCH(led);
+        scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(lv[cur].segs, lv[cur].chunks, src, dst,
+                                                        tree[cur], sorted[cur], hist);
+        QCK_LAUNCH(led);
+        LevelCounters hc[2];
+        QCK(cudaMemcpyAsync(&hc[0], lv[cur].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
+        QCK(cudaMemcpyAsync(&hc[1], lv[nxt].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
+        QCK(cudaStreamSynchronize(st));
+        ++led.syncs;
+        if (hc[0].overflow || hc[1].overflow)
+            return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
+        ++led.levels;
+        led.alg_bytes += 3ull * hc[0].nkeys * sizeof(K);  // count (1) + scatter (2)
+        const uint32_t nt[3] = {hc[0].ntasks[0], hc[0].ntasks[1], hc[0].ntasks[2]};
+        if (nt[0]) {
+            bs0<<<nt[0], TU::C0T, B0::kSmemBytes, st>>>(tasks, dst, A);
+            QCK_LAUNCH(led);
+        }
+        if (nt[1]) {
+            bs1<<<nt[1], TU::C1T, B1::kSmemBytes, st>>>(tasks + L.task_cap, dst, A);
+            QCK_LAUNCH(led);
+        }
+        if (nt[2]) {
+            bs2<<<nt[2], TU::C2T, B2::kSmemBytes, st>>>(tasks + 2 * (size_t)L.task_cap, dst, A);
+            QCK_LAUNCH(led);
+        }
+        led.alg_bytes += 2ull * hc[0].task_keys * sizeof(K);
+        if (hc[0].nfill) {
+            fill_kernel<K><<<1184, 256, 0, st>>>(fills, hc[0].nfill, lv[cur].segs, sorted[cur], A);
+            QCK_LAUNCH(led);
+            led.alg_bytes += hc[0].fill_keys * sizeof(K);
+        }
+        nsegs = hc[1].nsegs;
+        nchunks = hc[1].nchunks;
+        cur = nxt;
+        std::swap(src, dst);
+    }
+    return QMSORT_OK;
+}
+
+template <class K>
+static int sort_core(K* A, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
+                     const WsLayout& L, cudaStream_t st, Ledger& led) {
+    using TU = Tune<K>;
+    constexpr uint64_t cap = (uint64_t)TU::C2T * TU::C2I;
+    if (n <= 1) return QMSORT_OK;
+    K* B = reinterpret_cast<K*>(ws + L.b_off);
+    if (n <= cap) return blocksort_one<K>(A, A, 0, n, st, led);
+    if (cfg.algorithm == 1) return mergesort_range<K>(A, A, B, 0, n, st, led);
+    return samplesort<K>(A, B, n, cfg, ws, L, st, led);
+}
+
+static int core_dtype(int dt) {
+    if (dt == QMSORT_DT_I32) return QMSORT_DT_U32;
+    if (dt == QMSORT_DT_F64) return QMSORT_DT_U64;
+    return dt;
+}
+
+static size_t dtype_size(int dt) {
+    switch (dt) {
+        case QMSORT_DT_I32:
+        case QMSORT_DT_U32: return 4;
+        case QMSORT_DT_U64:
+        case QMSORT_DT_F64: return 8;
+        case QMSORT_DT_REC32: return 32;
+    }
+    return 0;
+}
+
+static size_t ws_bytes_for(int dt, size_t n) {
+    switch (core_dtype(dt)) {
+        case QMSORT_DT_U32: return make_layout<uint32_t>(n).total;
+        case QMSORT_DT_U64: return make_layout<uint64_t>(n).total;
+        case QMSORT_DT_REC32: return make_layout<Rec32>(n).total;
+    }
+    return 0;
+}
+
+// Launch the forward / inverse order-preserving transform.
+static int run_transform(int dt, int cmp, void* d, size_t n, int inverse, cudaStream_t st,
+                         Ledger& led) {
+    int mode = kXfNone;
+    bool wide = false;
+    size_t words = n;
+    switch (dt) {
+        case QMSORT_DT_I32: mode = cmp ? kXfI32Greater : kXfI32Less; break;
+        case QMSORT_DT_U32: mode = cmp ? kXfU32Greater : kXfNone; break;
+        case QMSORT_DT_U64: mode = cmp ? kXfU64Greater : kXfNone; wide = true; break;
+        case QMSORT_DT_F64: mode = cmp ? kXfF64Greater : kXfF64Less; wide = true; break;
+        case QMSORT_DT_REC32: mode = cmp ? kXfU64Greater : kXfNone; wide = true; words = 4 * n; break;
+    }
+    if (mode == kXfNone || n == 0) return QMSORT_OK;
+    const unsigned grid = (unsigned)std::min<size_t>((words + 255) / 256, 148 * 16);
+    if (wide)
+        transform64_kernel<<<grid, 256, 0, st>>>(static_cast<uint64_t*>(d), words, mode, inverse);
+    else
+        transform32_kernel<<<grid, 256, 0, st>>>(static_cast<uint32_t*>(d), words, mode);
+    QCK_LAUNCH(led);
+    led.alg_bytes += 2 * n * dtype_size(dt);
+    return QMSORT_OK;
+}
+
+static int validate(int dt, int cmp, size_t n, const void* p) {
+    if (dtype_size(dt) == 0) return fail(QMSORT_EINVAL, "unknown dtype");
+    if (cmp != QMSORT_LESS && cmp != QMSORT_GREATER) return fail(QMSORT_EINVAL, "unknown comparator");
+    if (n >= (1ull << 32)) return fail(QMSORT_EINVAL, "n must be < 2^32");
+    if (n > 0 && p == nullptr) return fail(QMSORT_EINVAL, "null data pointer");
+    return QMSORT_OK;
+}
+
+static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_config* cfgp,
+                       void* wsp, size_t ws_bytes, qmsort_gpu_metrics* m, cudaStream_t st) {
+    QTRY(validate(dt, cmp, n, d));
+    qmsort_gpu_config cfg;
+    if (cfgp) cfg = *cfgp;
+    else qmsort_gpu_config_init(&cfg, 0);
+    const size_t need = ws_bytes_for(dt, n);
+    void* ws = wsp;
+    bool own = false;
+    if (ws == nullptr && n > 1) {
+        QCK(cudaMallocAsync(&ws, need, st));
+        own = true;
+    } else if (n > 1 && ws_bytes < need) {
+        return fail(QMSORT_ENOWS, "workspace too small: need " + std::to_string(need) + " bytes");
+    }
+    Ledger led;
+    cudaEvent_t e0, e1;
+    QCK(cudaEventCreate(&e0));
+    QCK(cudaEventCreate(&e1));
+    QCK(cudaEventRecord(e0, st));
+    int rc = run_transform(dt, cmp, d, n, 0, st, led);
+    if (rc == QMSORT_OK) {
+        unsigned char* w = static_cast<unsigned char*>(ws);
+        switch (core_dtype(dt)) {
+            case QMSORT_DT_U32:
+                rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w, make_layout<uint32_t>(n), st, led);
+                break;
+            case QMSORT_DT_U64:
+                rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w, make_layout<uint64_t>(n), st, led);
+                break;
+            case QMSORT_DT_REC32:
+                rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n), st, led);
+                break;
+        }
+    }
+    if (rc == QMSORT_OK) rc = run_transform(dt, cmp, d, n, 1, st, led);
+    cudaEventRecord(e1, st);
+    cudaError_t se = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (own) cudaFreeAsync(ws, st);
+    if (rc != QMSORT_OK) return rc;
+    if (se != cudaSuccess) return fail(QMSORT_ECUDA, std::string("sort: ") + cudaGetErrorString(se));
+    if (m) {
+        std::memset(m, 0, sizeof(*m));
+        m->elapsed_ns = (uint64_t)((double)ms * 1e6);
+        m->max_depth = led.levels;
+        m->alg_bytes = led.alg_bytes;
+        m->levels = led.levels;
+        m->merge_passes = led.merge_passes;
+        m->kernel_launches = led.launches;
+        m->host_syncs = led.syncs + 1;
+    }
+    g_err.clear();
+    return QMSORT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sharded building blocks
+// ---------------------------------------------------------------------------
+template <class K>
+__global__ void gather_sample_kernel(const K* __restrict__ src, uint64_t n, uint64_t s,
+                                     uint64_t seed, K* __restrict__ out) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = sm_mix(seed + (i + 1) * kGamma);
+        out[i] = src[__umul64hi(h, n)];
+    }
+}
+
+// Build the Eytzinger tree of caller-given sorted splitters into one segment.
+template <class K>
+__global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nsplit, uint32_t logk,
+                                       SegDesc* seg, K* tree, K* sorted, uint64_t n,
+                                       uint32_t nchunks, ChunkDesc* chunks, uint64_t chunk_elems) {
+    const uint32_t K_ = 1u << logk;
+    for (uint32_t i = threadIdx.x; i < K_; i += blockDim.x) sorted[i] = i < nsplit ? spl[i] : KeyTraits<K>::max_key();
+    for (uint32_t t = threadIdx.x + 1; t < K_; t += blockDim.x) {
+        const uint32_t depth = 31 - __clz(t);
+        const uint32_t rank = ((2 * (t - (1u << depth)) + 1) << (logk - 1 - depth)) - 1;
+        tree[t] = rank < nsplit ? spl[rank] : KeyTraits<K>::max_key();
+    }
+    for (uint32_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
+        ChunkDesc cd;
+        cd.seg = 0;
+        cd.pad = 0;
+        cd.begin = (uint64_t)c * chunk_elems;
+        cd.end = min(n, cd.begin + chunk_elems);
+        chunks[c] = cd;
+    }
+    if (threadIdx.x == 0) {
+        SegDesc d;
+        d.off = 0;
+        d.len = n;
+        d.chunk_begin = 0;
+        d.nchunks = nchunks;
+        d.logk = logk;
+        d.m = nsplit;
+        d.eq = 0;
+        d.sp = 0;
+        d.hist_base = 0;
+        d.pad = 0;
+        *seg = d;
+    }
+}
+
+// Offsets only (no children): per-chunk offsets in place and bucket counts.
+template <int T, int LOG_KMAX>
+__global__ void __launch_bounds__(T) offsets_kernel(const SegDesc* __restrict__ segs,
+                                                    uint32_t* __restrict__ chunk_hist,
+                                                    uint32_t nsplit, uint64_t* counts) {
+    constexpr int NB = 2 << LOG_KMAX;
+    __shared__ uint32_t start[NB];
+    __shared__ uint32_t warp_sums[32];
+    const SegDesc d = segs[0];
+    const uint32_t nb = 2u << d.logk;
+    for (uint32_t b = threadIdx.x; b < nb; b += T) {
+        uint32_t sum = 0;
+        for (uint32_t c = 0; c < d.nchunks; ++c) sum += chunk_hist[(size_t)c * nb + b];
+        start[b] = sum;
+        if ((b & 1) == 0 && (b >> 1) <= nsplit) counts[b >> 1] = sum;
+    }
+    __syncthreads();
+    block_exclusive_scan_smem<T>(start, (int)nb, warp_sums);
+    for (uint32_t b = threadIdx.x; b < nb; b += T) {
+        uint32_t run = start[b];
+        for (uint32_t c = 0; c < d.nchunks; ++c) {
+            const uint32_t v = chunk_hist[(size_t)c * nb + b];
+            chunk_hist[(size_t)c * nb + b] = run;
+            run += v;
+        }
+    }
+}
+
+template <class K>
+static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit, K* out,
+                           uint64_t* counts, unsigned char* ws, const WsLayout& L, cudaStream_t st,
+                           Ledger& led) {
+    using TU = Tune<K>;
+    const uint32_t logk = std::max<uint32_t>(1, ceil_log2_u64((uint64_t)nsplit + 1));
+    if (logk > (uint32_t)TU::LOGKMAX) return fail(QMSORT_EINVAL, "too many splitters");
+    SegDesc* seg = reinterpret_cast<SegDesc*>(ws + L.segs_off[0]);
+    ChunkDesc* chunks = reinterpret_cast<ChunkDesc*>(ws + L.chunks_off[0]);
+    K* tree = reinterpret_cast<K*>(ws + L.tree_off[0]);
+    K* sorted = reinterpret_cast<K*>(ws + L.sorted_off[0]);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
+    const uint32_t nchunks = (uint32_t)std::max<uint64_t>(1, (n + L.chunk_elems - 1) / L.chunk_elems);
+    given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, n, nchunks,
+                                                 chunks, L.chunk_elems);
+    QCK_LAUNCH(led);
+    QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
+    if (n == 0) return QMSORT_OK;
+    count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(seg, chunks, in, tree, sorted, hist);
+    QCK_LAUNCH(led);
+    offsets_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts);
+    QCK_LAUNCH(led);
+    using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
+    auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
+    QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
+    scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(seg, chunks, in, out, tree, sorted, hist);
+    QCK_LAUNCH(led);
+    led.alg_bytes += 3 * n * sizeof(K);
+    return QMSORT_OK;
+}
+
+}  // namespace qmsort_b200
+
+using namespace qmsort_b200;
+
+extern "C" {
+
+void qmsort_gpu_config_init(qmsort_gpu_config* c, int variant) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    // SortConfig defaults (sort.hpp:25-34, merge.hpp:26-31)
+    c->variant = 0;
+    c->pivot = 0;
+    c->base_case_kind = 1;
+    c->base_case_size_threshold = 10;
+    c->base_case_use_levels = 0;
+    c->beta = 0.5;
+    c->delta = 1.0 / 16.0;
+    c->side = 1;
+    c->three_way = 0;
+    c->block = 128;
+    c->algorithm = 0;
+    c->seed = 42;
+    c->max_levels = 8;
+    switch (variant) {
+        case 1:  // qmqs (sort.hpp:41-48)
+            c->variant = 1;
+            c->base_case_kind = 2;
+            c->base_case_size_threshold = 16;
+            c->base_case_use_levels = 1;
+            break;
+        case 2:  // momqms (sort.hpp:52-57)
+            c->variant = 2;
+            c->pivot = 2;
+            break;
+        case 3:  // hqms (sort.hpp:61-66)
+            c->variant = 3;
+            c->pivot = 3;
+            break;
+        default: break;
+    }
+}
+
+size_t qmsort_gpu_dtype_size(int dtype) { return dtype_size(dtype); }
+
+int qmsort_gpu_core_dtype(int dtype) { return core_dtype(dtype); }
+
+size_t qmsort_gpu_workspace_bytes(int dtype, size_t n, const qmsort_gpu_config*) {
+    if (dtype_size(dtype) == 0) return 0;
+    return ws_bytes_for(dtype, n);
+}
+
+int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu_config* cfg,
+                    void* d_ws, size_t ws_bytes, qmsort_gpu_metrics* metrics, void* stream) {
+    return sort_device(dtype, cmp, d_data, n, cfg, d_ws, ws_bytes, metrics,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
+                         qmsort_gpu_metrics* metrics) {
+    QTRY(validate(dtype, cmp, n, h_data));
+    if (n <= 1) {
+        if (metrics) std::memset(metrics, 0, sizeof(*metrics));
+        return QMSORT_OK;
+    }
+    // Per-thread cached device arena (grow-only) and stream.
+    struct Arena {
+        void* buf = nullptr;
+        size_t bytes = 0;
+        cudaStream_t st = nullptr;
+        ~Arena() {
+            if (buf) cudaFree(buf);
+            if (st) cudaStreamDestroy(st);
+        }
+    };
+    static thread_local Arena ar;
+    const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
+    const size_t need = data_bytes + ws_bytes_for(dtype, n);
+    if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
+    if (ar.bytes < need) {
+        if (ar.buf) QCK(cudaFree(ar.buf));
+        ar.buf = nullptr;
+        ar.bytes = 0;
+        QCK(cudaMalloc(&ar.buf, need));
+        ar.bytes = need;
+    }
+    unsigned char* base = static_cast<unsigned char*>(ar.buf);
+    QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, ar.st));
+    int rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, need - data_bytes, metrics, ar.st);
+    if (rc != QMSORT_OK) return rc;
+    QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, ar.st));
+    QCK(cudaStreamSynchronize(ar.st));
+    return QMSORT_OK;
+}
+
+const char* qmsort_gpu_last_error(void) { return g_err.c_str(); }
+
+int qmsort_gpu_transform(int dtype, int cmp, void* d_data, size_t n, int inverse, void* stream) {
+    QTRY(validate(dtype, cmp, n, d_data));
+    Ledger led;
+    QTRY(run_transform(dtype, cmp, d_data, n, inverse, static_cast<cudaStream_t>(stream), led));
+    return QMSORT_OK;
+}
+
+int qmsort_gpu_sample(int core, const void* d, size_t n, size_t s, uint64_t seed, void* out,
+                      void* stream) {
+    QTRY(validate(core, 0, n, d));
+    if (core != core_dtype(core)) return fail(QMSORT_EINVAL, "sample expects a core dtype");
+    if (n == 0 || s == 0) return QMSORT_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)std::min<size_t>((s + 255) / 256, 1184);
+    switch (core) {
+        case QMSORT_DT_U32: gather_sample_kernel<uint32_t><<<grid, 256, 0, st>>>((const uint32_t*)d, n, s, seed, (uint32_t*)out); break;
+        case QMSORT_DT_U64: gather_sample_kernel<uint64_t><<<grid, 256, 0, st>>>((const uint64_t*)d, n, s, seed, (uint64_t*)out); break;
+        case QMSORT_DT_REC32: gather_sample_kernel<Rec32><<<grid, 256, 0, st>>>((const Rec32*)d, n, s, seed, (Rec32*)out); break;
+    }
+    QCK(cudaGetLastError());
+    return QMSORT_OK;
+}
+
+size_t qmsort_gpu_partition_workspace_bytes(int core, size_t n) {
+    if (dtype_size(core) == 0) return 0;
+    return ws_bytes_for(core, n);
+}
+
+int qmsort_gpu_partition(int core, const void* d_in, size_t n, const void* spl, uint32_t nsplit,
+                         void* d_out, uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream) {
+    QTRY(validate(core, 0, n, d_in));
+    if (core != core_dtype(core)) return fail(QMSORT_EINVAL, "partition expects a core dtype");
+    if (nsplit > 1023) return fail(QMSORT_EINVAL, "nsplit must be <= 1023");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t need = ws_bytes_for(core, std::max<size_t>(n, 2));
+    void* ws = d_ws;
+    bool own = false;
+    if (!ws) {
+        QCK(cudaMallocAsync(&ws, need, st));
+        own = true;
+    } else if (ws_bytes < need) {
+        return fail(QMSORT_ENOWS, "partition workspace too small");
+    }
+    Ledger led;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    int rc = QMSORT_OK;
+    const size_t nn = std::max<size_t>(n, 2);
+    switch (core) {
+        case QMSORT_DT_U32:
+            rc = partition_given<uint32_t>((const uint32_t*)d_in, n, (const uint32_t*)spl, nsplit,
+                                           (uint32_t*)d_out, d_counts, w, make_layout<uint32_t>(nn), st, led);
+            break;
+        case QMSORT_DT_U64:
+            rc = partition_given<uint64_t>((const uint64_t*)d_in, n, (const uint64_t*)spl, nsplit,
+                                           (uint64_t*)d_out, d_counts, w, make_layout<uint64_t>(nn), st, led);
+            break;
+        case QMSORT_DT_REC32:
+            if (nsplit > 255) rc = fail(QMSORT_EINVAL, "rec32 partition supports <= 255 splitters");
+            else
+                rc = partition_given<Rec32>((const Rec32*)d_in, n, (const Rec32*)spl, nsplit,
+                                            (Rec32*)d_out, d_counts, w, make_layout<Rec32>(nn), st, led);
+            break;
+    }
+    if (own) cudaFreeAsync(ws, st);
+    return rc;
+}
+
+int qmsort_gpu_generate(int kind, void* d_out, size_t n, uint64_t seed, uint64_t start,
+                        uint64_t total, void* stream) {
+    if (n == 0) return QMSORT_OK;
+    if (!d_out) return fail(QMSORT_EINVAL, "null output");
+    if (!(kind == 0 || kind == 1 || kind == 2 || (kind >= 10 && kind <= 14)))
+        return fail(QMSORT_EINVAL, "unknown generator kind");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const unsigned grid = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+    generate_kernel<<<grid, 256, 0, st>>>(d_out, n, seed, start, kind, total ? total : n);
+    QCK(cudaGetLastError());
+    return QMSORT_OK;
+}
+
+int qmsort_gpu_check(int dtype, int cmp, const void* d, size_t n, int check_order, uint64_t* out3,
+                     void* stream) {
+    QTRY(validate(dtype, cmp, n, d));
+    if (!out3) return fail(QMSORT_EINVAL, "null out3");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    unsigned long long* res = nullptr;
+    QCK(cudaMallocAsync(&res, 3 * sizeof(unsigned long long), st));
+    QCK(cudaMemsetAsync(res, 0, 3 * sizeof(unsigned long long), st));
+    const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8));
+    if (n > 0) {
+#define QCHK(T)                                                                             \
+    (cmp ? check_kernel<T, true><<<grid, 256, 0, st>>>((const T*)d, n, res, check_order)    \
+         : check_kernel<T, false><<<grid, 256, 0, st>>>((const T*)d, n, res, check_order))
+        switch (dtype) {
+            case QMSORT_DT_I32: QCHK(int32_t); break;
+            case QMSORT_DT_U32: QCHK(uint32_t); break;
+            case QMSORT_DT_U64: QCHK(uint64_t); break;
+            case QMSORT_DT_F64: QCHK(double); break;
+            case QMSORT_DT_REC32: QCHK(Rec32); break;
+        }
+#undef QCHK
+        QCK(cudaGetLastError());
+    }
+    unsigned long long h[3];
+    QCK(cudaMemcpyAsync(h, res, sizeof(h), cudaMemcpyDeviceToHost, st));
+    QCK(cudaFreeAsync(res, st));
+    QCK(cudaStreamSynchronize(st));
+    out3[0] = h[0];
+    out3[1] = h[1];
+    out3[2] = h[2];
+    return QMSORT_OK;
+}
+
+const char* qmsort_gpu_version(void) { return "qmsort-b200 0.1 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+"""GPU parity: the B200 sort through the C-ABI vs the CPU QuickMergesort oracle.
+
+Mirrors the reference's own suites (test_sort.cpp:37-77, 356-362;
+acceptance.cpp:86-114): every variant x distribution x size must give output
+byte-identical to the oracle on the same seeded input.  Bit-exact (integer /
+record / IEEE bit patterns): there is no tolerance.
+"""
+import numpy as np
+import pytest
+
+import paper_1804_10062_b200 as q
+from oracle_lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DTYPES = [DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32]
+
+
+def rand_input(dt, n, seed, dist="uniform"):
+    rng = np.random.default_rng(seed)
+    shape = (n, 4) if dt == DT_REC32 else (n,)
+    if dist == "uniform":
+        raw = rng.integers(0, 2**63, size=shape, dtype=np.uint64) * 2 + rng.integers(0, 2, size=shape, dtype=np.uint64)
+    elif dist == "fewdistinct":
+        raw = (rng.integers(0, 7, size=shape, dtype=np.uint64) + 1) * np.uint64(0x0101010101)
+    elif dist == "allequal":
+        raw = np.full(shape, 0x123456789, dtype=np.uint64)
+    elif dist == "sorted":
+        raw = np.arange(n, dtype=np.uint64) * np.uint64(3)
+        if dt == DT_REC32:
+            raw = np.repeat(raw[:, None], 4, axis=1)
+    elif dist == "reverse":
+        raw = (np.arange(n, dtype=np.uint64)[::-1] * np.uint64(3)).copy()
+        if dt == DT_REC32:
+            raw = np.repeat(raw[:, None], 4, axis=1)
+    elif dist == "organpipe":
+        i = np.arange(n, dtype=np.uint64)
+        raw = np.minimum(i + 1, np.uint64(n) - i)
+        if dt == DT_REC32:
+            raw = np.repeat(raw[:, None], 4, axis=1)
+    else:
+        raise ValueError(dist)
+    if dt == DT_I32:
+        return (raw & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.int32)
+    if dt == DT_U32:
+        return (raw >> np.uint64(7) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    if dt == DT_U64:
+        return raw.astype(np.uint64)
+    if dt == DT_F64:
+        # finite doubles, no NaN / -0.0: scale signed integers
+        s = (raw >> np.uint64(11)).astype(np.int64) - (1 << 51)
+        x = s.astype(np.float64) * 1.25e-3
+        x[x == 0] = 0.0
+        return x
+    if dt == DT_REC32:
+        r = raw.astype(np.uint64).copy()
+        if dist == "uniform":
+            r[:, 0] >>= np.uint64(52)  # word 0 from 2^12 values, as config 5
+        return r
+    raise ValueError(dt)
+
+
+def gpu_sort(a, cfg=None, less="less"):
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    m = q.sort(t, cfg or q.qms(), less)
+    torch.cuda.synchronize()
+    return t.cpu().numpy(), m
+
+
+SIZES = [0, 1, 2, 3, 9, 10, 100, 511, 512, 513, 1000, 1024, 2047, 4096, 4097, 8191, 8192,
+         8193, 20000, 65536, 100003, 1 << 20]
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("n", SIZES)
+def test_uniform_sizes_samplesort(oracle, dt, n):
+    a = rand_input(dt, n, seed=n + 17 * dt)
+    got, _ = gpu_sort(a)
+    np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("n", [8193, 100003, 1 << 19])
+def test_uniform_sizes_mergesort(oracle, dt, n):
+    a = rand_input(dt, n, seed=n + 3 * dt)
+    cfg = q.qms()
+    cfg.algorithm = q.Algorithm.mergesort
+    got, m = gpu_sort(a, cfg)
+    np.testing.assert_array_equal(got, oracle.sort(dt, a))
+    assert m.merge_passes >= 1
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("dist", ["fewdistinct", "allequal", "sorted", "reverse", "organpipe"])
+@pytest.mark.parametrize("n", [5000, 300001])
+def test_distributions(oracle, dt, dist, n):
+    a = rand_input(dt, n, seed=5, dist=dist)
+    got, _ = gpu_sort(a)
+    np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+@pytest.mark.parametrize("dt", DTYPES)
+@pytest.mark.parametrize("n", [7, 5000, 200000])
+def test_descending_greater(oracle, dt, n):
+    """std::greater comparator (test_sort.cpp:356-362)."""
+    a = rand_input(dt, n, seed=99)
+    got, _ = gpu_sort(a, less="greater")
+    np.testing.assert_array_equal(got, oracle.sort(dt, a, greater=True))
+
+
+@pytest.mark.parametrize("preset", [q.qms, q.qmqs, q.momqms, q.hqms])
+def test_fig1_all_presets(preset):
+    """Worked 12-element example (test_sort.cpp:24,37-45) under every variant."""
+    a = np.array([7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8], dtype=np.int32)
+    got, _ = gpu_sort(a, preset())
+    np.testing.assert_array_equal(got, np.arange(12, dtype=np.int32))
+
+
+def test_host_dropin_matches(oracle):
+    """qmsort_gpu_sort_host: the host-array drop-in (sort.hpp:215-226)."""
+    a = rand_input(DT_U32, 300000, seed=3)
+    b = a.copy()
+    m = q.sort(b)  # numpy -> host path
+    np.testing.assert_array_equal(b, oracle.sort(DT_U32, a))
+    assert m.elapsed_ns > 0
+
+
+def test_fuzz_all_variants(oracle):
+    """Fuzz over random n < 3000 and the six reference distributions
+    (test_sort.cpp:59-77)."""
+    rng = np.random.default_rng(1001)
+    for trial in range(60):
+        n = int(rng.integers(0, 3000))
+        dt = DTYPES[trial % 5]
+        dist = ["uniform", "sorted", "reverse", "organpipe", "fewdistinct", "allequal"][trial % 6]
+        a = rand_input(dt, n, seed=trial, dist=dist)
+        for preset in (q.qms, q.qmqs, q.momqms, q.hqms):
+            got, _ = gpu_sort(a, preset())
+            np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+@pytest.mark.parametrize("cfgname", ["i32_perm", "u32", "u64", "f64_sorted", "f64_reverse",
+                                     "f64_distinct16", "f64_gauss", "f64_organ", "rec32"])
+def test_config_shapes_reduced(oracle, cfgname):
+    """The five BASELINE configs at 2^20 elements, seeded recipes of SURVEY.md 8(d)."""
+    n = 1 << 20
+    a = oracle.gen(cfgname, n, seed=42)
+    dt = {"i32_perm": DT_I32, "u32": DT_U32, "u64": DT_U64, "rec32": DT_REC32}.get(cfgname, DT_F64)
+    got, _ = gpu_sort(a)
+    if cfgname == "i32_perm":
+        np.testing.assert_array_equal(got, np.arange(n, dtype=np.int32))  # closed form
+    np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+@pytest.mark.parametrize("kind,dt,cfgname", [(q.GEN_U32, DT_U32, "u32"), (q.GEN_U64, DT_U64, "u64"),
+                                             (q.GEN_REC32, DT_REC32, "rec32"),
+                                             (q.GEN_F64_DISTINCT16, DT_F64, "f64_distinct16"),
+                                             (q.GEN_F64_ORGAN, DT_F64, "f64_organ")])
+def test_device_generators_match_host(oracle, kind, dt, cfgname):
+    n = 100000
+    shape = (n, 4) if dt == DT_REC32 else (n,)
+    tdt = {DT_U32: torch.uint32, DT_U64: torch.uint64, DT_REC32: torch.uint64, DT_F64: torch.float64}[dt]
+    t = torch.empty(shape, dtype=tdt, device="cuda")
+    q.generate(kind, t, seed=7, start=0, total=n)
+    np.testing.assert_array_equal(t.cpu().numpy(), oracle.gen(cfgname, n, seed=7))
