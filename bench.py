@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""bench.py -- the driver's benchmark contract for qmsort-b200.
+
+Workload (BASELINE.json metric, config 2): sort n = 2^28 uint32 keys drawn
+i.i.d. uniform by the seeded SplitMix64 recipe, Median-of-3
+preset qms(), one sort per step, keys resident in HBM.  Output:
+one JSON line with the metric "sorted Gkeys/s at n=2^28 uint32" plus the
+roofline of the dominant kernel, the pass-ledger roofline of the whole sort,
+the reference CPU QuickMergesort timed on the host cores (cpu_baseline) and
+the end-to-end number through the host-array drop-in call (e2e).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+With N > 1 (torchrun, one rank per GPU) every rank holds 2^28 keys and the
+ranks run the distributed samplesort (sharded.py): global splitters, one NCCL
+all-to-all, local sorts -- weak scaling, whole-job keys/s.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted Gkeys/s at n=2^28 uint32 (1-8 B200); achieved HBM GB/s vs roofline"
+UNIT = "Gkeys/s"
+N_DEFAULT = 1 << 28
+SEED = 42
+CPU_SAMPLE = 1 << 24  # bounded CPU sample (~3 s per qms() sort on one core)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="keys per GPU")
+    ap.add_argument("--algorithm", choices=["samplesort", "mergesort"], default="samplesort")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="profiling runs: skip extras")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 6 and parts[0].isdigit():
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(int(r[0]) for r in rows),
+                "sm_max_mhz": max(int(r[1]) for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs: the reference QuickMergesort (oracle/_ref) or the C restatement
+# ---------------------------------------------------------------------------
+def cpu_lib():
+    ref = os.path.join(ROOT, "oracle", "_ref", "libqmsref.so")
+    if os.path.exists(ref):
+        lib = ctypes.CDLL(ref)
+        lib.qmsref_sort.argtypes = [ctypes.c_int] * 5 + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        return "reference", lambda a, std=False: lib.qmsref_sort(
+            1, 0, 0, 0, int(std), a.ctypes.data_as(ctypes.c_void_p), a.shape[0], None)
+    port = os.path.join(ROOT, "oracle", "liboracle.so")
+    if not os.path.exists(port):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
+    lib = ctypes.CDLL(port)
+    lib.qmso_sort.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
+    return "port", lambda a, std=False: lib.qmso_sort(1, 0, 0, a.ctypes.data_as(ctypes.c_void_p), a.shape[0])
+
+
+def host_input(n: int):
+    """C2 recipe on the host: u32[i] = SplitMix64(seed)_i >> 32 (numpy, vectorised)."""
+    import numpy as np
+    j = np.arange(1, n + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = np.uint64(SEED) + j * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return (z >> np.uint64(32)).astype(np.uint32)
+
+
+def cpu_baseline(reps: int = 3) -> dict:
+    kind, fn = cpu_lib()
+    base = host_input(CPU_SAMPLE)
+    times, std_times = [], []
+    for _ in range(reps):
+        a = base.copy()
+        t = time.perf_counter()
+        fn(a)
+        times.append(time.perf_counter() - t)
+    if kind == "reference":
+        a = base.copy()
+        t = time.perf_counter()
+        fn(a, std=True)
+        std_times.append(time.perf_counter() - t)
+    best = min(times)
+    out = {"value": CPU_SAMPLE / best / 1e9, "unit": UNIT, "cores": 1, "kind": kind,
+           "sample": f"qmsort::sort(qms(), std::less) on the first 2^24 keys of the C2 input, "
+                     f"best of {reps}, 1 of {os.cpu_count()} host cores (single-threaded reference)"}
+    if std_times:
+        out["std_sort_value"] = CPU_SAMPLE / min(std_times) / 1e9
+    return out
+
+
+def run_reference(args) -> None:
+    """--impl reference: the reference CPU QuickMergesort on the host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    kind, fn = cpu_lib()
+    base = host_input(CPU_SAMPLE)
+    for _ in range(args.warmup):
+        a = base.copy()
+        fn(a)
+    times = []
+    for _ in range(args.steps):
+        a = base.copy()
+        t = time.perf_counter()
+        fn(a)
+        times.append(time.perf_counter() - t)
+    ms = statistics.mean(times) * 1e3
+    value = CPU_SAMPLE / (ms / 1e3) / 1e9
+    sample = (f"each step: qmsort::sort(qms()) of the first 2^24 keys of the C2 input "
+              f"(bounded sample of the 2^28 workload); single-threaded reference, 1 of "
+              f"{os.cpu_count()} host cores")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe)",
+            "config": {"workload": "C2 uint32 uniform, CPU sample 2^24 keys", "n": CPU_SAMPLE},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args) -> None:
+    import torch
+
+    import paper_1804_10062_b200 as q
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        from paper_1804_10062_b200 import sharded
+        sharded.bench_main(args, METRIC, UNIT)
+        return
+
+    n = args.n
+    dev = torch.device("cuda", local)
+    pristine = torch.empty(n, dtype=torch.uint32, device=dev)
+    q.generate(q.GEN_U32, pristine, seed=SEED)
+    x = torch.empty_like(pristine)
+    cfg = q.qms()
+    if args.algorithm == "mergesort":
+        cfg.algorithm = q.Algorithm.mergesort
+    ws = torch.empty(q.workspace_bytes(q.DT_U32, n, cfg), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        x.copy_(pristine)
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        m = q.sort(x, cfg, workspace=ws, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), m
+
+    for _ in range(args.warmup):
+        step()
+    # correctness of the benchmarked sort (untimed): sorted + same multiset
+    viol, s_out, x_out = q.check(x)
+    _, s_in, x_in = q.check(pristine, order=False)
+    if viol != 0 or s_out != s_in or x_out != x_in:
+        raise RuntimeError(f"benchmarked sort is wrong: {viol} order violations / multiset mismatch")
+
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    times, launches, metrics = [], 0, None
+    for _ in range(args.steps):
+        t, m = step()
+        times.append(t)
+        launches += m.kernel_launches
+        metrics = m
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms = statistics.mean(times)
+    value = n / (ms / 1e3) / 1e9
+
+    # per-kernel-family device time (untimed profiling run with events per launch)
+    pcfg = q.qms()
+    pcfg.algorithm = cfg.algorithm
+    pcfg.profile = True
+    prof = None
+    for _ in range(2):
+        x.copy_(pristine)
+        flush.zero_()
+        torch.cuda.synchronize()
+        prof = q.sort(x, pcfg, workspace=ws, stream=stream)
+    peak, peak_src = peaks()
+    phases = prof.phases()
+    dom = max(phases.items(), key=lambda kv: kv[1][2])
+    dom_name, (dom_launches, dom_bytes, dom_ns) = dom
+    achieved = dom_bytes / dom_ns if dom_ns else 0.0  # bytes/ns == GB/s
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(dom_name)
+    sort_bytes = metrics.alg_bytes
+    sort_gbs = sort_bytes / (ms * 1e6)
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "alg_bytes_per_launch": dom_bytes / max(1, dom_launches),
+                "launches": dom_launches, "avg_launch_us": dom_ns / max(1, dom_launches) / 1e3,
+                "peak_source": peak_src}
+    sort_roofline = {"alg_bytes": sort_bytes, "achieved": sort_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": sort_gbs / peak,
+                     "floor_frac": 4 * n * 4 / (ms * 1e6) / peak,
+                     "ledger_bytes_over_nw": sort_bytes / (n * 4),
+                     "levels": metrics.levels,
+                     "phases": {k: {"launches": v[0], "alg_bytes": v[1], "us": v[2] / 1e3,
+                                    "GBps": (v[1] / v[2]) if v[2] else None}
+                                for k, v in phases.items()}}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe, seed 42)",
+            "config": {"workload": "C2: sort n=2^28 uint32 i.i.d. uniform, qms() preset, 1 B200",
+                       "n": n, "key_bytes": 4, "algorithm": args.algorithm,
+                       "l2": "flushed (256 MiB write) before every timed step; input 1 GiB > L2",
+                       "parallelism": "single GPU"},
+            "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+            "sort_roofline": sort_roofline}
+
+    if not args.no_e2e:
+        line["e2e"] = e2e(q, torch, n, pristine, cfg, args)
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline()
+    print(json.dumps(line), flush=True)
+
+
+def e2e(q, torch, n, pristine, cfg, args) -> dict:
+    """Same metric through the host-array drop-in (qmsort_gpu_sort_host): pinned
+    host input, H2D + sort + D2H inside the timed region."""
+    host_src = pristine.cpu()
+    host = torch.empty(n, dtype=torch.uint32, pin_memory=True)
+    times = []
+    steps = max(1, min(args.steps, 5))
+    for i in range(1 + steps):  # first call warms the cached device arena
+        host.copy_(host_src)
+        t = time.perf_counter()
+        q.sort(host, cfg)
+        dt = time.perf_counter() - t
+        if i > 0:
+            times.append(dt)
+    ms = statistics.mean(times) * 1e3
+    return {"value": n / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": n * 4, "d2h_bytes_per_step": n * 4,
+            "api": "qmsort_gpu_sort_host (C-ABI host drop-in), pinned host buffer"}
+
+
+def main():
+    args = parse()
+    if args.quick:
+        args.no_cpu_baseline = True
+        args.no_e2e = True
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

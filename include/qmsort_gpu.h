@@ -69,7 +69,13 @@ typedef struct {
     int algorithm;                   /* 0 samplesort (default), 1 mergesort          */
     uint64_t seed;                   /* sampling seed                                */
     int max_levels;                  /* partition levels before the merge fallback   */
+    int profile;                     /* 1: time every launch (phase_ns in metrics)   */
 } qmsort_gpu_config;
+
+/* Kernel families of the per-phase ledger: 0 transform, 1 sample (K1),
+ * 2 count (K2), 3 plan (K3), 4 scatter (K4), 5 block sort (K5), 6 merge pass
+ * (K6/K7), 7 equal-bucket fill (K8). */
+#define QMSORT_NUM_PHASES 8
 
 /* ---- Metrics (metrics.hpp:14-24) plus GPU pass ledger ------------------- */
 typedef struct {
@@ -82,6 +88,9 @@ typedef struct {
     uint32_t merge_passes;/* merge-path passes (fallback / mergesort)       */
     uint32_t kernel_launches; /* kernels launched by this call              */
     uint32_t host_syncs;  /* host synchronisations inside the sort          */
+    uint64_t phase_bytes[QMSORT_NUM_PHASES];   /* algorithmic bytes per family */
+    uint64_t phase_ns[QMSORT_NUM_PHASES];      /* device ns (profile = 1 only)  */
+    uint32_t phase_launches[QMSORT_NUM_PHASES];
 } qmsort_gpu_metrics;
 
 /* Presets qms() / qmqs() / momqms() / hqms() (sort.hpp:37-66). */

@@ -93,6 +93,7 @@ class SortConfig:
     algorithm: Algorithm = Algorithm.samplesort
     seed: int = 42
     max_levels: int = 8
+    profile: bool = False  # time every kernel launch (Metrics.phase_ns)
 
     def to_c(self) -> _lib.GpuConfig:
         c = _lib.GpuConfig()
@@ -109,6 +110,7 @@ class SortConfig:
         c.algorithm = int(self.algorithm)
         c.seed = int(self.seed) & ((1 << 64) - 1)
         c.max_levels = int(self.max_levels)
+        c.profile = int(bool(self.profile))
         return c
 
 
@@ -148,10 +150,22 @@ class Metrics:
     merge_passes: int = 0
     kernel_launches: int = 0
     host_syncs: int = 0
+    phase_bytes: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
+    phase_ns: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
+    phase_launches: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
 
     @classmethod
     def from_c(cls, m: _lib.GpuMetrics) -> "Metrics":
-        return cls(**{f.name: int(getattr(m, f.name)) for f in dataclasses.fields(cls)})
+        kw = {}
+        for f in dataclasses.fields(cls):
+            v = getattr(m, f.name)
+            kw[f.name] = [int(x) for x in v] if f.name.startswith("phase_") else int(v)
+        return cls(**kw)
+
+    def phases(self) -> dict:
+        """{family: (launches, alg_bytes, ns)} for the families that ran."""
+        return {name: (self.phase_launches[i], self.phase_bytes[i], self.phase_ns[i])
+                for i, name in enumerate(_lib.PHASE_NAMES) if self.phase_launches[i]}
 
 
 def _cmp_code(less: Any) -> int:

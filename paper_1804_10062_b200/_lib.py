@@ -40,7 +40,12 @@ class GpuConfig(ctypes.Structure):
         ("algorithm", ctypes.c_int),
         ("seed", ctypes.c_uint64),
         ("max_levels", ctypes.c_int),
+        ("profile", ctypes.c_int),
     ]
+
+
+NUM_PHASES = 8
+PHASE_NAMES = ["transform", "sample", "count", "plan", "scatter", "blocksort", "merge", "fill"]
 
 
 class GpuMetrics(ctypes.Structure):
@@ -56,6 +61,9 @@ class GpuMetrics(ctypes.Structure):
         ("merge_passes", ctypes.c_uint32),
         ("kernel_launches", ctypes.c_uint32),
         ("host_syncs", ctypes.c_uint32),
+        ("phase_bytes", ctypes.c_uint64 * 8),
+        ("phase_ns", ctypes.c_uint64 * 8),
+        ("phase_launches", ctypes.c_uint32 * 8),
     ]
 
 

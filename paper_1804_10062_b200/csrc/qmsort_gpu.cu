@@ -52,6 +52,13 @@ static int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess)                                                               \
             return fail(QMSORT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
     } while (0)
+#define QLAUNCH(led, ph, bytes, ...) \
+    do {                             \
+        (led).pre(ph);               \
+        __VA_ARGS__;                 \
+        (led).post(bytes);           \
+        QCK_LAUNCH(led);             \
+    } while (0)
 #define QTRY(x)                      \
     do {                             \
         int r_ = (x);                \
@@ -90,9 +97,67 @@ struct Tune<Rec32> {
     static constexpr int MT = 512, MI = 8;
 };
 
+// Kernel families for the per-phase ledger (qmsort_gpu_metrics.phase_*).
+enum Phase {
+    kPhTransform = 0,
+    kPhSample = 1,
+    kPhCount = 2,
+    kPhPlan = 3,
+    kPhScatter = 4,
+    kPhBlocksort = 5,
+    kPhMerge = 6,
+    kPhFill = 7,
+};
+
+// Pass ledger: algorithmic bytes per kernel family and, when profiling is on,
+// CUDA-event device time of every launch.
 struct Ledger {
     uint64_t alg_bytes = 0;
     uint32_t launches = 0, syncs = 0, levels = 0, merge_passes = 0;
+    uint64_t ph_bytes[QMSORT_NUM_PHASES] = {};
+    uint32_t ph_launches[QMSORT_NUM_PHASES] = {};
+    bool prof = false;
+    cudaStream_t st = nullptr;
+    int cur = 0;
+    cudaEvent_t pending = nullptr;
+    struct Rec {
+        int ph;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    void pre(int ph) {
+        cur = ph;
+        if (prof) {
+            cudaEventCreate(&pending);
+            cudaEventRecord(pending, st);
+        }
+    }
+    void post(uint64_t bytes) {
+        ph_bytes[cur] += bytes;
+        alg_bytes += bytes;
+        ++ph_launches[cur];
+        if (prof) {
+            cudaEvent_t b;
+            cudaEventCreate(&b);
+            cudaEventRecord(b, st);
+            recs.push_back({cur, pending, b});
+            pending = nullptr;
+        }
+    }
+    // After the stream is synchronised: per-phase device time.
+    void collect(uint64_t* ph_ns) {
+        for (const Rec& r : recs) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) ph_ns[r.ph] += (uint64_t)((double)ms * 1e6);
+        }
+    }
+    ~Ledger() {
+        for (const Rec& r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        if (pending) cudaEventDestroy(pending);
+    }
 };
 
 // Raise the dynamic shared-memory limit of a kernel once per process.
@@ -164,9 +229,8 @@ static int launch_tiles(const K* src, K* dst, uint64_t off, uint64_t len, cudaSt
     auto fn = blocksort_tiles_kernel<K, T, I>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
     const uint64_t tiles = (len + BS::kCap - 1) / BS::kCap;
-    fn<<<(unsigned)tiles, T, BS::kSmemBytes, st>>>(src, dst, off, len);
-    QCK_LAUNCH(led);
-    led.alg_bytes += 2 * len * sizeof(K);
+    QLAUNCH(led, kPhBlocksort, 2 * len * sizeof(K),
+            fn<<<(unsigned)tiles, T, BS::kSmemBytes, st>>>(src, dst, off, len));
     return QMSORT_OK;
 }
 
@@ -200,9 +264,8 @@ static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStr
     K* s = Y;
     K* d = (Y == A) ? B : A;
     for (uint64_t run = C; run < len; run *= 2) {
-        fn<<<(unsigned)((len + MC - 1) / MC), TU::MT, BS::kSmemBytes, st>>>(s + off, d + off, len, run);
-        QCK_LAUNCH(led);
-        led.alg_bytes += 2 * len * sizeof(K);
+        QLAUNCH(led, kPhMerge, 2 * len * sizeof(K),
+                fn<<<(unsigned)((len + MC - 1) / MC), TU::MT, BS::kSmemBytes, st>>>(s + off, d + off, len, run));
         ++led.merge_passes;
         std::swap(s, d);
     }
@@ -246,8 +309,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     FillTask* fills = reinterpret_cast<FillTask*>(ws + L.fills_off);
 
     QCK(cudaMemsetAsync(lv[0].cnt, 0, sizeof(LevelCounters), st));
-    init_level_kernel<<<1, 32, 0, st>>>(lv[0], n, p);
-    QCK_LAUNCH(led);
+    QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<1, 32, 0, st>>>(lv[0], n, p));
 
     using BSS = BlockSorter<K, TU::ST, TU::SI>;
     auto sample_fn = sample_kernel<K, TU::ST, TU::SI>;
@@ -265,6 +327,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     QCK(allow_smem((const void*)bs1, B1::kSmemBytes));
     QCK(allow_smem((const void*)bs2, B2::kSmemBytes));
 
+    uint64_t level_keys = n;
     uint32_t nsegs = 1;
     uint32_t nchunks = (uint32_t)((n + L.chunk_elems - 1) / L.chunk_elems);
     int cur = 0;
@@ -285,18 +348,19 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         }
         p.dst_is_a = (dst == A) ? 1 : 0;
         const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
-        sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur], sorted[cur], seed);
-        QCK_LAUNCH(led);
-        count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
-            lv[cur].segs, lv[cur].chunks, src, tree[cur], sorted[cur], hist);
-        QCK_LAUNCH(led);
+        QLAUNCH(led, kPhSample, 0,
+                sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur],
+                                                                  sorted[cur], seed));
+        QLAUNCH(led, kPhCount, level_keys * sizeof(K),
+                count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
+                    lv[cur].segs, lv[cur].chunks, src, tree[cur], sorted[cur], hist));
         QCK(cudaMemsetAsync(lv[nxt].cnt, 0, sizeof(LevelCounters), st));
-        plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(lv[cur].segs, hist, lv[nxt], p,
-                                                                 tasks, fills, lv[cur].cnt);
-        QCK_LAUNCH(led);
-        scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(lv[cur].segs, lv[cur].chunks, src, dst,
-                                                        tree[cur], sorted[cur], hist);
-        QCK_LAUNCH(led);
+        QLAUNCH(led, kPhPlan, 0,
+                plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(lv[cur].segs, hist, lv[nxt],
+                                                                         p, tasks, fills, lv[cur].cnt));
+        QLAUNCH(led, kPhScatter, 2 * level_keys * sizeof(K),
+                scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(lv[cur].segs, lv[cur].chunks, src,
+                                                                dst, tree[cur], sorted[cur], hist));
         LevelCounters hc[2];
         QCK(cudaMemcpyAsync(&hc[0], lv[cur].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         QCK(cudaMemcpyAsync(&hc[1], lv[nxt].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
@@ -305,26 +369,27 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         if (hc[0].overflow || hc[1].overflow)
             return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
         ++led.levels;
-        led.alg_bytes += 3ull * hc[0].nkeys * sizeof(K);  // count (1) + scatter (2)
         const uint32_t nt[3] = {hc[0].ntasks[0], hc[0].ntasks[1], hc[0].ntasks[2]};
+        // the block-sort bytes of a level are credited to its first launch
+        uint64_t bs_bytes = 2ull * hc[0].task_keys * sizeof(K);
         if (nt[0]) {
-            bs0<<<nt[0], TU::C0T, B0::kSmemBytes, st>>>(tasks, dst, A);
-            QCK_LAUNCH(led);
+            QLAUNCH(led, kPhBlocksort, bs_bytes, bs0<<<nt[0], TU::C0T, B0::kSmemBytes, st>>>(tasks, dst, A));
+            bs_bytes = 0;
         }
         if (nt[1]) {
-            bs1<<<nt[1], TU::C1T, B1::kSmemBytes, st>>>(tasks + L.task_cap, dst, A);
-            QCK_LAUNCH(led);
+            QLAUNCH(led, kPhBlocksort, bs_bytes,
+                    bs1<<<nt[1], TU::C1T, B1::kSmemBytes, st>>>(tasks + L.task_cap, dst, A));
+            bs_bytes = 0;
         }
         if (nt[2]) {
-            bs2<<<nt[2], TU::C2T, B2::kSmemBytes, st>>>(tasks + 2 * (size_t)L.task_cap, dst, A);
-            QCK_LAUNCH(led);
+            QLAUNCH(led, kPhBlocksort, bs_bytes,
+                    bs2<<<nt[2], TU::C2T, B2::kSmemBytes, st>>>(tasks + 2 * (size_t)L.task_cap, dst, A));
         }
-        led.alg_bytes += 2ull * hc[0].task_keys * sizeof(K);
         if (hc[0].nfill) {
-            fill_kernel<K><<<1184, 256, 0, st>>>(fills, hc[0].nfill, lv[cur].segs, sorted[cur], A);
-            QCK_LAUNCH(led);
-            led.alg_bytes += hc[0].fill_keys * sizeof(K);
+            QLAUNCH(led, kPhFill, hc[0].fill_keys * sizeof(K),
+                    fill_kernel<K><<<1184, 256, 0, st>>>(fills, hc[0].nfill, lv[cur].segs, sorted[cur], A));
         }
+        level_keys = hc[1].nkeys;
         nsegs = hc[1].nsegs;
         nchunks = hc[1].nchunks;
         cur = nxt;
@@ -387,11 +452,11 @@ static int run_transform(int dt, int cmp, void* d, size_t n, int inverse, cudaSt
     if (mode == kXfNone || n == 0) return QMSORT_OK;
     const unsigned grid = (unsigned)std::min<size_t>((words + 255) / 256, 148 * 16);
     if (wide)
-        transform64_kernel<<<grid, 256, 0, st>>>(static_cast<uint64_t*>(d), words, mode, inverse);
+        QLAUNCH(led, kPhTransform, 2 * n * dtype_size(dt),
+                transform64_kernel<<<grid, 256, 0, st>>>(static_cast<uint64_t*>(d), words, mode, inverse));
     else
-        transform32_kernel<<<grid, 256, 0, st>>>(static_cast<uint32_t*>(d), words, mode);
-    QCK_LAUNCH(led);
-    led.alg_bytes += 2 * n * dtype_size(dt);
+        QLAUNCH(led, kPhTransform, 2 * n * dtype_size(dt),
+                transform32_kernel<<<grid, 256, 0, st>>>(static_cast<uint32_t*>(d), words, mode));
     return QMSORT_OK;
 }
 
@@ -419,6 +484,8 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
         return fail(QMSORT_ENOWS, "workspace too small: need " + std::to_string(need) + " bytes");
     }
     Ledger led;
+    led.prof = cfg.profile != 0;
+    led.st = st;
     cudaEvent_t e0, e1;
     QCK(cudaEventCreate(&e0));
     QCK(cudaEventCreate(&e1));
@@ -457,6 +524,11 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
         m->merge_passes = led.merge_passes;
         m->kernel_launches = led.launches;
         m->host_syncs = led.syncs + 1;
+        for (int i = 0; i < QMSORT_NUM_PHASES; ++i) {
+            m->phase_bytes[i] = led.ph_bytes[i];
+            m->phase_launches[i] = led.ph_launches[i];
+        }
+        led.collect(m->phase_ns);
     }
     g_err.clear();
     return QMSORT_OK;
@@ -552,21 +624,20 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     K* sorted = reinterpret_cast<K*>(ws + L.sorted_off[0]);
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
     const uint32_t nchunks = (uint32_t)std::max<uint64_t>(1, (n + L.chunk_elems - 1) / L.chunk_elems);
-    given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, n, nchunks,
-                                                 chunks, L.chunk_elems);
-    QCK_LAUNCH(led);
+    QLAUNCH(led, kPhSample, 0,
+            given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, n,
+                                                         nchunks, chunks, L.chunk_elems));
     QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
     if (n == 0) return QMSORT_OK;
-    count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(seg, chunks, in, tree, sorted, hist);
-    QCK_LAUNCH(led);
-    offsets_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts);
-    QCK_LAUNCH(led);
+    QLAUNCH(led, kPhCount, n * sizeof(K),
+            count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(seg, chunks, in, tree,
+                                                                             sorted, hist));
+    QLAUNCH(led, kPhPlan, 0, offsets_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
-    scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(seg, chunks, in, out, tree, sorted, hist);
-    QCK_LAUNCH(led);
-    led.alg_bytes += 3 * n * sizeof(K);
+    QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
+            scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(seg, chunks, in, out, tree, sorted, hist));
     return QMSORT_OK;
 }
 
@@ -593,6 +664,7 @@ void qmsort_gpu_config_init(qmsort_gpu_config* c, int variant) {
     c->algorithm = 0;
     c->seed = 42;
     c->max_levels = 8;
+    c->profile = 0;
     switch (variant) {
         case 1:  // qmqs (sort.hpp:41-48)
             c->variant = 1;
