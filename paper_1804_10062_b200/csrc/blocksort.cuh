@@ -72,39 +72,42 @@ template <class K>
 __device__ __forceinline__ int merge_path_smem(const K* s, int a0, int alen, int b0, int blen,
                                                int diag) {
     using P = SmemPad<K>;
-    int lo = diag > blen ? diag - blen : 0;
-    int hi = diag < alen ? diag : alen;
+    unsigned lo = diag > blen ? (unsigned)(diag - blen) : 0u;
+    unsigned hi = diag < alen ? (unsigned)diag : (unsigned)alen;
+    const unsigned bd = (unsigned)(b0 + diag - 1);
     while (lo < hi) {
-        int mid = (lo + hi) >> 1;
+        const unsigned mid = (lo + hi) >> 1;
         // A[mid] goes first unless B[diag-1-mid] < A[mid]
-        if (!KeyTraits<K>::lt(s[P::idx(b0 + diag - 1 - mid)], s[P::idx(a0 + mid)]))
-            lo = mid + 1;
-        else
-            hi = mid;
+        const bool a_first = !KeyTraits<K>::lt(s[P::idx(bd - mid)], s[P::idx((unsigned)a0 + mid)]);
+        lo = a_first ? mid + 1 : lo;
+        hi = a_first ? hi : mid;
     }
-    return lo;
+    return (int)lo;
 }
 
-// Serially merge ITEMS outputs from positions (ai in A, bi in B) of two sorted
-// shared-memory runs [a0,a0+alen) and [b0,b0+blen) into registers.
+// Serially merge ITEMS outputs from positions ai (run A, ends at aend) and bi
+// (run B, ends at bend) of shared memory into registers.  Branch-free: an
+// exhausted run reads as the maximum key, which is also exactly what any
+// remaining keys of the other run equal when a tie with it takes run A.
 template <class K, int ITEMS>
 __device__ __forceinline__ void serial_merge_smem(const K* s, int ai, int aend, int bi, int bend,
                                                   K (&out)[ITEMS]) {
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
-    K ka = ai < aend ? s[P::idx(ai)] : KT::max_key();
-    K kb = bi < bend ? s[P::idx(bi)] : KT::max_key();
+    K ka = ai < aend ? s[P::idx((unsigned)ai)] : KT::max_key();
+    K kb = bi < bend ? s[P::idx((unsigned)bi)] : KT::max_key();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const bool take_b = (bi < bend) && ((ai >= aend) || KT::lt(kb, ka));
-        out[i] = take_b ? kb : ka;
-        if (take_b) {
-            ++bi;
-            if (bi < bend) kb = s[P::idx(bi)];
-        } else {
-            ++ai;
-            if (ai < aend) ka = s[P::idx(ai)];
-        }
+        const bool tb = KT::lt(kb, ka);
+        out[i] = tb ? kb : ka;
+        ai += tb ? 0 : 1;
+        bi += tb ? 1 : 0;
+        const int ni = tb ? bi : ai;
+        const int ne = tb ? bend : aend;
+        K v = s[P::idx((unsigned)ni)];  // at most ITEMS slots past a run end: inside the slack
+        v = ni < ne ? v : KT::max_key();
+        ka = tb ? ka : v;
+        kb = tb ? v : kb;
     }
 }
 
@@ -118,11 +121,16 @@ struct BlockSorter {
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
 
+    // Keys rounded up to whole threads: threads at or beyond mp / ITEMS own
+    // no keys and only take part in the barriers.
+    __device__ __forceinline__ static int padded(int m) { return (m + ITEMS - 1) / ITEMS * ITEMS; }
+
     // Coalesced (striped) load of m <= kCap keys into shared memory, padding
-    // the tail with the maximum key.
+    // up to a whole thread with the maximum key.
     __device__ __forceinline__ static void load_striped(const K* __restrict__ src, int m, K* s) {
+        const int mp = padded(m);
 #pragma unroll 4
-        for (int i = threadIdx.x; i < kCap; i += T) s[P::idx(i)] = i < m ? src[i] : KT::max_key();
+        for (int i = threadIdx.x; i < mp; i += T) s[P::idx(i)] = i < m ? src[i] : KT::max_key();
     }
     __device__ __forceinline__ static void store_blocked(const K (&k)[ITEMS], K* s) {
         const int base = threadIdx.x * ITEMS;
@@ -139,24 +147,32 @@ struct BlockSorter {
         for (int i = threadIdx.x; i < m; i += T) dst[i] = s[P::idx(i)];
     }
 
-    // Sort the kCap keys held in registers (blocked arrangement).  On return
-    // the sorted tile sits in shared memory s (padded indexing).  Must be
-    // called by all T threads; s must not be in use.
-    __device__ __forceinline__ static void sort(K (&k)[ITEMS], K* s) {
-        register_sort<K, ITEMS>(k);
+    // Sort the first m keys held in registers (blocked arrangement; the last
+    // owning thread is padded with the maximum key).  Cost scales with m:
+    // ceil(log2(m / ITEMS)) merge rounds over the owning threads only.  On
+    // return the sorted keys sit in shared memory s (padded indexing).  Must
+    // be called by all T threads; s must not be in use.
+    __device__ __forceinline__ static void sort(K (&k)[ITEMS], K* s, int m) {
+        const int mp = padded(m);
+        const int out = threadIdx.x * ITEMS;
+        const bool owner = out < mp;
+        if (owner) register_sort<K, ITEMS>(k);
 #pragma unroll 1
-        for (int run = ITEMS; run < kCap; run <<= 1) {
-            store_blocked(k, s);
+        for (int run = ITEMS; run < mp; run <<= 1) {
+            if (owner) store_blocked(k, s);
             __syncthreads();
-            const int out = threadIdx.x * ITEMS;
-            const int pair = out & ~(2 * run - 1);
-            const int diag = out - pair;
-            const int a0 = pair, b0 = pair + run;
-            const int a = merge_path_smem<K>(s, a0, run, b0, run, diag);
-            serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + run, b0 + diag - a, b0 + run, k);
+            if (owner) {
+                const int pair = out & ~(2 * run - 1);
+                const int diag = out - pair;
+                const int a0 = pair, b0 = pair + run;
+                const int alen = min(run, mp - a0);
+                const int blen = max(0, min(run, mp - b0));
+                const int a = merge_path_smem<K>(s, a0, alen, b0, blen, diag);
+                serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + alen, b0 + diag - a, b0 + blen, k);
+            }
             __syncthreads();
         }
-        store_blocked(k, s);
+        if (owner) store_blocked(k, s);
         __syncthreads();
     }
 
@@ -165,9 +181,9 @@ struct BlockSorter {
         load_striped(src, m, s);
         __syncthreads();
         K k[ITEMS];
-        load_blocked(k, s);
+        if ((int)threadIdx.x * ITEMS < padded(m)) load_blocked(k, s);
         __syncthreads();
-        sort(k, s);
+        sort(k, s, m);
         store_striped(dst, m, s);
     }
 };

@@ -34,6 +34,9 @@ struct KeyTraits<uint32_t> {
         b = hi;
     }
     __device__ __forceinline__ static uint64_t hash(uint32_t a) { return a; }
+    // bucket lookup table (LUT) support: keys are unsigned integers
+    static constexpr bool kLut = true;
+    __device__ __forceinline__ static uint64_t bits(uint32_t a) { return a; }
 };
 
 template <>
@@ -49,6 +52,8 @@ struct KeyTraits<uint64_t> {
         b = hi;
     }
     __device__ __forceinline__ static uint64_t hash(uint64_t a) { return a; }
+    static constexpr bool kLut = true;
+    __device__ __forceinline__ static uint64_t bits(uint64_t a) { return a; }
 };
 
 template <>
@@ -84,16 +89,21 @@ struct KeyTraits<Rec32> {
         return a.w[0] * 0x9E3779B97F4A7C15ull ^ a.w[1] * 0xBF58476D1CE4E5B9ull ^
                a.w[2] * 0x94D049BB133111EBull ^ a.w[3];
     }
+    static constexpr bool kLut = false;  // classified by the search tree only
+    __device__ __forceinline__ static uint64_t bits(const Rec32& a) { return a.w[0]; }
 };
 
 // Shared-memory padding: one spare element every 128 bytes so that a thread
 // that owns ITEMS consecutive keys ("blocked" arrangement) can store them
 // without bank conflicts when ITEMS*sizeof(K) is a multiple of 128 bytes.
+// elems() leaves 64 elements of slack so that merge loops may read a few
+// slots past the end of a run without leaving the allocation.
 template <class K>
 struct SmemPad {
     static constexpr int kPer = (128 / KeyTraits<K>::kBytes) > 0 ? (128 / KeyTraits<K>::kBytes) : 1;
-    __device__ __forceinline__ static int idx(int i) { return i + i / kPer; }
-    static constexpr int elems(int n) { return n + n / kPer + 1; }
+    static constexpr int kShift = kPer >= 32 ? 5 : kPer >= 16 ? 4 : kPer >= 8 ? 3 : kPer >= 4 ? 2 : kPer >= 2 ? 1 : 0;
+    __device__ __forceinline__ static unsigned idx(unsigned i) { return i + (i >> kShift); }
+    static constexpr int elems(int n) { return n + n / kPer + 64; }
 };
 
 // SplitMix64 finaliser (reference rng.hpp:14-19) -- also used as a hash.

@@ -74,11 +74,14 @@ __global__ void __launch_bounds__(T) merge_pass_kernel(const K* __restrict__ src
     for (int i = threadIdx.x; i < total; i += T) s[P::idx(i)] = i < na ? As[i] : Bs[i - na];
     __syncthreads();
     K k[ITEMS];
-    const int diag = min((int)threadIdx.x * ITEMS, total);
-    const int a = merge_path_smem<K>(s, 0, na, na, nb, diag);
-    serial_merge_smem<K, ITEMS>(s, a, na, na + diag - a, na + nb, k);
+    const int diag = (int)threadIdx.x * ITEMS;
+    const bool owner = diag < total;
+    if (owner) {
+        const int a = merge_path_smem<K>(s, 0, na, na, nb, diag);
+        serial_merge_smem<K, ITEMS>(s, a, na, na + diag - a, na + nb, k);
+    }
     __syncthreads();
-    BS::store_blocked(k, s);
+    if (owner) BS::store_blocked(k, s);
     __syncthreads();
     BS::store_striped(dst + pair + d0, total, s);
 }

@@ -75,7 +75,7 @@ struct Tune<uint32_t> {
     static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
     static constexpr int ST = 512, SI = 16;  // sampler
     static constexpr int XT = 512, XI = 16;  // scatter tile
-    static constexpr int CT = 512;           // count
+    static constexpr int CT = 512, CU = 16;  // count
     static constexpr int MT = 512, MI = 16;  // merge pass
 };
 template <>
@@ -84,7 +84,7 @@ struct Tune<uint64_t> {
     static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
     static constexpr int ST = 512, SI = 16;
     static constexpr int XT = 512, XI = 8;
-    static constexpr int CT = 512;
+    static constexpr int CT = 512, CU = 8;
     static constexpr int MT = 512, MI = 16;
 };
 template <>
@@ -93,7 +93,7 @@ struct Tune<Rec32> {
     static constexpr int C0T = 64, C0I = 8, C1T = 256, C1I = 8, C2T = 512, C2I = 8;
     static constexpr int ST = 512, SI = 8;
     static constexpr int XT = 256, XI = 8;
-    static constexpr int CT = 256;
+    static constexpr int CT = 256, CU = 4;
     static constexpr int MT = 512, MI = 8;
 };
 
@@ -176,7 +176,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct WsLayout {
     size_t b_off = 0, segs_off[2] = {0, 0}, chunks_off[2] = {0, 0}, cnt_off[2] = {0, 0};
-    size_t tree_off[2] = {0, 0}, sorted_off[2] = {0, 0};
+    size_t tree_off[2] = {0, 0}, sorted_off[2] = {0, 0}, lut_off[2] = {0, 0};
     size_t hist_off = 0, tasks_off = 0, fills_off = 0, misc_off = 0, total = 0;
     uint32_t seg_cap = 0, chunk_cap = 0, split_cap = 0, task_cap = 0, fill_cap = 0, hist_cap = 0;
     uint64_t chunk_elems = 0;
@@ -189,8 +189,8 @@ static WsLayout make_layout(size_t n) {
     constexpr uint64_t target = cap / 2;
     constexpr uint64_t tile = (uint64_t)TU::XT * TU::XI;
     WsLayout L;
-    // ~8 chunks per SM on a 148-SM part at level 0
-    uint64_t ch = (n + 1183) / 1184;
+    // ~4 chunks per SM on a 148-SM part at level 0
+    uint64_t ch = (n + 591) / 592;
     ch = std::max<uint64_t>(tile, align_up(ch, tile));
     L.chunk_elems = ch;
     L.seg_cap = (uint32_t)(n / cap + 2);
@@ -212,6 +212,7 @@ static WsLayout make_layout(size_t n) {
         L.cnt_off[i] = take(sizeof(LevelCounters));
         L.tree_off[i] = take(sizeof(K) * L.split_cap);
         L.sorted_off[i] = take(sizeof(K) * L.split_cap);
+        L.lut_off[i] = take(KeyTraits<K>::kLut ? sizeof(uint32_t) * kLutPerSplitter * (size_t)L.split_cap : 0);
     }
     L.hist_off = take(sizeof(uint32_t) * (size_t)L.hist_cap);
     L.tasks_off = take(sizeof(SortTask) * (size_t)kNumClasses * L.task_cap);
@@ -293,6 +294,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     LevelBufs lv[2];
     K* tree[2];
     K* sorted[2];
+    uint32_t* lut[2];
     for (int i = 0; i < 2; ++i) {
         lv[i].segs = reinterpret_cast<SegDesc*>(ws + L.segs_off[i]);
         lv[i].chunks = reinterpret_cast<ChunkDesc*>(ws + L.chunks_off[i]);
@@ -303,13 +305,14 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         lv[i].hist_cap = L.hist_cap;
         tree[i] = reinterpret_cast<K*>(ws + L.tree_off[i]);
         sorted[i] = reinterpret_cast<K*>(ws + L.sorted_off[i]);
+        lut[i] = reinterpret_cast<uint32_t*>(ws + L.lut_off[i]);
     }
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
     SortTask* tasks = reinterpret_cast<SortTask*>(ws + L.tasks_off);
     FillTask* fills = reinterpret_cast<FillTask*>(ws + L.fills_off);
 
     QCK(cudaMemsetAsync(lv[0].cnt, 0, sizeof(LevelCounters), st));
-    QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<1, 32, 0, st>>>(lv[0], n, p));
+    QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<1, 32, 0, st>>>(lv[0], n, ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K))), p));
 
     using BSS = BlockSorter<K, TU::ST, TU::SI>;
     auto sample_fn = sample_kernel<K, TU::ST, TU::SI>;
@@ -350,17 +353,19 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
         QLAUNCH(led, kPhSample, 0,
                 sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur],
-                                                                  sorted[cur], seed));
+                                                                  sorted[cur], lut[cur], seed, 16u));
         QLAUNCH(led, kPhCount, level_keys * sizeof(K),
-                count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
-                    lv[cur].segs, lv[cur].chunks, src, tree[cur], sorted[cur], hist));
+                count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
+                    lv[cur].segs, lv[cur].chunks, src, tree[cur], sorted[cur], lut[cur], hist));
+        const unsigned gy = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(128, nchunks / nsegs / 4));
+        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(nsegs, gy), 512, 0, st>>>(lv[cur].segs, hist));
         QCK(cudaMemsetAsync(lv[nxt].cnt, 0, sizeof(LevelCounters), st));
         QLAUNCH(led, kPhPlan, 0,
-                plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(lv[cur].segs, hist, lv[nxt],
-                                                                         p, tasks, fills, lv[cur].cnt));
+                plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(
+                    lv[cur].segs, hist, sorted[cur], lv[nxt], p, tasks, fills, lv[cur].cnt));
         QLAUNCH(led, kPhScatter, 2 * level_keys * sizeof(K),
                 scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(lv[cur].segs, lv[cur].chunks, src,
-                                                                dst, tree[cur], sorted[cur], hist));
+                                                                dst, tree[cur], sorted[cur], lut[cur], hist));
         LevelCounters hc[2];
         QCK(cudaMemcpyAsync(&hc[0], lv[cur].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         QCK(cudaMemcpyAsync(&hc[1], lv[nxt].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
@@ -547,17 +552,48 @@ __global__ void gather_sample_kernel(const K* __restrict__ src, uint64_t n, uint
     }
 }
 
-// Build the Eytzinger tree of caller-given sorted splitters into one segment.
+// Classifier (LUT or Eytzinger tree) of caller-given sorted splitters for one
+// segment covering the whole input; three-way classification off.
 template <class K>
 __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nsplit, uint32_t logk,
-                                       SegDesc* seg, K* tree, K* sorted, uint64_t n,
-                                       uint32_t nchunks, ChunkDesc* chunks, uint64_t chunk_elems) {
+                                       SegDesc* seg, K* tree, K* sorted, uint32_t* lut, uint64_t n,
+                                       uint32_t nchunks, ChunkDesc* chunks, uint64_t chunk_elems,
+                                       uint64_t key_max) {
+    using KT = KeyTraits<K>;
     const uint32_t K_ = 1u << logk;
-    for (uint32_t i = threadIdx.x; i < K_; i += blockDim.x) sorted[i] = i < nsplit ? spl[i] : KeyTraits<K>::max_key();
-    for (uint32_t t = threadIdx.x + 1; t < K_; t += blockDim.x) {
-        const uint32_t depth = 31 - __clz(t);
-        const uint32_t rank = ((2 * (t - (1u << depth)) + 1) << (logk - 1 - depth)) - 1;
-        tree[t] = rank < nsplit ? spl[rank] : KeyTraits<K>::max_key();
+    const uint32_t lutbits = min(logk + 4, (uint32_t)kLutMaxBits);
+    uint32_t bl = 0;
+    while (bl < 64 && (key_max >> bl) != 0) ++bl;
+    const uint32_t shift = bl > lutbits ? bl - lutbits : 0;
+    for (uint32_t i = threadIdx.x; i < K_; i += blockDim.x) sorted[i] = i < nsplit ? spl[i] : KT::max_key();
+    if constexpr (KT::kLut) {
+        for (uint32_t c = threadIdx.x; c < (1u << lutbits); c += blockDim.x) {
+            const uint64_t cmin = (uint64_t)c << shift;
+            uint64_t cmax = cmin + (((uint64_t)1 << shift) - 1);
+            if (c == (1u << lutbits) - 1 || cmax > key_max || cmax < cmin) cmax = key_max;
+            uint32_t r[2];
+            for (int w = 0; w < 2; ++w) {
+                const uint64_t v = w == 0 ? cmin : cmax;
+                uint32_t lo = 0, cnt = nsplit;
+                while (cnt > 0) {
+                    const uint32_t half = cnt >> 1;
+                    if ((uint64_t)KT::bits(spl[lo + half]) < v) {
+                        lo += half + 1;
+                        cnt -= half + 1;
+                    } else {
+                        cnt = half;
+                    }
+                }
+                r[w] = lo;
+            }
+            lut[c] = r[0] | ((r[1] - r[0]) << 16);
+        }
+    } else {
+        for (uint32_t t = threadIdx.x + 1; t < K_; t += blockDim.x) {
+            const uint32_t depth = 31 - __clz(t);
+            const uint32_t rank = ((2 * (t - (1u << depth)) + 1) << (logk - 1 - depth)) - 1;
+            tree[t] = rank < nsplit ? spl[rank] : KT::max_key();
+        }
     }
     for (uint32_t c = threadIdx.x; c < nchunks; c += blockDim.x) {
         ChunkDesc cd;
@@ -571,6 +607,8 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
         SegDesc d;
         d.off = 0;
         d.len = n;
+        d.lo = 0;
+        d.hi = key_max;
         d.chunk_begin = 0;
         d.nchunks = nchunks;
         d.logk = logk;
@@ -578,37 +616,33 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
         d.eq = 0;
         d.sp = 0;
         d.hist_base = 0;
-        d.pad = 0;
+        d.shift = shift;
+        d.lutbits = lutbits;
+        d.pad[0] = d.pad[1] = d.pad[2] = 0;
         *seg = d;
     }
 }
 
-// Offsets only (no children): per-chunk offsets in place and bucket counts.
+// Offsets only (no children): bucket starts in place of the totals and the
+// bucket counts (bin b = bucket j, three-way off).
 template <int T, int LOG_KMAX>
-__global__ void __launch_bounds__(T) offsets_kernel(const SegDesc* __restrict__ segs,
-                                                    uint32_t* __restrict__ chunk_hist,
-                                                    uint32_t nsplit, uint64_t* counts) {
+__global__ void __launch_bounds__(T) given_plan_kernel(const SegDesc* __restrict__ segs,
+                                                       uint32_t* __restrict__ hist,
+                                                       uint32_t nsplit, uint64_t* counts) {
     constexpr int NB = 2 << LOG_KMAX;
     __shared__ uint32_t start[NB];
     __shared__ uint32_t warp_sums[32];
     const SegDesc d = segs[0];
-    const uint32_t nb = 2u << d.logk;
+    const uint32_t nb = 1u << d.logk;
+    const uint32_t stride = d.nchunks + 1;
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
-        uint32_t sum = 0;
-        for (uint32_t c = 0; c < d.nchunks; ++c) sum += chunk_hist[(size_t)c * nb + b];
-        start[b] = sum;
-        if ((b & 1) == 0 && (b >> 1) <= nsplit) counts[b >> 1] = sum;
+        const uint32_t v = hist[b * stride + d.nchunks];
+        start[b] = v;
+        if (b <= nsplit) counts[b] = v;
     }
     __syncthreads();
     block_exclusive_scan_smem<T>(start, (int)nb, warp_sums);
-    for (uint32_t b = threadIdx.x; b < nb; b += T) {
-        uint32_t run = start[b];
-        for (uint32_t c = 0; c < d.nchunks; ++c) {
-            const uint32_t v = chunk_hist[(size_t)c * nb + b];
-            chunk_hist[(size_t)c * nb + b] = run;
-            run += v;
-        }
-    }
+    for (uint32_t b = threadIdx.x; b < nb; b += T) hist[b * stride + d.nchunks] = start[b];
 }
 
 template <class K>
@@ -622,22 +656,25 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     ChunkDesc* chunks = reinterpret_cast<ChunkDesc*>(ws + L.chunks_off[0]);
     K* tree = reinterpret_cast<K*>(ws + L.tree_off[0]);
     K* sorted = reinterpret_cast<K*>(ws + L.sorted_off[0]);
+    uint32_t* lut = reinterpret_cast<uint32_t*>(ws + L.lut_off[0]);
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
+    const uint64_t key_max = ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K)));
     const uint32_t nchunks = (uint32_t)std::max<uint64_t>(1, (n + L.chunk_elems - 1) / L.chunk_elems);
     QLAUNCH(led, kPhSample, 0,
-            given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, n,
-                                                         nchunks, chunks, L.chunk_elems));
+            given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, lut,
+                                                         n, nchunks, chunks, L.chunk_elems, key_max));
     QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
     if (n == 0) return QMSORT_OK;
     QLAUNCH(led, kPhCount, n * sizeof(K),
-            count_kernel<K, TU::CT, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(seg, chunks, in, tree,
-                                                                             sorted, hist));
-    QLAUNCH(led, kPhPlan, 0, offsets_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
+            count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
+                seg, chunks, in, tree, sorted, lut, hist));
+    QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(1, 64), 512, 0, st>>>(seg, hist));
+    QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
     QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
-            scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(seg, chunks, in, out, tree, sorted, hist));
+            scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(seg, chunks, in, out, tree, sorted, lut, hist));
     return QMSORT_OK;
 }
 

@@ -3,46 +3,62 @@
 // Generalises the reference's pivot step (median_of_3_index,
 // partition.hpp:21-30; median_of_sqrt_pivot, partition.hpp:235-251) and its
 // partition (block_partition, partition.hpp:37-164) from one pivot / two sides
-// to K-1 splitters / up to 2K-1 buckets per pass:
+// to K-1 splitters / K (or 2K-1 with equality buckets) buckets per pass:
 //   * sample_kernel   (K1) -- per segment, draws a seeded sample, sorts it on
 //                             chip (blocksort.cuh) and picks K-1 evenly spaced
-//                             splitters, exactly like the Median-of-sqrt(n)
-//                             sample generalised to K-1 quantiles.  Duplicate
+//                             splitters: the Median-of-sqrt(n) sample
+//                             generalised to K-1 quantiles.  Duplicate
 //                             splitters switch the segment to three-way
 //                             classification (K8, the "equal block takes no
 //                             further part" rule of three_way_partition,
 //                             partition.hpp:194-195).
-//   * count_kernel    (K2) -- branchless search-tree classification, per-chunk
-//                             bucket histogram in shared memory.
-//   * plan_kernel     (K3) -- per segment: bucket totals, exclusive scan,
-//                             per-(chunk, bucket) output offsets; emits the
-//                             child work (next-level segments, block-sort
+//   * count_kernel    (K2) -- classification of U keys per thread in lock
+//                             step, shared-memory bucket histogram per chunk.
+//   * colsum_kernel +
+//     plan_kernel     (K3) -- per (segment, bucket): exclusive prefix over the
+//                             chunks; per segment: bucket totals, starts and
+//                             the child work (next-level segments, block-sort
 //                             tasks, equal-bucket fills).
 //   * scatter_kernel  (K4) -- re-classifies each tile, groups it by bucket in
 //                             shared memory and writes every bucket run with
 //                             coalesced stores to its final offset.
 // Offsets are deterministic (no global atomics on the data path): chunk c of
-// a segment writes bucket b at  start[b] + sum_{c' < c} hist[c'][b].
+// a segment writes bucket b at  start[b] + sum_{c' < c} hist[b][c'].
+//
+// Classification.  The bucket of key x is j = #{splitters < x} -- the same
+// comparisons against the same splitters for every key type.  For integer
+// keys the search is shortened by a bucket lookup table: the segment's key
+// range [lo, hi] (known from the parent's splitters) is cut into 2^lutbits
+// cells; cell c stores the bucket range [j_lo, j_hi] its keys can fall in, and
+// only keys of cells that straddle a splitter finish with a binary search over
+// sorted[j_lo..j_hi).  Records (rec32) walk an Eytzinger search tree.
 #pragma once
+#include <type_traits>
+
 #include "blocksort.cuh"
 #include "common.cuh"
 
 namespace qmsort_b200 {
 
 constexpr int kNumClasses = 3;  // block-sort size classes
+constexpr int kLutMaxBits = 12;
+constexpr int kLutPerSplitter = 16;  // LUT words reserved per splitter slot
 
 struct SegDesc {
     uint64_t off;          // absolute element offset of the segment
     uint64_t len;          // number of keys
+    uint64_t lo, hi;       // integer keys: every key of the segment is in [lo, hi]
     uint32_t chunk_begin;  // first chunk in the level's chunk table
     uint32_t nchunks;
-    uint32_t logk;         // K = 1 << logk buckets (2K with equality buckets)
+    uint32_t logk;         // K = 1 << logk buckets
     uint32_t m;            // unique splitters (set by sample_kernel)
-    uint32_t eq;           // three-way classification on
+    uint32_t eq;           // three-way classification on: 2K bins, bin = 2j + (key == s_j)
     uint32_t sp;           // base index of this segment's splitter storage
-    uint32_t hist_base;    // first histogram word; chunk i's row is at
-                           // hist_base + i * 2K (2K bins per row)
-    uint32_t pad;
+    uint32_t hist_base;    // histogram block: bin b, chunk i at hist_base + b*(nchunks+1) + i;
+                           // entry i = nchunks holds the bucket total, then its start
+    uint32_t shift;        // LUT cell = (key - lo) >> shift
+    uint32_t lutbits;      // 2^lutbits LUT cells
+    uint32_t pad[3];
 };
 
 struct ChunkDesc {
@@ -73,6 +89,7 @@ struct LevelCounters {
     uint32_t nfill;
     uint32_t ntasks[kNumClasses];
     uint32_t overflow;  // capacity exceeded somewhere (host reports an error)
+    uint32_t pad;
     unsigned long long nkeys;      // keys in this level's segments (pass ledger)
     unsigned long long task_keys;  // keys handed to the block sorter
     unsigned long long fill_keys;  // keys written by equal-bucket fills
@@ -116,22 +133,25 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
 
 // Append a segment (and its chunk table) to the next level.  Called by one
 // thread.  Returns false on capacity overflow.
-__device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len,
-                                    const PlanParams& p) {
+__device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len, uint64_t lo,
+                                    uint64_t hi, const PlanParams& p) {
     const uint32_t logk = choose_logk(len, p.target, p.log_kmax);
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
+    const uint32_t hwords = (nch + 1) * (2u << logk);
     const uint32_t s = atomicAdd(&nb.cnt->nsegs, 1u);
     const uint32_t sp = atomicAdd(&nb.cnt->nsplit, 1u << logk);
     const uint32_t c0 = atomicAdd(&nb.cnt->nchunks, nch);
-    const uint32_t hb = atomicAdd(&nb.cnt->nhist, nch * (2u << logk));
+    const uint32_t hb = atomicAdd(&nb.cnt->nhist, hwords);
     if (s >= nb.seg_cap || sp + (1u << logk) > nb.split_cap || c0 + nch > nb.chunk_cap ||
-        hb + nch * (2u << logk) > nb.hist_cap) {
+        hb + hwords > nb.hist_cap) {
         atomicExch(&nb.cnt->overflow, 1u);
         return false;
     }
     SegDesc d;
     d.off = off;
     d.len = len;
+    d.lo = lo;
+    d.hi = hi;
     d.chunk_begin = c0;
     d.nchunks = nch;
     d.logk = logk;
@@ -139,7 +159,12 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     d.eq = 0;
     d.sp = sp;
     d.hist_base = hb;
-    d.pad = 0;
+    d.lutbits = min(logk + 4, (uint32_t)kLutMaxBits);
+    const uint64_t span = hi - lo;  // keys in [lo, hi]
+    uint32_t bl = 0;
+    while (bl < 64 && (span >> bl) != 0) ++bl;  // bit length of span
+    d.shift = bl > d.lutbits ? bl - d.lutbits : 0;
+    d.pad[0] = d.pad[1] = d.pad[2] = 0;
     nb.segs[s] = d;
     atomicAdd(&nb.cnt->nkeys, (unsigned long long)len);
     for (uint32_t i = 0; i < nch; ++i) {
@@ -153,22 +178,85 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     return true;
 }
 
-__global__ void init_level_kernel(LevelBufs nb, uint64_t n, PlanParams p) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) emit_segment(nb, 0, n, p);
+__global__ void init_level_kernel(LevelBufs nb, uint64_t n, uint64_t key_max, PlanParams p) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) emit_segment(nb, 0, n, 0, key_max, p);
 }
 
-// Search-tree classification (Eytzinger layout, tree[1..K-1]).  Returns
-// 2j + e where j = #{splitters < key} and e = 1 iff three-way mode is on and
-// key equals splitter j.
-template <class K>
-__device__ __forceinline__ uint32_t classify(const K& key, const K* tree, const K* sorted,
-                                             uint32_t logk, uint32_t m, uint32_t eq) {
-    uint32_t t = 1;
-    for (uint32_t l = 0; l < logk; ++l) t = 2 * t + (KeyTraits<K>::lt(tree[t], key) ? 1u : 0u);
-    const uint32_t j = t - (1u << logk);
-    uint32_t e = 0;
-    if (eq && j < m) e = KeyTraits<K>::eq(key, sorted[j]) ? 1u : 0u;
-    return 2 * j + e;
+// ---------------------------------------------------------------------------
+// Classification
+// ---------------------------------------------------------------------------
+// Shared-memory view of one segment's classifier.
+template <class K, int LOG_KMAX>
+struct ClassifierSmem {
+    static constexpr int KMAX = 1 << LOG_KMAX;
+    K sorted[KMAX];                                           // unique splitters
+    K tree[KeyTraits<K>::kLut ? 1 : KMAX];                    // rec32: Eytzinger tree
+    uint32_t lut[KeyTraits<K>::kLut ? (1 << kLutMaxBits) : 1];  // integers: j_lo | (j_hi-j_lo) << 16
+};
+
+template <class K, int LOG_KMAX, int T>
+__device__ __forceinline__ void load_classifier(ClassifierSmem<K, LOG_KMAX>& c, const SegDesc& d,
+                                                const K* __restrict__ tree_store,
+                                                const K* __restrict__ sorted_store,
+                                                const uint32_t* __restrict__ lut_store) {
+    const uint32_t K_ = 1u << d.logk;
+    for (uint32_t i = threadIdx.x; i < K_; i += T) c.sorted[i] = sorted_store[d.sp + i];
+    if constexpr (KeyTraits<K>::kLut) {
+        const uint32_t nc = 1u << d.lutbits;
+        const uint32_t* src = lut_store + (size_t)d.sp * kLutPerSplitter;
+        for (uint32_t i = threadIdx.x; i < nc; i += T) c.lut[i] = src[i];
+    } else {
+        for (uint32_t i = threadIdx.x; i < K_; i += T) c.tree[i] = tree_store[d.sp + i];
+    }
+}
+
+// Bins of U keys.  bin = j, or 2j + (key == splitter j) with equality buckets.
+template <class K, int LOG_KMAX, int U>
+__device__ __forceinline__ void classify_keys(const K (&key)[U],
+                                              const ClassifierSmem<K, LOG_KMAX>& c,
+                                              const SegDesc& d, uint32_t (&bin)[U]) {
+    using KT = KeyTraits<K>;
+    uint32_t j[U];
+    if constexpr (KT::kLut) {
+        const uint64_t lo = d.lo;
+        const uint32_t shift = d.shift;
+        const uint32_t cmax = (1u << d.lutbits) - 1;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t rel = (uint64_t)KT::bits(key[u]) - lo;
+            const uint32_t cell = (uint32_t)min(rel >> shift, (uint64_t)cmax);
+            const uint32_t e = c.lut[cell];
+            j[u] = e & 0xFFFFu;
+            uint32_t cnt = e >> 16;
+            // finish inside the cell's bucket range: #{sorted[j..j+cnt) < key}
+            while (cnt > 0) {
+                const uint32_t half = cnt >> 1;
+                const bool less = KT::lt(c.sorted[j[u] + half], key[u]);
+                j[u] = less ? j[u] + half + 1 : j[u];
+                cnt = less ? cnt - half - 1 : half;
+            }
+        }
+    } else {
+        uint32_t t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] = 1;
+        for (uint32_t l = 0; l < d.logk; ++l) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) t[u] = 2 * t[u] + (KT::lt(c.tree[t[u]], key[u]) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = t[u] - (1u << d.logk);
+    }
+    if (d.eq) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t jj = j[u] < d.m ? j[u] : 0;
+            bin[u] = 2 * j[u] + ((j[u] < d.m && KT::eq(key[u], c.sorted[jj])) ? 1u : 0u);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) bin[u] = j[u];
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -176,9 +264,12 @@ __device__ __forceinline__ uint32_t classify(const K& key, const K* tree, const 
 // ---------------------------------------------------------------------------
 template <class K, int T, int ITEMS>
 __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __restrict__ src,
-                                                   K* tree_store, K* sorted_store, uint64_t seed) {
+                                                   K* tree_store, K* sorted_store,
+                                                   uint32_t* lut_store, uint64_t seed,
+                                                   uint32_t oversample) {
     using BS = BlockSorter<K, T, ITEMS>;
     using P = SmemPad<K>;
+    using KT = KeyTraits<K>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s = reinterpret_cast<K*>(smem_raw);
     __shared__ uint32_t flags[1024 + 1];
@@ -187,25 +278,28 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
     const uint32_t seg = blockIdx.x;
     const SegDesc d = segs[seg];
     const uint32_t K_ = 1u << d.logk;
+    const int S = (int)min((uint32_t)BS::kCap, max(1024u, oversample * K_));
 
     // Seeded sample with replacement (counter-based SplitMix64 of the sample
     // index; uniform position via a 64x64 high multiply).
     K k[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const uint64_t idx = (uint64_t)threadIdx.x * ITEMS + i;
-        const uint64_t h = sm_mix(seed + (d.off + 1) * kGamma + (idx + 1) * 0xD1B54A32D192ED03ull);
-        const uint64_t pos = __umul64hi(h, d.len);
-        k[i] = src[d.off + pos];
+        const int idx = (int)threadIdx.x * ITEMS + i;
+        if (idx < S) {
+            const uint64_t h = sm_mix(seed + (d.off + 1) * kGamma + (uint64_t)(idx + 1) * 0xD1B54A32D192ED03ull);
+            k[i] = src[d.off + __umul64hi(h, d.len)];
+        } else {
+            k[i] = KT::max_key();
+        }
     }
-    BS::sort(k, s);  // sorted sample of BS::kCap keys in s (padded)
+    BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
 
     // candidate splitter j (0 <= j < K-1): sample quantile (j+1)/K
-    const int S = BS::kCap;
     for (uint32_t j = threadIdx.x; j < K_ - 1; j += T) {
         const int q = (int)(((uint64_t)(j + 1) * S) / K_);
         const K c = s[P::idx(q)];
-        const bool keep = (j == 0) || !KeyTraits<K>::eq(c, s[P::idx((int)(((uint64_t)j * S) / K_))]);
+        const bool keep = (j == 0) || !KT::eq(c, s[P::idx((int)(((uint64_t)j * S) / K_))]);
         flags[j] = keep ? 1u : 0u;
     }
     if (threadIdx.x == 0) flags[K_ - 1] = 0;
@@ -215,16 +309,46 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
     K* sorted = sorted_store + d.sp;
     for (uint32_t j = threadIdx.x; j < K_ - 1; j += T) {
         const int q = (int)(((uint64_t)(j + 1) * S) / K_);
-        const bool keep = (j + 1 < K_ - 1) ? (flags[j + 1] != flags[j]) : (flags[j] != m);
-        if (keep) sorted[flags[j]] = s[P::idx(q)];
+        if (flags[j + 1] != flags[j]) sorted[flags[j]] = s[P::idx(q)];
     }
     __syncthreads();  // sorted[] (global) is visible block-wide after the barrier
-    // Eytzinger tree over sorted[0..m), padded with the maximum key.
-    K* tree = tree_store + d.sp;
-    for (uint32_t t = threadIdx.x + 1; t < K_; t += T) {
-        const uint32_t depth = 31 - __clz(t);
-        const uint32_t rank = ((2 * (t - (1u << depth)) + 1) << (d.logk - 1 - depth)) - 1;
-        tree[t] = rank < m ? sorted[rank] : KeyTraits<K>::max_key();
+    for (uint32_t j = threadIdx.x; j < m; j += T) s[P::idx(j)] = sorted[j];  // compacted copy
+    __syncthreads();
+    if constexpr (KT::kLut) {
+        // LUT cell c covers keys [lo + c<<shift, lo + (c+1)<<shift - 1] within [lo, hi]
+        const uint32_t nc = 1u << d.lutbits;
+        uint32_t* lut = lut_store + (size_t)d.sp * kLutPerSplitter;
+        for (uint32_t c = threadIdx.x; c < nc; c += T) {
+            const uint64_t cmin = d.lo + ((uint64_t)c << d.shift);
+            uint64_t cmax = cmin + (((uint64_t)1 << d.shift) - 1);
+            if (c == nc - 1 || cmax > d.hi || cmax < cmin) cmax = d.hi;
+            // #{sorted < v} by binary search over the m unique splitters
+            uint32_t jl = 0, jh = 0;
+            for (int w = 0; w < 2; ++w) {
+                const uint64_t v = w == 0 ? cmin : cmax;
+                uint32_t lo2 = 0, cnt = m;
+                while (cnt > 0) {
+                    const uint32_t half = cnt >> 1;
+                    if ((uint64_t)KT::bits(s[P::idx(lo2 + half)]) < v) {
+                        lo2 += half + 1;
+                        cnt -= half + 1;
+                    } else {
+                        cnt = half;
+                    }
+                }
+                if (w == 0) jl = lo2;
+                else jh = lo2;
+            }
+            lut[c] = jl | ((jh - jl) << 16);
+        }
+    } else {
+        // Eytzinger tree over sorted[0..m), padded with the maximum key.
+        K* tree = tree_store + d.sp;
+        for (uint32_t t = threadIdx.x + 1; t < K_; t += T) {
+            const uint32_t depth = 31 - __clz(t);
+            const uint32_t rank = ((2 * (t - (1u << depth)) + 1) << (d.logk - 1 - depth)) - 1;
+            tree[t] = rank < m ? s[P::idx(rank)] : KT::max_key();
+        }
     }
     if (threadIdx.x == 0) {
         segs[seg].m = m;
@@ -235,50 +359,91 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
 // ---------------------------------------------------------------------------
 // K2: per-chunk bucket histogram.
 // ---------------------------------------------------------------------------
-template <class K, int T, int LOG_KMAX>
+template <class K, int T, int U, int LOG_KMAX>
 __global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ segs,
                                                   const ChunkDesc* __restrict__ chunks,
                                                   const K* __restrict__ src,
                                                   const K* __restrict__ tree_store,
                                                   const K* __restrict__ sorted_store,
-                                                  uint32_t* __restrict__ chunk_hist) {
+                                                  const uint32_t* __restrict__ lut_store,
+                                                  uint32_t* __restrict__ hist) {
     constexpr int KMAX = 1 << LOG_KMAX;
-    constexpr int NB = 2 * KMAX;
-    __shared__ K tree[KMAX];
-    __shared__ K sorted[KMAX];
-    __shared__ uint32_t hist[NB];
+    __shared__ ClassifierSmem<K, LOG_KMAX> cls;
+    __shared__ uint32_t shist[2 * KMAX];
     const ChunkDesc c = chunks[blockIdx.x];
     const SegDesc d = segs[c.seg];
-    const uint32_t K_ = 1u << d.logk;
-    for (uint32_t i = threadIdx.x; i < K_; i += T) {
-        tree[i] = tree_store[d.sp + i];
-        sorted[i] = sorted_store[d.sp + i];
-    }
-    for (uint32_t i = threadIdx.x; i < 2 * K_; i += T) hist[i] = 0;
+    const uint32_t nb = (1u << d.logk) << d.eq;
+    load_classifier<K, LOG_KMAX, T>(cls, d, tree_store, sorted_store, lut_store);
+    for (uint32_t i = threadIdx.x; i < nb; i += T) shist[i] = 0;
     __syncthreads();
-    constexpr int U = 8;
-    uint64_t i = c.begin + threadIdx.x;
-    for (; i + (U - 1) * T < c.end; i += U * T) {
+    const K* p = src + c.begin;
+    const uint32_t len = (uint32_t)(c.end - c.begin);
+    constexpr uint32_t STEP = (uint32_t)T * U;
+    uint32_t base = 0;
+    for (; base + STEP <= len; base += STEP) {  // full tiles: no bounds checks
         K k[U];
+        uint32_t bin[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) k[u] = src[i + (uint64_t)u * T];
+        for (int u = 0; u < U; ++u) k[u] = p[base + u * T + threadIdx.x];
+        classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
+#pragma unroll
+        for (int u = 0; u < U; ++u) atomicAdd(&shist[bin[u]], 1u);
+    }
+    if (base < len) {
+        K k[U];
+        uint32_t bin[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t i = base + u * T + threadIdx.x;
+            k[u] = i < len ? p[i] : KeyTraits<K>::max_key();
+        }
+        classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            atomicAdd(&hist[classify<K>(k[u], tree, sorted, d.logk, d.m, d.eq)], 1u);
+            if (base + u * T + threadIdx.x < len) atomicAdd(&shist[bin[u]], 1u);
     }
-    for (; i < c.end; i += T)
-        atomicAdd(&hist[classify<K>(src[i], tree, sorted, d.logk, d.m, d.eq)], 1u);
     __syncthreads();
-    uint32_t* row = chunk_hist + d.hist_base + (size_t)(blockIdx.x - d.chunk_begin) * (2 * K_);
-    for (uint32_t b = threadIdx.x; b < 2 * K_; b += T) row[b] = hist[b];
+    const uint32_t ci = blockIdx.x - d.chunk_begin;
+    const uint32_t stride = d.nchunks + 1;
+    for (uint32_t b = threadIdx.x; b < nb; b += T) hist[d.hist_base + b * stride + ci] = shist[b];
 }
 
 // ---------------------------------------------------------------------------
-// K3: per-segment plan: totals, bucket starts, per-chunk offsets, children.
+// K3a: per (segment, bin): exclusive prefix over the segment's chunks (in
+// place) and the bin total (entry nchunks).  One warp per bin.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__ segs,
+                                                     uint32_t* __restrict__ hist) {
+    const SegDesc d = segs[blockIdx.x];
+    const uint32_t nb = (1u << d.logk) << d.eq;
+    const int lane = threadIdx.x & 31;
+    const uint32_t stride = d.nchunks + 1;
+    for (uint32_t b = blockIdx.y * 16 + (threadIdx.x >> 5); b < nb; b += gridDim.y * 16) {
+        uint32_t* col = hist + d.hist_base + b * stride;
+        uint32_t carry = 0;
+        for (uint32_t c0 = 0; c0 < d.nchunks; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            const uint32_t v = c < d.nchunks ? col[c] : 0;
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (c < d.nchunks) col[c] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) col[d.nchunks] = carry;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: per segment: bucket starts and child work.
 // ---------------------------------------------------------------------------
 template <class K, int T, int LOG_KMAX>
 __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ segs,
-                                                 uint32_t* __restrict__ chunk_hist,
+                                                 uint32_t* __restrict__ hist,
+                                                 const K* __restrict__ sorted_store,
                                                  LevelBufs next, PlanParams p,
                                                  SortTask* __restrict__ tasks,
                                                  FillTask* __restrict__ fills,
@@ -289,29 +454,21 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     __shared__ uint32_t warp_sums[32];
     const uint32_t seg = blockIdx.x;
     const SegDesc d = segs[seg];
-    const uint32_t nb = 2u << d.logk;
+    const uint32_t nb = (1u << d.logk) << d.eq;
+    const uint32_t stride = d.nchunks + 1;
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
-        uint32_t sum = 0;
-        const uint32_t* col = chunk_hist + d.hist_base + b;
-#pragma unroll 8
-        for (uint32_t c = 0; c < d.nchunks; ++c) sum += col[(size_t)c * nb];
-        tot[b] = sum;
-        start[b] = sum;
+        const uint32_t v = hist[d.hist_base + b * stride + d.nchunks];
+        tot[b] = v;
+        start[b] = v;
     }
     __syncthreads();
     block_exclusive_scan_smem<T>(start, (int)nb, warp_sums);
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
-        uint32_t run = start[b];
-        uint32_t* col = chunk_hist + d.hist_base + b;
-        for (uint32_t c = 0; c < d.nchunks; ++c) {
-            const uint32_t v = col[(size_t)c * nb];
-            col[(size_t)c * nb] = run;
-            run += v;
-        }
+        hist[d.hist_base + b * stride + d.nchunks] = start[b];
         const uint32_t len = tot[b];
         if (len == 0) continue;
         const uint64_t off = d.off + start[b];
-        if (b & 1) {  // equal-key bucket: already final when it landed in the caller's buffer
+        if (d.eq && (b & 1)) {  // equal-key bucket: final once it is in the caller's buffer
             if (!p.dst_is_a) {
                 const uint32_t f = atomicAdd(&cur_cnt->nfill, 1u);
                 if (f < p.fill_cap) {
@@ -342,74 +499,86 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 atomicExch(&cur_cnt->overflow, 1u);
             }
         } else {
-            emit_segment(next, off, len, p);
+            // child key range: (splitter j-1, splitter j] within the parent's [lo, hi]
+            const uint32_t j = d.eq ? (b >> 1) : b;
+            const K* sp = sorted_store + d.sp;
+            uint64_t clo = d.lo, chi = d.hi;
+            if (KeyTraits<K>::kLut) {
+                if (j > 0) clo = KeyTraits<K>::bits(sp[j - 1]) + 1;
+                if (j < d.m) chi = KeyTraits<K>::bits(sp[j]);
+            }
+            emit_segment(next, off, len, clo, chi, p);
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// K4: scatter.  Tile = T * ITEMS keys; one CTA walks the tiles of one chunk.
+// K4: scatter.  Tile = T * U keys; one CTA walks the tiles of one chunk.
 // ---------------------------------------------------------------------------
-template <class K, int T, int ITEMS, int LOG_KMAX>
+template <class K, int T, int U, int LOG_KMAX>
 struct ScatterSmem {
     static constexpr int KMAX = 1 << LOG_KMAX;
     static constexpr int NB = 2 * KMAX;
-    static constexpr int TILE = T * ITEMS;
-    K tree[KMAX];
-    K sorted[KMAX];
+    static constexpr int TILE = T * U;
+    ClassifierSmem<K, LOG_KMAX> cls;
     K stage[TILE];
     uint16_t stage_bin[TILE];
     uint32_t hist[NB];
     uint32_t start[NB];
-    uint64_t gdst[NB];
-    uint32_t cursor[NB];
+    uint32_t gdst[NB];    // destination of staged slot i is gdst[bin] + i (segment-relative)
+    uint32_t cursor[NB];  // segment-relative write cursor per bucket
     uint32_t warp_sums[32];
 };
 
-template <class K, int T, int ITEMS, int LOG_KMAX>
+template <class K, int T, int U, int LOG_KMAX>
 __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ segs,
                                                     const ChunkDesc* __restrict__ chunks,
                                                     const K* __restrict__ src, K* __restrict__ dst,
                                                     const K* __restrict__ tree_store,
                                                     const K* __restrict__ sorted_store,
-                                                    const uint32_t* __restrict__ chunk_off) {
-    using SM = ScatterSmem<K, T, ITEMS, LOG_KMAX>;
-    constexpr int TILE = SM::TILE;
+                                                    const uint32_t* __restrict__ lut_store,
+                                                    const uint32_t* __restrict__ hist) {
+    using SM = ScatterSmem<K, T, U, LOG_KMAX>;
+    constexpr uint32_t TILE = SM::TILE;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
     const ChunkDesc c = chunks[blockIdx.x];
     const SegDesc d = segs[c.seg];
-    const uint32_t K_ = 1u << d.logk;
-    const uint32_t nb = 2 * K_;
-    for (uint32_t i = threadIdx.x; i < K_; i += T) {
-        sm.tree[i] = tree_store[d.sp + i];
-        sm.sorted[i] = sorted_store[d.sp + i];
-    }
-    const uint32_t* row = chunk_off + d.hist_base + (size_t)(blockIdx.x - d.chunk_begin) * nb;
+    const uint32_t nb = (1u << d.logk) << d.eq;
+    load_classifier<K, LOG_KMAX, T>(sm.cls, d, tree_store, sorted_store, lut_store);
+    const uint32_t ci = blockIdx.x - d.chunk_begin;
+    const uint32_t stride = d.nchunks + 1;
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
-        sm.cursor[b] = row[b];
+        const uint32_t* col = hist + d.hist_base + b * stride;
+        sm.cursor[b] = col[d.nchunks] + col[ci];  // bucket start + chunk prefix
         sm.hist[b] = 0;
     }
     __syncthreads();
 
-    for (uint64_t t0 = c.begin; t0 < c.end; t0 += TILE) {
-        const int m = (int)min((uint64_t)TILE, c.end - t0);
-        K k[ITEMS];
-        uint32_t bin[ITEMS];
-        uint32_t rank[ITEMS];
+    const K* p = src + c.begin;
+    K* out = dst + d.off;
+    const uint32_t len = (uint32_t)(c.end - c.begin);
+    for (uint32_t t0 = 0; t0 < len; t0 += TILE) {
+        const uint32_t m = min(TILE, len - t0);
+        K k[U];
+        uint32_t bin[U];
+        if (m == TILE) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const int li = i * T + threadIdx.x;
-            if (li < m) k[i] = src[t0 + li];
-        }
+            for (int u = 0; u < U; ++u) k[u] = p[t0 + u * T + threadIdx.x];
+        } else {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const int li = i * T + threadIdx.x;
-            if (li < m) {
-                bin[i] = classify<K>(k[i], sm.tree, sm.sorted, d.logk, d.m, d.eq);
-                rank[i] = atomicAdd(&sm.hist[bin[i]], 1u);
+            for (int u = 0; u < U; ++u) {
+                const uint32_t li = u * T + threadIdx.x;
+                k[u] = li < m ? p[t0 + li] : KeyTraits<K>::max_key();
             }
+        }
+        classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
+        // rank within the tile's bucket; pack (bin, rank) into one word
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t li = u * T + threadIdx.x;
+            if (li < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
         }
         __syncthreads();
         for (uint32_t b = threadIdx.x; b < nb; b += T) sm.start[b] = sm.hist[b];
@@ -417,22 +586,23 @@ __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ 
         block_exclusive_scan_smem<T>(sm.start, (int)nb, sm.warp_sums);
         for (uint32_t b = threadIdx.x; b < nb; b += T) {
             const uint32_t h = sm.hist[b];
-            sm.gdst[b] = d.off + sm.cursor[b] - sm.start[b];
+            sm.gdst[b] = sm.cursor[b] - sm.start[b];
             sm.cursor[b] += h;
             sm.hist[b] = 0;
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const int li = i * T + threadIdx.x;
+        for (int u = 0; u < U; ++u) {
+            const uint32_t li = u * T + threadIdx.x;
             if (li < m) {
-                const uint32_t pos = sm.start[bin[i]] + rank[i];
-                sm.stage[pos] = k[i];
-                sm.stage_bin[pos] = (uint16_t)bin[i];
+                const uint32_t b = bin[u] >> 16;
+                const uint32_t pos = sm.start[b] + (bin[u] & 0xFFFFu);
+                sm.stage[pos] = k[u];
+                sm.stage_bin[pos] = (uint16_t)b;
             }
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < m; i += T) dst[sm.gdst[sm.stage_bin[i]] + i] = sm.stage[i];
+        for (uint32_t i = threadIdx.x; i < m; i += T) out[sm.gdst[sm.stage_bin[i]] + i] = sm.stage[i];
         __syncthreads();
     }
 }
