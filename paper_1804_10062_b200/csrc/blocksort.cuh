@@ -111,6 +111,48 @@ __device__ __forceinline__ void serial_merge_smem(const K* s, int ai, int aend, 
     }
 }
 
+// min (lower = true) or max of a and b.
+template <class K>
+__device__ __forceinline__ K select_minmax(const K& a, const K& b, bool lower) {
+    const bool b_less = KeyTraits<K>::lt(b, a);
+    return (b_less == lower) ? b : a;
+}
+
+// One warp-level merge round: every pair of ascending runs of `lr` lanes x
+// ITEMS keys (lane-blocked) becomes one ascending run of 2*lr lanes.  Bitonic
+// merge in its all-ascending form: a flip stage pairs position p with its
+// mirror p ^ (2*lr*ITEMS - 1), then half-cleaners at distances lr*ITEMS/2 ..
+// 1.  Cross-lane distances use register shuffles, in-lane distances plain
+// compare-and-swap; no shared memory and no barriers.
+template <class K, int ITEMS>
+__device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
+    using KT = KeyTraits<K>;
+    const int lane = threadIdx.x & 31;
+    {
+        const int fm = 2 * lr - 1;
+        const bool lower = (lane & lr) == 0;
+#pragma unroll
+        for (int j = 0; j < ITEMS / 2; ++j) {
+            const K y0 = KT::shfl_xor(k[ITEMS - 1 - j], fm);
+            const K y1 = KT::shfl_xor(k[j], fm);
+            k[j] = select_minmax(k[j], y0, lower);
+            k[ITEMS - 1 - j] = select_minmax(k[ITEMS - 1 - j], y1, lower);
+        }
+    }
+#pragma unroll 1
+    for (int s = lr >> 1; s >= 1; s >>= 1) {
+        const bool lower = (lane & s) == 0;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) k[j] = select_minmax(k[j], KT::shfl_xor(k[j], s), lower);
+    }
+#pragma unroll
+    for (int s = ITEMS / 2; s >= 1; s >>= 1) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+            if ((j & s) == 0) KT::cas(k[j], k[j + s]);
+    }
+}
+
 template <class K, int T, int ITEMS>
 struct BlockSorter {
     static constexpr int kThreads = T;
@@ -124,13 +166,19 @@ struct BlockSorter {
     // Keys rounded up to whole threads: threads at or beyond mp / ITEMS own
     // no keys and only take part in the barriers.
     __device__ __forceinline__ static int padded(int m) { return (m + ITEMS - 1) / ITEMS * ITEMS; }
+    // Keys rounded up to whole warps (the warp-level rounds need all lanes).
+    static constexpr int kWarpKeys = 32 * ITEMS;
+    __device__ __forceinline__ static int warp_padded(int m) {
+        const int w = (m + kWarpKeys - 1) / kWarpKeys * kWarpKeys;
+        return w < kCap ? w : kCap;
+    }
 
     // Coalesced (striped) load of m <= kCap keys into shared memory, padding
-    // up to a whole thread with the maximum key.
+    // up to a whole warp with the maximum key.
     __device__ __forceinline__ static void load_striped(const K* __restrict__ src, int m, K* s) {
-        const int mp = padded(m);
+        const int mw = warp_padded(m);
 #pragma unroll 4
-        for (int i = threadIdx.x; i < mp; i += T) s[P::idx(i)] = i < m ? src[i] : KT::max_key();
+        for (int i = threadIdx.x; i < mw; i += T) s[P::idx(i)] = i < m ? src[i] : KT::max_key();
     }
     __device__ __forceinline__ static void store_blocked(const K (&k)[ITEMS], K* s) {
         const int base = threadIdx.x * ITEMS;
@@ -156,9 +204,15 @@ struct BlockSorter {
         const int mp = padded(m);
         const int out = threadIdx.x * ITEMS;
         const bool owner = out < mp;
-        if (owner) register_sort<K, ITEMS>(k);
+        // warps holding any key (their other lanes hold maximum-key padding)
+        const bool warp_active = (int)(threadIdx.x & ~31u) * ITEMS < mp;
+        if (warp_active) {
+            register_sort<K, ITEMS>(k);
 #pragma unroll 1
-        for (int run = ITEMS; run < mp; run <<= 1) {
+            for (int lr = 1; lr < 32 && lr * ITEMS < mp; lr <<= 1) warp_merge_round<K, ITEMS>(k, lr);
+        }
+#pragma unroll 1
+        for (int run = kWarpKeys; run < mp; run <<= 1) {
             if (owner) store_blocked(k, s);
             __syncthreads();
             if (owner) {
@@ -181,7 +235,7 @@ struct BlockSorter {
         load_striped(src, m, s);
         __syncthreads();
         K k[ITEMS];
-        if ((int)threadIdx.x * ITEMS < padded(m)) load_blocked(k, s);
+        if ((int)threadIdx.x * ITEMS < warp_padded(m)) load_blocked(k, s);
         __syncthreads();
         sort(k, s, m);
         store_striped(dst, m, s);

@@ -34,9 +34,13 @@ struct KeyTraits<uint32_t> {
         b = hi;
     }
     __device__ __forceinline__ static uint64_t hash(uint32_t a) { return a; }
+    __device__ __forceinline__ static uint32_t shfl_xor(uint32_t a, int m) {
+        return __shfl_xor_sync(0xffffffffu, a, m);
+    }
     // bucket lookup table (LUT) support: keys are unsigned integers
     static constexpr bool kLut = true;
-    __device__ __forceinline__ static uint64_t bits(uint32_t a) { return a; }
+    using UInt = uint32_t;
+    __device__ __forceinline__ static uint32_t bits(uint32_t a) { return a; }
 };
 
 template <>
@@ -52,7 +56,11 @@ struct KeyTraits<uint64_t> {
         b = hi;
     }
     __device__ __forceinline__ static uint64_t hash(uint64_t a) { return a; }
+    __device__ __forceinline__ static uint64_t shfl_xor(uint64_t a, int m) {
+        return __shfl_xor_sync(0xffffffffu, a, m);
+    }
     static constexpr bool kLut = true;
+    using UInt = uint64_t;
     __device__ __forceinline__ static uint64_t bits(uint64_t a) { return a; }
 };
 
@@ -85,11 +93,18 @@ struct KeyTraits<Rec32> {
         a = lo;
         b = hi;
     }
+    __device__ __forceinline__ static Rec32 shfl_xor(const Rec32& a, int m) {
+        Rec32 r;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r.w[i] = __shfl_xor_sync(0xffffffffu, a.w[i], m);
+        return r;
+    }
     __device__ __forceinline__ static uint64_t hash(const Rec32& a) {
         return a.w[0] * 0x9E3779B97F4A7C15ull ^ a.w[1] * 0xBF58476D1CE4E5B9ull ^
                a.w[2] * 0x94D049BB133111EBull ^ a.w[3];
     }
     static constexpr bool kLut = false;  // classified by the search tree only
+    using UInt = uint64_t;
     __device__ __forceinline__ static uint64_t bits(const Rec32& a) { return a.w[0]; }
 };
 

@@ -71,20 +71,20 @@ template <class K>
 struct Tune;
 template <>
 struct Tune<uint32_t> {
-    static constexpr int LOGKMAX = 10;
+    static constexpr int LOGKMAX = 9;
     static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
     static constexpr int ST = 512, SI = 16;  // sampler
-    static constexpr int XT = 512, XI = 16;  // scatter tile
-    static constexpr int CT = 512, CU = 16;  // count
+    static constexpr int XT = 256, XI = 16;  // scatter tile
+    static constexpr int CT = 256, CU = 16;  // count
     static constexpr int MT = 512, MI = 16;  // merge pass
 };
 template <>
 struct Tune<uint64_t> {
-    static constexpr int LOGKMAX = 10;
+    static constexpr int LOGKMAX = 9;
     static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
     static constexpr int ST = 512, SI = 16;
-    static constexpr int XT = 512, XI = 8;
-    static constexpr int CT = 512, CU = 8;
+    static constexpr int XT = 256, XI = 16;
+    static constexpr int CT = 256, CU = 8;
     static constexpr int MT = 512, MI = 16;
 };
 template <>
@@ -189,8 +189,8 @@ static WsLayout make_layout(size_t n) {
     constexpr uint64_t target = cap / 2;
     constexpr uint64_t tile = (uint64_t)TU::XT * TU::XI;
     WsLayout L;
-    // ~4 chunks per SM on a 148-SM part at level 0
-    uint64_t ch = (n + 591) / 592;
+    // ~8 chunks per SM on a 148-SM part at level 0
+    uint64_t ch = (n + 1183) / 1184;
     ch = std::max<uint64_t>(tile, align_up(ch, tile));
     L.chunk_elems = ch;
     L.seg_cap = (uint32_t)(n / cap + 2);

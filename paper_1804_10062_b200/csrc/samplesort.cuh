@@ -218,22 +218,36 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
     using KT = KeyTraits<K>;
     uint32_t j[U];
     if constexpr (KT::kLut) {
-        const uint64_t lo = d.lo;
+        using UI = typename KT::UInt;
+        const UI lo = (UI)d.lo;
         const uint32_t shift = d.shift;
-        const uint32_t cmax = (1u << d.lutbits) - 1;
+        const UI cmax = (UI)((1u << d.lutbits) - 1);
+        uint32_t wide = 0;  // keys whose cell straddles two or more splitters
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint64_t rel = (uint64_t)KT::bits(key[u]) - lo;
-            const uint32_t cell = (uint32_t)min(rel >> shift, (uint64_t)cmax);
+            const UI rel = KT::bits(key[u]) - lo;
+            const uint32_t cell = (uint32_t)min((UI)(rel >> shift), cmax);
             const uint32_t e = c.lut[cell];
-            j[u] = e & 0xFFFFu;
-            uint32_t cnt = e >> 16;
-            // finish inside the cell's bucket range: #{sorted[j..j+cnt) < key}
-            while (cnt > 0) {
-                const uint32_t half = cnt >> 1;
-                const bool less = KT::lt(c.sorted[j[u] + half], key[u]);
-                j[u] = less ? j[u] + half + 1 : j[u];
-                cnt = less ? cnt - half - 1 : half;
+            const uint32_t cnt = e >> 16;
+            // branch-free finish for cells straddling at most one splitter
+            const uint32_t j0 = e & 0xFFFFu;
+            j[u] = j0 + ((cnt != 0 && KT::lt(c.sorted[j0], key[u])) ? 1u : 0u);
+            wide |= (cnt > 1 ? 1u : 0u) << u;
+        }
+        if (wide) {  // rare: binary search #{sorted[j0 .. j0+cnt) < key}
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (!((wide >> u) & 1u)) continue;
+                const UI rel = KT::bits(key[u]) - lo;
+                const uint32_t e = c.lut[(uint32_t)min((UI)(rel >> shift), cmax)];
+                uint32_t jj = e & 0xFFFFu, cnt = e >> 16;
+                while (cnt > 0) {
+                    const uint32_t half = cnt >> 1;
+                    const bool less = KT::lt(c.sorted[jj + half], key[u]);
+                    jj = less ? jj + half + 1 : jj;
+                    cnt = less ? cnt - half - 1 : half;
+                }
+                j[u] = jj;
             }
         }
     } else {
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ se
     load_classifier<K, LOG_KMAX, T>(cls, d, tree_store, sorted_store, lut_store);
     for (uint32_t i = threadIdx.x; i < nb; i += T) shist[i] = 0;
     __syncthreads();
-    const K* p = src + c.begin;
+    const K* p = src + c.begin + threadIdx.x;
     const uint32_t len = (uint32_t)(c.end - c.begin);
     constexpr uint32_t STEP = (uint32_t)T * U;
     uint32_t base = 0;
@@ -384,23 +398,24 @@ __global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ se
         K k[U];
         uint32_t bin[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) k[u] = p[base + u * T + threadIdx.x];
+        for (int u = 0; u < U; ++u) k[u] = p[base + u * T];
         classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
 #pragma unroll
         for (int u = 0; u < U; ++u) atomicAdd(&shist[bin[u]], 1u);
     }
     if (base < len) {
+        const uint32_t rem = len - base;
         K k[U];
         uint32_t bin[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const uint32_t i = base + u * T + threadIdx.x;
-            k[u] = i < len ? p[i] : KeyTraits<K>::max_key();
+            const uint32_t i = u * T + threadIdx.x;
+            k[u] = i < rem ? p[base + u * T] : KeyTraits<K>::max_key();
         }
         classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (base + u * T + threadIdx.x < len) atomicAdd(&shist[bin[u]], 1u);
+            if (u * T + threadIdx.x < rem) atomicAdd(&shist[bin[u]], 1u);
     }
     __syncthreads();
     const uint32_t ci = blockIdx.x - d.chunk_begin;
@@ -519,16 +534,123 @@ template <class K, int T, int U, int LOG_KMAX>
 struct ScatterSmem {
     static constexpr int KMAX = 1 << LOG_KMAX;
     static constexpr int NB = 2 * KMAX;
+    static constexpr int BPT = NB / T;  // bins owned by each thread in the scan
+    static_assert(NB % T == 0 && (BPT == 1 || BPT == 2 || BPT == 4), "bins per thread");
     static constexpr int TILE = T * U;
     ClassifierSmem<K, LOG_KMAX> cls;
     K stage[TILE];
     uint16_t stage_bin[TILE];
-    uint32_t hist[NB];
-    uint32_t start[NB];
-    uint32_t gdst[NB];    // destination of staged slot i is gdst[bin] + i (segment-relative)
-    uint32_t cursor[NB];  // segment-relative write cursor per bucket
-    uint32_t warp_sums[32];
+    alignas(16) uint32_t hist[NB];
+    alignas(16) uint32_t start[NB];
+    alignas(16) uint32_t gdst[NB];  // destination of staged slot i is gdst[bin] + i (segment-relative)
+    uint32_t warp_sums[T / 32];
 };
+
+template <int N>
+struct VecU32;
+template <>
+struct VecU32<1> {
+    using type = uint32_t;
+};
+template <>
+struct VecU32<2> {
+    using type = uint2;
+};
+template <>
+struct VecU32<4> {
+    using type = uint4;
+};
+template <int N>
+__device__ __forceinline__ void vec_load(const uint32_t* p, uint32_t (&v)[N]) {
+    const typename VecU32<N>::type x = *reinterpret_cast<const typename VecU32<N>::type*>(p);
+    memcpy(v, &x, sizeof(x));
+}
+template <int N>
+__device__ __forceinline__ void vec_store(uint32_t* p, const uint32_t (&v)[N]) {
+    typename VecU32<N>::type x;
+    memcpy(&x, v, sizeof(x));
+    *reinterpret_cast<typename VecU32<N>::type*>(p) = x;
+}
+
+// One tile of m keys (m == T*U when FULL): classify, rank within the tile's
+// bucket (shared-memory counter), exclusive scan of the tile histogram (each
+// thread owns BPT consecutive bins and keeps their write cursors in
+// registers), group by bucket in shared memory, then write every bucket run
+// with coalesced stores.
+template <class K, int T, int U, int LOG_KMAX, bool FULL>
+__device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm, const SegDesc& d,
+                                             const K* __restrict__ p, uint32_t m,
+                                             K* __restrict__ out,
+                                             uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT]) {
+    using SM = ScatterSmem<K, T, U, LOG_KMAX>;
+    constexpr int BPT = SM::BPT;
+    const uint32_t tid = threadIdx.x;
+    K k[U];
+    uint32_t bin[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t li = u * T + tid;
+        if (FULL) k[u] = p[li];
+        else k[u] = li < m ? p[li] : KeyTraits<K>::max_key();
+    }
+    classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
+    // rank within the tile's bucket; pack (bin, rank) into one word
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (FULL || u * T + tid < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
+    }
+    __syncthreads();
+    {  // block exclusive scan over all NB bins, BPT per thread
+        uint32_t h[BPT];
+        vec_load<BPT>(&sm.hist[tid * BPT], h);
+        uint32_t local = 0;
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) local += h[i];
+        const uint32_t lane = tid & 31, wid = tid >> 5;
+        uint32_t x = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) sm.warp_sums[wid] = x;
+        __syncthreads();
+        uint32_t excl = x - local;
+#pragma unroll
+        for (int w = 0; w < T / 32; ++w) excl += (w < (int)wid) ? sm.warp_sums[w] : 0u;
+        uint32_t st[BPT], gd[BPT], z[BPT];
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            st[i] = excl;
+            gd[i] = cursor[i] - excl;
+            cursor[i] += h[i];
+            excl += h[i];
+            z[i] = 0;
+        }
+        vec_store<BPT>(&sm.start[tid * BPT], st);
+        vec_store<BPT>(&sm.gdst[tid * BPT], gd);
+        vec_store<BPT>(&sm.hist[tid * BPT], z);
+    }
+    __syncthreads();
+    K* stage = sm.stage;
+    uint16_t* sbin = sm.stage_bin;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (FULL || u * T + tid < m) {
+            const uint32_t b = bin[u] >> 16;
+            const uint32_t pos = sm.start[b] + (bin[u] & 0xFFFFu);
+            stage[pos] = k[u];
+            sbin[pos] = (uint16_t)b;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const uint32_t i = u * T + tid;
+        if (FULL || i < m) out[sm.gdst[sbin[i]] + i] = stage[i];
+    }
+    __syncthreads();
+}
 
 template <class K, int T, int U, int LOG_KMAX>
 __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ segs,
@@ -540,6 +662,7 @@ __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ 
                                                     const uint32_t* __restrict__ hist) {
     using SM = ScatterSmem<K, T, U, LOG_KMAX>;
     constexpr uint32_t TILE = SM::TILE;
+    constexpr int BPT = SM::BPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
 
@@ -549,9 +672,15 @@ __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ 
     load_classifier<K, LOG_KMAX, T>(sm.cls, d, tree_store, sorted_store, lut_store);
     const uint32_t ci = blockIdx.x - d.chunk_begin;
     const uint32_t stride = d.nchunks + 1;
-    for (uint32_t b = threadIdx.x; b < nb; b += T) {
-        const uint32_t* col = hist + d.hist_base + b * stride;
-        sm.cursor[b] = col[d.nchunks] + col[ci];  // bucket start + chunk prefix
+    uint32_t cursor[BPT];
+#pragma unroll
+    for (int i = 0; i < BPT; ++i) {
+        const uint32_t b = threadIdx.x * BPT + i;
+        cursor[i] = 0;
+        if (b < nb) {
+            const uint32_t* col = hist + d.hist_base + b * stride;
+            cursor[i] = col[d.nchunks] + col[ci];  // bucket start + chunk prefix
+        }
         sm.hist[b] = 0;
     }
     __syncthreads();
@@ -559,52 +688,10 @@ __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ 
     const K* p = src + c.begin;
     K* out = dst + d.off;
     const uint32_t len = (uint32_t)(c.end - c.begin);
-    for (uint32_t t0 = 0; t0 < len; t0 += TILE) {
-        const uint32_t m = min(TILE, len - t0);
-        K k[U];
-        uint32_t bin[U];
-        if (m == TILE) {
-#pragma unroll
-            for (int u = 0; u < U; ++u) k[u] = p[t0 + u * T + threadIdx.x];
-        } else {
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const uint32_t li = u * T + threadIdx.x;
-                k[u] = li < m ? p[t0 + li] : KeyTraits<K>::max_key();
-            }
-        }
-        classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
-        // rank within the tile's bucket; pack (bin, rank) into one word
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t li = u * T + threadIdx.x;
-            if (li < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
-        }
-        __syncthreads();
-        for (uint32_t b = threadIdx.x; b < nb; b += T) sm.start[b] = sm.hist[b];
-        __syncthreads();
-        block_exclusive_scan_smem<T>(sm.start, (int)nb, sm.warp_sums);
-        for (uint32_t b = threadIdx.x; b < nb; b += T) {
-            const uint32_t h = sm.hist[b];
-            sm.gdst[b] = sm.cursor[b] - sm.start[b];
-            sm.cursor[b] += h;
-            sm.hist[b] = 0;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const uint32_t li = u * T + threadIdx.x;
-            if (li < m) {
-                const uint32_t b = bin[u] >> 16;
-                const uint32_t pos = sm.start[b] + (bin[u] & 0xFFFFu);
-                sm.stage[pos] = k[u];
-                sm.stage_bin[pos] = (uint16_t)b;
-            }
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < m; i += T) out[sm.gdst[sm.stage_bin[i]] + i] = sm.stage[i];
-        __syncthreads();
-    }
+    uint32_t t0 = 0;
+    for (; t0 + TILE <= len; t0 += TILE)
+        scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
+    if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
 }
 
 // Equal-key buckets that landed in the workspace: write the splitter value.
