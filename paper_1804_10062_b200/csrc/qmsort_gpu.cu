@@ -20,6 +20,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
@@ -174,6 +175,23 @@ static cudaError_t allow_smem(const void* fn, size_t bytes) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Grid size of a persistent kernel: resident CTAs per SM x SMs (cached).
+static unsigned resident_grid(const void* fn, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, unsigned> cache;
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(fn);
+    if (it != cache.end()) return it->second;
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const unsigned r = (unsigned)(per_sm * sms);
+    cache[fn] = r;
+    return r;
+}
+
 struct WsLayout {
     size_t b_off = 0, segs_off[2] = {0, 0}, chunks_off[2] = {0, 0}, cnt_off[2] = {0, 0};
     size_t tree_off[2] = {0, 0}, sorted_off[2] = {0, 0}, lut_off[2] = {0, 0};
@@ -189,9 +207,8 @@ static WsLayout make_layout(size_t n) {
     constexpr uint64_t target = cap / 2;
     constexpr uint64_t tile = (uint64_t)TU::XT * TU::XI;
     WsLayout L;
-    // ~8 chunks per SM on a 148-SM part at level 0
-    uint64_t ch = (n + 1183) / 1184;
-    ch = std::max<uint64_t>(tile, align_up(ch, tile));
+    // chunks of 16 tiles, dispensed dynamically to persistent CTAs
+    const uint64_t ch = tile * 16;
     L.chunk_elems = ch;
     L.seg_cap = (uint32_t)(n / cap + 2);
     L.chunk_cap = (uint32_t)(L.seg_cap + n / ch + 2);
@@ -320,6 +337,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
+    auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
+    const unsigned scatter_grid = resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM));
+    const unsigned count_grid = resident_grid((const void*)count_fn, TU::CT, 0);
     using B0 = BlockSorter<K, TU::C0T, TU::C0I>;
     using B1 = BlockSorter<K, TU::C1T, TU::C1I>;
     using B2 = BlockSorter<K, TU::C2T, TU::C2I>;
@@ -355,8 +375,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                 sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur],
                                                                   sorted[cur], lut[cur], seed, 16u));
         QLAUNCH(led, kPhCount, level_keys * sizeof(K),
-                count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
-                    lv[cur].segs, lv[cur].chunks, src, tree[cur], sorted[cur], lut[cur], hist));
+                count_fn<<<std::min(nchunks, count_grid), TU::CT, 0, st>>>(
+                    lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_count, src, tree[cur],
+                    sorted[cur], lut[cur], hist));
         const unsigned gy = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(128, nchunks / nsegs / 4));
         QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(nsegs, gy), 512, 0, st>>>(lv[cur].segs, hist));
         QCK(cudaMemsetAsync(lv[nxt].cnt, 0, sizeof(LevelCounters), st));
@@ -364,8 +385,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                 plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(
                     lv[cur].segs, hist, sorted[cur], lv[nxt], p, tasks, fills, lv[cur].cnt));
         QLAUNCH(led, kPhScatter, 2 * level_keys * sizeof(K),
-                scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(lv[cur].segs, lv[cur].chunks, src,
-                                                                dst, tree[cur], sorted[cur], lut[cur], hist));
+                scatter_fn<<<std::min(nchunks, scatter_grid), TU::XT, sizeof(SM), st>>>(
+                    lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_scatter, src, dst,
+                    tree[cur], sorted[cur], lut[cur], hist));
         LevelCounters hc[2];
         QCK(cudaMemcpyAsync(&hc[0], lv[cur].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
         QCK(cudaMemcpyAsync(&hc[1], lv[nxt].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
@@ -665,16 +687,21 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
                                                          n, nchunks, chunks, L.chunk_elems, key_max));
     QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
     if (n == 0) return QMSORT_OK;
+    LevelCounters* cnt = reinterpret_cast<LevelCounters*>(ws + L.cnt_off[0]);
+    QCK(cudaMemsetAsync(cnt, 0, sizeof(LevelCounters), st));
+    auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
     QLAUNCH(led, kPhCount, n * sizeof(K),
-            count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX><<<nchunks, TU::CT, 0, st>>>(
-                seg, chunks, in, tree, sorted, lut, hist));
+            count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
+                       st>>>(seg, chunks, nchunks, &cnt->work_count, in, tree, sorted, lut, hist));
     QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(1, 64), 512, 0, st>>>(seg, hist));
     QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
     QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
-            scatter_fn<<<nchunks, TU::XT, sizeof(SM), st>>>(seg, chunks, in, out, tree, sorted, lut, hist));
+            scatter_fn<<<std::min(nchunks, resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM))),
+                         TU::XT, sizeof(SM), st>>>(seg, chunks, nchunks, &cnt->work_scatter, in, out,
+                                                   tree, sorted, lut, hist));
     return QMSORT_OK;
 }
 

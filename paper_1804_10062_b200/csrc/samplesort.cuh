@@ -89,6 +89,7 @@ struct LevelCounters {
     uint32_t nfill;
     uint32_t ntasks[kNumClasses];
     uint32_t overflow;  // capacity exceeded somewhere (host reports an error)
+    uint32_t work_count, work_scatter;  // dynamic chunk dispensers of this level's kernels
     uint32_t pad;
     unsigned long long nkeys;      // keys in this level's segments (pass ledger)
     unsigned long long task_keys;  // keys handed to the block sorter
@@ -374,20 +375,10 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
 // K2: per-chunk bucket histogram.
 // ---------------------------------------------------------------------------
 template <class K, int T, int U, int LOG_KMAX>
-__global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ segs,
-                                                  const ChunkDesc* __restrict__ chunks,
-                                                  const K* __restrict__ src,
-                                                  const K* __restrict__ tree_store,
-                                                  const K* __restrict__ sorted_store,
-                                                  const uint32_t* __restrict__ lut_store,
-                                                  uint32_t* __restrict__ hist) {
-    constexpr int KMAX = 1 << LOG_KMAX;
-    __shared__ ClassifierSmem<K, LOG_KMAX> cls;
-    __shared__ uint32_t shist[2 * KMAX];
-    const ChunkDesc c = chunks[blockIdx.x];
-    const SegDesc d = segs[c.seg];
+__device__ __forceinline__ void count_chunk(const ClassifierSmem<K, LOG_KMAX>& cls, uint32_t* shist,
+                                            const SegDesc& d, const ChunkDesc& c, uint32_t ck,
+                                            const K* __restrict__ src, uint32_t* __restrict__ hist) {
     const uint32_t nb = (1u << d.logk) << d.eq;
-    load_classifier<K, LOG_KMAX, T>(cls, d, tree_store, sorted_store, lut_store);
     for (uint32_t i = threadIdx.x; i < nb; i += T) shist[i] = 0;
     __syncthreads();
     const K* p = src + c.begin + threadIdx.x;
@@ -418,9 +409,41 @@ __global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ se
             if (u * T + threadIdx.x < rem) atomicAdd(&shist[bin[u]], 1u);
     }
     __syncthreads();
-    const uint32_t ci = blockIdx.x - d.chunk_begin;
+    const uint32_t ci = ck - d.chunk_begin;
     const uint32_t stride = d.nchunks + 1;
     for (uint32_t b = threadIdx.x; b < nb; b += T) hist[d.hist_base + b * stride + ci] = shist[b];
+    __syncthreads();
+}
+
+// Persistent CTAs fetch chunks dynamically from *work (no tail of idle SMs);
+// the classifier is reloaded only when the segment changes.
+template <class K, int T, int U, int LOG_KMAX>
+__global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ segs,
+                                                  const ChunkDesc* __restrict__ chunks,
+                                                  uint32_t nchunks, uint32_t* __restrict__ work,
+                                                  const K* __restrict__ src,
+                                                  const K* __restrict__ tree_store,
+                                                  const K* __restrict__ sorted_store,
+                                                  const uint32_t* __restrict__ lut_store,
+                                                  uint32_t* __restrict__ hist) {
+    constexpr int KMAX = 1 << LOG_KMAX;
+    __shared__ ClassifierSmem<K, LOG_KMAX> cls;
+    __shared__ uint32_t shist[2 * KMAX];
+    __shared__ uint32_t next_chunk;
+    uint32_t cur_seg = 0xFFFFFFFFu;
+    for (;;) {
+        if (threadIdx.x == 0) next_chunk = atomicAdd(work, 1u);
+        __syncthreads();
+        const uint32_t ck = next_chunk;
+        if (ck >= nchunks) break;
+        const ChunkDesc c = chunks[ck];
+        const SegDesc d = segs[c.seg];
+        if (c.seg != cur_seg) {
+            load_classifier<K, LOG_KMAX, T>(cls, d, tree_store, sorted_store, lut_store);
+            cur_seg = c.seg;
+        }
+        count_chunk<K, T, U, LOG_KMAX>(cls, shist, d, c, ck, src, hist);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -436,17 +459,25 @@ __global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__
     for (uint32_t b = blockIdx.y * 16 + (threadIdx.x >> 5); b < nb; b += gridDim.y * 16) {
         uint32_t* col = hist + d.hist_base + b * stride;
         uint32_t carry = 0;
-        for (uint32_t c0 = 0; c0 < d.nchunks; c0 += 32) {
-            const uint32_t c = c0 + lane;
-            const uint32_t v = c < d.nchunks ? col[c] : 0;
-            uint32_t x = v;
+        for (uint32_t c0 = 0; c0 < d.nchunks; c0 += 128) {
+            uint32_t v[4];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+            for (int q = 0; q < 4; ++q) {  // four loads in flight per lane
+                const uint32_t c = c0 + q * 32 + lane;
+                v[q] = c < d.nchunks ? col[c] : 0;
             }
-            if (c < d.nchunks) col[c] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t c = c0 + q * 32 + lane;
+                uint32_t x = v[q];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (c < d.nchunks) col[c] = carry + x - v[q];
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
         }
         if (lane == 0) col[d.nchunks] = carry;
     }
@@ -466,11 +497,16 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     constexpr int NB = 2 << LOG_KMAX;
     __shared__ uint32_t tot[NB];
     __shared__ uint32_t start[NB];
+    __shared__ uint32_t slot[NB];  // block-sort task: class << 28 | index within the class
     __shared__ uint32_t warp_sums[32];
+    __shared__ uint32_t cls_count[kNumClasses], cls_base[kNumClasses];
+    __shared__ unsigned long long cls_keys;
     const uint32_t seg = blockIdx.x;
     const SegDesc d = segs[seg];
     const uint32_t nb = (1u << d.logk) << d.eq;
     const uint32_t stride = d.nchunks + 1;
+    if (threadIdx.x < kNumClasses) cls_count[threadIdx.x] = 0;
+    if (threadIdx.x == 0) cls_keys = 0;
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
         const uint32_t v = hist[d.hist_base + b * stride + d.nchunks];
         tot[b] = v;
@@ -478,6 +514,26 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     }
     __syncthreads();
     block_exclusive_scan_smem<T>(start, (int)nb, warp_sums);
+    // block-sort tasks: reserve per class in shared memory first, then one
+    // global atomic per class and CTA (the global counters are contended)
+    for (uint32_t b = threadIdx.x; b < nb; b += T) {
+        const uint32_t len = tot[b];
+        uint32_t sl = 0xFFFFFFFFu;
+        if (len != 0 && !(d.eq && (b & 1)) && len <= p.cap && !(len == 1 && p.dst_is_a)) {
+            uint32_t cls = 0;
+            while (cls < kNumClasses - 1 && len > p.class_cap[cls]) ++cls;
+            sl = (cls << 28) | atomicAdd(&cls_count[cls], 1u);
+            atomicAdd(&cls_keys, (unsigned long long)len);
+        }
+        slot[b] = sl;
+    }
+    __syncthreads();
+    if (threadIdx.x < kNumClasses)
+        cls_base[threadIdx.x] = cls_count[threadIdx.x]
+                                    ? atomicAdd(&cur_cnt->ntasks[threadIdx.x], cls_count[threadIdx.x])
+                                    : 0u;
+    if (threadIdx.x == 0 && cls_keys) atomicAdd(&cur_cnt->task_keys, cls_keys);
+    __syncthreads();
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
         hist[d.hist_base + b * stride + d.nchunks] = start[b];
         const uint32_t len = tot[b];
@@ -499,17 +555,16 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 }
             }
         } else if (len <= p.cap) {
-            if (len == 1 && p.dst_is_a) continue;
-            int cls = 0;
-            while (cls < kNumClasses - 1 && len > p.class_cap[cls]) ++cls;
-            const uint32_t t = atomicAdd(&cur_cnt->ntasks[cls], 1u);
+            const uint32_t sl = slot[b];
+            if (sl == 0xFFFFFFFFu) continue;  // single key already in place
+            const uint32_t cls = sl >> 28;
+            const uint32_t t = cls_base[cls] + (sl & 0x0FFFFFFFu);
             if (t < p.task_cap) {
                 SortTask st;
                 st.off = off;
                 st.len = len;
                 st.pad = 0;
                 tasks[(size_t)cls * p.task_cap + t] = st;
-                atomicAdd(&cur_cnt->task_keys, (unsigned long long)len);
             } else {
                 atomicExch(&cur_cnt->overflow, 1u);
             }
@@ -537,12 +592,16 @@ struct ScatterSmem {
     static constexpr int BPT = NB / T;  // bins owned by each thread in the scan
     static_assert(NB % T == 0 && (BPT == 1 || BPT == 2 || BPT == 4), "bins per thread");
     static constexpr int TILE = T * U;
+    // a staged key travels with its segment-relative destination, so the
+    // write-out reads one record per key and needs no per-bucket lookup
+    struct alignas(sizeof(K) >= 8 ? 16 : 8) Rec {
+        K key;
+        uint32_t dest;
+    };
     ClassifierSmem<K, LOG_KMAX> cls;
-    K stage[TILE];
-    uint16_t stage_bin[TILE];
+    Rec stage[TILE];
     alignas(16) uint32_t hist[NB];
-    alignas(16) uint32_t start[NB];
-    alignas(16) uint32_t gdst[NB];  // destination of staged slot i is gdst[bin] + i (segment-relative)
+    alignas(16) uint2 sd[NB];  // {bucket start in the tile, destination base}
     uint32_t warp_sums[T / 32];
 };
 
@@ -618,43 +677,45 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         uint32_t excl = x - local;
 #pragma unroll
         for (int w = 0; w < T / 32; ++w) excl += (w < (int)wid) ? sm.warp_sums[w] : 0u;
-        uint32_t st[BPT], gd[BPT], z[BPT];
+        uint32_t z[BPT];
 #pragma unroll
         for (int i = 0; i < BPT; ++i) {
-            st[i] = excl;
-            gd[i] = cursor[i] - excl;
+            sm.sd[tid * BPT + i] = make_uint2(excl, cursor[i] - excl);
             cursor[i] += h[i];
             excl += h[i];
             z[i] = 0;
         }
-        vec_store<BPT>(&sm.start[tid * BPT], st);
-        vec_store<BPT>(&sm.gdst[tid * BPT], gd);
         vec_store<BPT>(&sm.hist[tid * BPT], z);
     }
     __syncthreads();
-    K* stage = sm.stage;
-    uint16_t* sbin = sm.stage_bin;
+    typename SM::Rec* stage = sm.stage;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (FULL || u * T + tid < m) {
-            const uint32_t b = bin[u] >> 16;
-            const uint32_t pos = sm.start[b] + (bin[u] & 0xFFFFu);
-            stage[pos] = k[u];
-            sbin[pos] = (uint16_t)b;
+            const uint2 sg = sm.sd[bin[u] >> 16];
+            const uint32_t pos = sg.x + (bin[u] & 0xFFFFu);
+            typename SM::Rec r;
+            r.key = k[u];
+            r.dest = sg.y + pos;
+            stage[pos] = r;
         }
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const uint32_t i = u * T + tid;
-        if (FULL || i < m) out[sm.gdst[sbin[i]] + i] = stage[i];
+        if (FULL || i < m) {
+            const typename SM::Rec r = stage[i];
+            out[r.dest] = r.key;
+        }
     }
     __syncthreads();
 }
 
 template <class K, int T, int U, int LOG_KMAX>
-__global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ segs,
+__global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict__ segs,
                                                     const ChunkDesc* __restrict__ chunks,
+                                                    uint32_t nchunks, uint32_t* __restrict__ work,
                                                     const K* __restrict__ src, K* __restrict__ dst,
                                                     const K* __restrict__ tree_store,
                                                     const K* __restrict__ sorted_store,
@@ -665,33 +726,44 @@ __global__ void __launch_bounds__(T) scatter_kernel(const SegDesc* __restrict__ 
     constexpr int BPT = SM::BPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
-
-    const ChunkDesc c = chunks[blockIdx.x];
-    const SegDesc d = segs[c.seg];
-    const uint32_t nb = (1u << d.logk) << d.eq;
-    load_classifier<K, LOG_KMAX, T>(sm.cls, d, tree_store, sorted_store, lut_store);
-    const uint32_t ci = blockIdx.x - d.chunk_begin;
-    const uint32_t stride = d.nchunks + 1;
-    uint32_t cursor[BPT];
-#pragma unroll
-    for (int i = 0; i < BPT; ++i) {
-        const uint32_t b = threadIdx.x * BPT + i;
-        cursor[i] = 0;
-        if (b < nb) {
-            const uint32_t* col = hist + d.hist_base + b * stride;
-            cursor[i] = col[d.nchunks] + col[ci];  // bucket start + chunk prefix
+    __shared__ uint32_t next_chunk;
+    uint32_t cur_seg = 0xFFFFFFFFu;
+    // persistent CTAs fetch chunks dynamically (no tail of idle SMs)
+    for (;;) {
+        if (threadIdx.x == 0) next_chunk = atomicAdd(work, 1u);
+        __syncthreads();
+        const uint32_t ck = next_chunk;
+        if (ck >= nchunks) break;
+        const ChunkDesc c = chunks[ck];
+        const SegDesc d = segs[c.seg];
+        const uint32_t nb = (1u << d.logk) << d.eq;
+        if (c.seg != cur_seg) {
+            load_classifier<K, LOG_KMAX, T>(sm.cls, d, tree_store, sorted_store, lut_store);
+            cur_seg = c.seg;
         }
-        sm.hist[b] = 0;
-    }
-    __syncthreads();
+        const uint32_t ci = ck - d.chunk_begin;
+        const uint32_t stride = d.nchunks + 1;
+        uint32_t cursor[BPT];
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) {
+            const uint32_t b = threadIdx.x * BPT + i;
+            cursor[i] = 0;
+            if (b < nb) {
+                const uint32_t* col = hist + d.hist_base + b * stride;
+                cursor[i] = col[d.nchunks] + col[ci];  // bucket start + chunk prefix
+            }
+            sm.hist[b] = 0;
+        }
+        __syncthreads();
 
-    const K* p = src + c.begin;
-    K* out = dst + d.off;
-    const uint32_t len = (uint32_t)(c.end - c.begin);
-    uint32_t t0 = 0;
-    for (; t0 + TILE <= len; t0 += TILE)
-        scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
-    if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+        const K* p = src + c.begin;
+        K* out = dst + d.off;
+        const uint32_t len = (uint32_t)(c.end - c.begin);
+        uint32_t t0 = 0;
+        for (; t0 + TILE <= len; t0 += TILE)
+            scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
+        if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+    }
 }
 
 // Equal-key buckets that landed in the workspace: write the splitter value.
