@@ -158,6 +158,10 @@ int qmsort_gpu_check(int dtype, int cmp, const void* d_data, size_t n, int check
 /* Library build identification (e.g. "qmsort-b200 sm_100a"). */
 const char* qmsort_gpu_version(void);
 
+/* Layout check for foreign binders: sizeof(qmsort_gpu_config) and
+ * sizeof(qmsort_gpu_metrics) as compiled into the library. */
+void qmsort_gpu_abi_sizes(size_t* config_bytes, size_t* metrics_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -82,6 +82,7 @@ EXPORTED = [
     "qmsort_gpu_generate",
     "qmsort_gpu_check",
     "qmsort_gpu_version",
+    "qmsort_gpu_abi_sizes",
 ]
 
 _lib = None

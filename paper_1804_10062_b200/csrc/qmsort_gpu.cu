@@ -918,3 +918,8 @@ int qmsort_gpu_check(int dtype, int cmp, const void* d, size_t n, int check_orde
 const char* qmsort_gpu_version(void) { return "qmsort-b200 0.1 sm_100a"; }
 
 }  // extern "C"
+
+extern "C" void qmsort_gpu_abi_sizes(size_t* config_bytes, size_t* metrics_bytes) {
+    if (config_bytes) *config_bytes = sizeof(qmsort_gpu_config);
+    if (metrics_bytes) *metrics_bytes = sizeof(qmsort_gpu_metrics);
+}

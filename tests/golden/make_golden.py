@@ -1,0 +1,96 @@
+"""Regenerate tests/golden/golden.json from the REFERENCE itself.
+
+Runs the unmodified reference QuickMergesort (compiled from /root/reference by
+oracle/Makefile into oracle/_ref/libqmsref.so) on the reference's own worked
+examples and on seeded inputs of every BASELINE.json config shape, and
+freezes the results (small arrays verbatim, large ones as SHA-256 digests).
+The GPU box has no /root/reference; the committed JSON travels instead.
+
+    python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+from oracle_lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64, Oracle  # noqa: E402
+
+N_CFG = 1 << 16
+SEEDS = [42, 1, 2]
+CONFIGS = {
+    "i32_perm": DT_I32, "u32": DT_U32, "u64": DT_U64, "f64_sorted": DT_F64, "f64_reverse": DT_F64,
+    "f64_distinct16": DT_F64, "f64_gauss": DT_F64, "f64_organ": DT_F64, "rec32": DT_REC32,
+}
+VARIANTS = {"qms": 0, "qmqs": 1, "momqms": 2, "hqms": 3}
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def main() -> None:
+    o = Oracle()
+    if o.ref is None:
+        raise SystemExit("oracle/_ref/libqmsref.so is not built (needs /root/reference)")
+    ref = o.ref
+    out: dict = {"generated_by": "tests/golden/make_golden.py (reference qmsort compiled from "
+                                 "/root/reference/proj/core/include)"}
+
+    # Fig. 1 worked example under every preset (reference test_sort.cpp:24,37-45)
+    fig = np.array([7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8], dtype=np.int64)
+    out["fig1"] = {"input": fig.tolist(), "outputs": {}}
+    for name, var in VARIANTS.items():
+        b = fig.copy()
+        ref.qmsref_sort(5, 0, var, 0, 0, b.ctypes.data_as(ctypes.c_void_p), b.shape[0], None)
+        out["fig1"]["outputs"][name] = b.tolist()
+
+    # swap_merge examples (reference test_merge.cpp:48-85)
+    cases = [([3, 5, 100, 101, 2, 4], (0, 2, 2, 6)), ([7, 1, 2, 3], (1, 1, 1, 4)),
+             ([9, 10, 8, 11, 2, 3, 4, 7, 0, 1, 5, 6], (8, 12, 0, 7))]
+    out["swap_merge"] = []
+    for arr, (b1, e1, t, te) in cases:
+        a = np.array(arr, dtype=np.int64)
+        ref.qmsref_swap_merge_i64(a.ctypes.data_as(ctypes.c_void_p), b1, e1, t, te)
+        out["swap_merge"].append({"input": arr, "args": [b1, e1, t, te], "output": a.tolist()})
+
+    # generator patterns and replay (reference test_dataset.cpp:18-38)
+    gens = []
+    for kind, param, n, seed in [(1, 0, 4, 0), (2, 0, 4, 0), (3, 0, 6, 0), (3, 0, 5, 0), (4, 3, 7, 0)]:
+        v = np.empty(n, np.int64)
+        ref.qmsref_generate(kind, param, n, seed, v.ctypes.data_as(ctypes.c_void_p))
+        gens.append({"kind": kind, "param": param, "n": n, "seed": seed, "output": v.tolist()})
+    out["generators"] = gens
+    perm = np.empty(1000, np.int64)
+    ref.qmsref_generate(0, 0, 1000, 41, perm.ctypes.data_as(ctypes.c_void_p))
+    dup = np.empty(N_CFG, np.int64)
+    ref.qmsref_generate(5, 16, N_CFG, 42, dup.ctypes.data_as(ctypes.c_void_p))
+    out["random_perm_1000_seed41_sha256"] = sha(perm)
+    out["randomdup16_65536_seed42_sha256"] = sha(dup)
+
+    # seeded config shapes: input digest (our recipe) and the
+    # reference qms() / std::sort output digests, ascending and descending
+    cfgs = {}
+    for name, dt in CONFIGS.items():
+        for seed in SEEDS:
+            a = o.gen(name, N_CFG, seed=seed)
+            rec = {"n": N_CFG, "seed": seed, "dtype": dt, "input_sha256": sha(a)}
+            rec["qms_sha256"] = sha(o.ref_sort(dt, a))
+            rec["std_sort_sha256"] = sha(o.ref_sort(dt, a, use_std=True))
+            rec["hqms_sha256"] = sha(o.ref_sort(dt, a, variant=3))
+            rec["qms_greater_sha256"] = sha(o.ref_sort(dt, a, greater=True))
+            cfgs[f"{name}/{seed}"] = rec
+    out["configs"] = cfgs
+    with open(os.path.join(HERE, "golden.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(f"wrote {len(cfgs)} config records")
+
+
+if __name__ == "__main__":
+    main()
