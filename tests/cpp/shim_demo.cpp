@@ -1,0 +1,81 @@
+// shim_demo.cpp -- TEST: the C++ drop-in include/qmsort_gpu.hpp used exactly
+// like the reference call qmsort::sort(v.begin(), v.end(), cfg, less)
+// (sort.hpp:215-226).  With WITH_REFERENCE the reference's own SortConfig
+// presets (qmsort::qms(), qmsort::hqms()) are passed straight through.
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <functional>
+#include <numeric>
+#include <vector>
+
+#include "qmsort_gpu.hpp"
+#ifdef WITH_REFERENCE
+#include "qmsort/qmsort.hpp"
+#endif
+
+static int fails = 0;
+#define CHECK(c)                                              \
+    do {                                                      \
+        if (!(c)) {                                           \
+            std::printf("CHECK failed: %s (line %d)\n", #c, __LINE__); \
+            ++fails;                                          \
+        }                                                     \
+    } while (0)
+
+struct Rec {
+    std::uint64_t w[4];
+};
+namespace qmsort::gpu {
+template <>
+struct is_rec32<Rec> : std::true_type {};
+}  // namespace qmsort::gpu
+
+int main() {
+    // Fig. 1 worked example (test_sort.cpp:24,37-45) under every preset
+    for (auto cfg : {qmsort::gpu::qms(), qmsort::gpu::qmqs(), qmsort::gpu::momqms(), qmsort::gpu::hqms()}) {
+        std::vector<std::int32_t> v{7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8};
+        qmsort::gpu::sort(v.begin(), v.end(), cfg);
+        std::vector<std::int32_t> e(12);
+        std::iota(e.begin(), e.end(), 0);
+        CHECK(v == e);
+    }
+    // seeded uint32 / double / rec32, ascending and descending
+    std::vector<std::uint32_t> u(1 << 20);
+    std::uint64_t s = 42;
+    for (auto& x : u) {
+        s = s * 6364136223846793005ull + 1442695040888963407ull;
+        x = (std::uint32_t)(s >> 32);
+    }
+    auto u2 = u;
+    qmsort::gpu::sort(u.begin(), u.end());
+    std::sort(u2.begin(), u2.end());
+    CHECK(u == u2);
+    qmsort::gpu::sort(u.begin(), u.end(), qmsort::gpu::qms(), std::greater<>{});
+    CHECK(std::is_sorted(u.begin(), u.end(), std::greater<>{}));
+    std::vector<double> d(100000);
+    for (std::size_t i = 0; i < d.size(); ++i) d[i] = (double)((i * 7919) % 1000) - 499.5;
+    auto d2 = d;
+    qmsort::gpu::sort(d.begin(), d.end(), qmsort::gpu::qms(), std::less<double>{});
+    std::sort(d2.begin(), d2.end());
+    CHECK(d == d2);
+    std::vector<Rec> r(50000);
+    for (std::size_t i = 0; i < r.size(); ++i) r[i] = Rec{{(i * 37) % 4096, (i * 2654435761u) % 1000003, i, 7}};
+    qmsort::gpu::sort(r.begin(), r.end());
+    CHECK(std::is_sorted(r.begin(), r.end(), [](const Rec& a, const Rec& b) {
+        return std::lexicographical_compare(a.w, a.w + 4, b.w, b.w + 4);
+    }));
+#ifdef WITH_REFERENCE
+    // the reference's own config objects and comparator types drop straight in
+    std::vector<std::int32_t> v{7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8};
+    qmsort::gpu::sort(v.begin(), v.end(), qmsort::hqms(), std::greater<>{});
+    CHECK(std::is_sorted(v.begin(), v.end(), std::greater<>{}));
+    std::vector<std::int32_t> w{7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8};
+    qmsort::SortConfig rc = qmsort::qms();
+    rc.pivot = qmsort::PivotStrategy::median_of_sqrt_n;
+    qmsort::gpu::sort(w.begin(), w.end(), rc);
+    CHECK(std::is_sorted(w.begin(), w.end()));
+#endif
+    std::printf(fails ? "shim FAILED (%d)\n" : "shim ok\n", fails);
+    return fails ? 1 : 0;
+}
