@@ -131,12 +131,16 @@ __device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
     {
         const int fm = 2 * lr - 1;
         const bool lower = (lane & lr) == 0;
+        if constexpr (ITEMS == 1) {
+            k[0] = select_minmax(k[0], KT::shfl_xor(k[0], fm), lower);
+        } else {
 #pragma unroll
-        for (int j = 0; j < ITEMS / 2; ++j) {
-            const K y0 = KT::shfl_xor(k[ITEMS - 1 - j], fm);
-            const K y1 = KT::shfl_xor(k[j], fm);
-            k[j] = select_minmax(k[j], y0, lower);
-            k[ITEMS - 1 - j] = select_minmax(k[ITEMS - 1 - j], y1, lower);
+            for (int j = 0; j < ITEMS / 2; ++j) {
+                const K y0 = KT::shfl_xor(k[ITEMS - 1 - j], fm);
+                const K y1 = KT::shfl_xor(k[j], fm);
+                k[j] = select_minmax(k[j], y0, lower);
+                k[ITEMS - 1 - j] = select_minmax(k[ITEMS - 1 - j], y1, lower);
+            }
         }
     }
 #pragma unroll 1
@@ -151,6 +155,15 @@ __device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
         for (int j = 0; j < ITEMS; ++j)
             if ((j & s) == 0) KT::cas(k[j], k[j + s]);
     }
+}
+
+// Sort the 32*ITEMS keys of a warp (lane-blocked: lane l ends up holding
+// positions l*ITEMS .. l*ITEMS+ITEMS-1 of the ascending order).
+template <class K, int ITEMS>
+__device__ __forceinline__ void warp_sort(K (&k)[ITEMS]) {
+    register_sort<K, ITEMS>(k);
+#pragma unroll 1
+    for (int lr = 1; lr < 32; lr <<= 1) warp_merge_round<K, ITEMS>(k, lr);
 }
 
 template <class K, int T, int ITEMS>

@@ -67,13 +67,15 @@ static int fail(int code, const std::string& msg) {
     } while (0)
 
 // Per-key-type tile shapes.  Class c of the block sorter sorts buckets of up to
-// C_cT * C_cI keys with C_cT threads.
+// CLS_T[c] * BI keys with CLS_T[c] threads; the largest class is the cap.
 template <class K>
 struct Tune;
 template <>
 struct Tune<uint32_t> {
     static constexpr int LOGKMAX = 9;
-    static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
+    static constexpr int BI = 16;                                 // block sort keys / thread
+    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};  // block sort classes
+    static constexpr int TARGET_DIV = 2;                          // target bucket = cap / 4
     static constexpr int ST = 512, SI = 16;  // sampler
     static constexpr int XT = 256, XI = 16;  // scatter tile
     static constexpr int CT = 256, CU = 16;  // count
@@ -82,7 +84,9 @@ struct Tune<uint32_t> {
 template <>
 struct Tune<uint64_t> {
     static constexpr int LOGKMAX = 9;
-    static constexpr int C0T = 64, C0I = 16, C1T = 256, C1I = 16, C2T = 512, C2I = 16;
+    static constexpr int BI = 16;
+    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};
+    static constexpr int TARGET_DIV = 4;
     static constexpr int ST = 512, SI = 16;
     static constexpr int XT = 256, XI = 16;
     static constexpr int CT = 256, CU = 8;
@@ -91,12 +95,18 @@ struct Tune<uint64_t> {
 template <>
 struct Tune<Rec32> {
     static constexpr int LOGKMAX = 8;
-    static constexpr int C0T = 64, C0I = 8, C1T = 256, C1I = 8, C2T = 512, C2I = 8;
+    static constexpr int BI = 8;
+    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};
+    static constexpr int TARGET_DIV = 2;
     static constexpr int ST = 512, SI = 8;
     static constexpr int XT = 256, XI = 8;
     static constexpr int CT = 256, CU = 4;
     static constexpr int MT = 512, MI = 8;
 };
+template <class K>
+constexpr uint32_t class_cap(int c) {
+    return (uint32_t)Tune<K>::CLS_T[c] * Tune<K>::BI;
+}
 
 // Kernel families for the per-phase ledger (qmsort_gpu_metrics.phase_*).
 enum Phase {
@@ -203,8 +213,8 @@ struct WsLayout {
 template <class K>
 static WsLayout make_layout(size_t n) {
     using TU = Tune<K>;
-    constexpr uint64_t cap = (uint64_t)TU::C2T * TU::C2I;
-    constexpr uint64_t target = cap / 2;
+    constexpr uint64_t cap = class_cap<K>(kNumClasses - 1);
+    constexpr uint64_t target = cap / TU::TARGET_DIV;
     constexpr uint64_t tile = (uint64_t)TU::XT * TU::XI;
     WsLayout L;
     // chunks of 16 tiles, dispensed dynamically to persistent CTAs
@@ -252,14 +262,28 @@ static int launch_tiles(const K* src, K* dst, uint64_t off, uint64_t len, cudaSt
     return QMSORT_OK;
 }
 
-// Sort [off, off+len) with len <= class-2 capacity: one CTA of the smallest class.
+// Sort [off, off+len) with len <= the cap: one CTA of the smallest class.
 template <class K>
 static int blocksort_one(const K* src, K* dst, uint64_t off, uint64_t len, cudaStream_t st,
                          Ledger& led) {
     using TU = Tune<K>;
-    if (len <= (uint64_t)TU::C0T * TU::C0I) return launch_tiles<K, TU::C0T, TU::C0I>(src, dst, off, len, st, led);
-    if (len <= (uint64_t)TU::C1T * TU::C1I) return launch_tiles<K, TU::C1T, TU::C1I>(src, dst, off, len, st, led);
-    return launch_tiles<K, TU::C2T, TU::C2I>(src, dst, off, len, st, led);
+    if (len <= class_cap<K>(0)) return launch_tiles<K, TU::CLS_T[0], TU::BI>(src, dst, off, len, st, led);
+    if (len <= class_cap<K>(1)) return launch_tiles<K, TU::CLS_T[1], TU::BI>(src, dst, off, len, st, led);
+    if (len <= class_cap<K>(2)) return launch_tiles<K, TU::CLS_T[2], TU::BI>(src, dst, off, len, st, led);
+    return launch_tiles<K, TU::CLS_T[3], TU::BI>(src, dst, off, len, st, led);
+}
+
+// Block-sort every task of size class C (src -> dst at the same offsets).
+template <class K, int C>
+static int launch_class(const SortTask* tasks, uint32_t count, const K* src, K* dst,
+                        uint64_t bytes, cudaStream_t st, Ledger& led) {
+    using TU = Tune<K>;
+    constexpr int T = TU::CLS_T[C];
+    using BS = BlockSorter<K, T, TU::BI>;
+    auto fn = blocksort_tasks_kernel<K, T, TU::BI>;
+    QCK(allow_smem((const void*)fn, BS::kSmemBytes));
+    QLAUNCH(led, kPhBlocksort, bytes, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, src, dst));
+    return QMSORT_OK;
 }
 
 // Block-sort tiles + merge-path passes over [off, off+len); the range currently
@@ -268,14 +292,14 @@ template <class K>
 static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStream_t st,
                            Ledger& led) {
     using TU = Tune<K>;
-    constexpr uint64_t C = (uint64_t)TU::C2T * TU::C2I;
+    constexpr uint64_t C = class_cap<K>(kNumClasses - 1);
     constexpr uint64_t MC = (uint64_t)TU::MT * TU::MI;
     static_assert(MC <= 2 * C, "merge tile must fit in one run pair");
     if (len <= C) return blocksort_one<K>(X, A, off, len, st, led);
     const uint64_t tiles = (len + C - 1) / C;
     const uint32_t passes = ceil_log2_u64(tiles);
     K* Y = (passes % 2 == 0) ? A : B;
-    QTRY((launch_tiles<K, TU::C2T, TU::C2I>(X, Y, off, len, st, led)));
+    QTRY((launch_tiles<K, TU::CLS_T[kNumClasses - 1], TU::BI>(X, Y, off, len, st, led)));
     using BS = BlockSorter<K, TU::MT, TU::MI>;
     auto fn = merge_pass_kernel<K, TU::MT, TU::MI>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
@@ -295,15 +319,13 @@ template <class K>
 static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
                       const WsLayout& L, cudaStream_t st, Ledger& led) {
     using TU = Tune<K>;
-    constexpr uint32_t cap = (uint32_t)TU::C2T * TU::C2I;
+    constexpr uint32_t cap = class_cap<K>(kNumClasses - 1);
     PlanParams p;
     p.chunk_elems = L.chunk_elems;
     p.cap = cap;
-    p.target = cap / 2;
+    p.target = cap / TU::TARGET_DIV;
     p.log_kmax = TU::LOGKMAX;
-    p.class_cap[0] = (uint32_t)TU::C0T * TU::C0I;
-    p.class_cap[1] = (uint32_t)TU::C1T * TU::C1I;
-    p.class_cap[2] = cap;
+    for (int c = 0; c < kNumClasses; ++c) p.class_cap[c] = class_cap<K>(c);
     p.task_cap = L.task_cap;
     p.fill_cap = L.fill_cap;
     p.dst_is_a = 0;
@@ -329,7 +351,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     FillTask* fills = reinterpret_cast<FillTask*>(ws + L.fills_off);
 
     QCK(cudaMemsetAsync(lv[0].cnt, 0, sizeof(LevelCounters), st));
-    QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<1, 32, 0, st>>>(lv[0], n, ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K))), p));
+    QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<16, 256, 0, st>>>(lv[0], n, ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K))), p));
 
     using BSS = BlockSorter<K, TU::ST, TU::SI>;
     auto sample_fn = sample_kernel<K, TU::ST, TU::SI>;
@@ -340,15 +362,6 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
     const unsigned scatter_grid = resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM));
     const unsigned count_grid = resident_grid((const void*)count_fn, TU::CT, 0);
-    using B0 = BlockSorter<K, TU::C0T, TU::C0I>;
-    using B1 = BlockSorter<K, TU::C1T, TU::C1I>;
-    using B2 = BlockSorter<K, TU::C2T, TU::C2I>;
-    auto bs0 = blocksort_tasks_kernel<K, TU::C0T, TU::C0I>;
-    auto bs1 = blocksort_tasks_kernel<K, TU::C1T, TU::C1I>;
-    auto bs2 = blocksort_tasks_kernel<K, TU::C2T, TU::C2I>;
-    QCK(allow_smem((const void*)bs0, B0::kSmemBytes));
-    QCK(allow_smem((const void*)bs1, B1::kSmemBytes));
-    QCK(allow_smem((const void*)bs2, B2::kSmemBytes));
 
     uint64_t level_keys = n;
     uint32_t nsegs = 1;
@@ -396,22 +409,20 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         if (hc[0].overflow || hc[1].overflow)
             return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
         ++led.levels;
-        const uint32_t nt[3] = {hc[0].ntasks[0], hc[0].ntasks[1], hc[0].ntasks[2]};
-        // the block-sort bytes of a level are credited to its first launch
+        // block-sort every bucket of this level; the bytes are credited to the
+        // level's first launch
         uint64_t bs_bytes = 2ull * hc[0].task_keys * sizeof(K);
-        if (nt[0]) {
-            QLAUNCH(led, kPhBlocksort, bs_bytes, bs0<<<nt[0], TU::C0T, B0::kSmemBytes, st>>>(tasks, dst, A));
-            bs_bytes = 0;
-        }
-        if (nt[1]) {
-            QLAUNCH(led, kPhBlocksort, bs_bytes,
-                    bs1<<<nt[1], TU::C1T, B1::kSmemBytes, st>>>(tasks + L.task_cap, dst, A));
-            bs_bytes = 0;
-        }
-        if (nt[2]) {
-            QLAUNCH(led, kPhBlocksort, bs_bytes,
-                    bs2<<<nt[2], TU::C2T, B2::kSmemBytes, st>>>(tasks + 2 * (size_t)L.task_cap, dst, A));
-        }
+        const uint32_t* nt = hc[0].ntasks;
+#define QCLASS(c)                                                                              \
+    if (nt[c]) {                                                                               \
+        QTRY((launch_class<K, c>(tasks + (size_t)(c) * L.task_cap, nt[c], dst, A, bs_bytes, st, led))); \
+        bs_bytes = 0;                                                                          \
+    }
+        QCLASS(0)
+        QCLASS(1)
+        QCLASS(2)
+        QCLASS(3)
+#undef QCLASS
         if (hc[0].nfill) {
             QLAUNCH(led, kPhFill, hc[0].fill_keys * sizeof(K),
                     fill_kernel<K><<<1184, 256, 0, st>>>(fills, hc[0].nfill, lv[cur].segs, sorted[cur], A));
@@ -429,7 +440,7 @@ template <class K>
 static int sort_core(K* A, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
                      const WsLayout& L, cudaStream_t st, Ledger& led) {
     using TU = Tune<K>;
-    constexpr uint64_t cap = (uint64_t)TU::C2T * TU::C2I;
+    constexpr uint64_t cap = class_cap<K>(kNumClasses - 1);
     if (n <= 1) return QMSORT_OK;
     K* B = reinterpret_cast<K*>(ws + L.b_off);
     if (n <= cap) return blocksort_one<K>(A, A, 0, n, st, led);

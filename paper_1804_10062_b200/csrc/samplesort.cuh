@@ -40,7 +40,7 @@
 
 namespace qmsort_b200 {
 
-constexpr int kNumClasses = 3;  // block-sort size classes
+constexpr int kNumClasses = 4;  // block-sort size classes
 constexpr int kLutMaxBits = 12;
 constexpr int kLutPerSplitter = 16;  // LUT words reserved per splitter slot
 
@@ -132,10 +132,10 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
     return k;
 }
 
-// Append a segment (and its chunk table) to the next level.  Called by one
-// thread.  Returns false on capacity overflow.
+// Append a segment (and, unless write_chunks is false, its chunk table) to
+// the next level.  Called by one thread.  Returns false on capacity overflow.
 __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len, uint64_t lo,
-                                    uint64_t hi, const PlanParams& p) {
+                                    uint64_t hi, const PlanParams& p, bool write_chunks = true) {
     const uint32_t logk = choose_logk(len, p.target, p.log_kmax);
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
     const uint32_t hwords = (nch + 1) * (2u << logk);
@@ -168,7 +168,7 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     d.pad[0] = d.pad[1] = d.pad[2] = 0;
     nb.segs[s] = d;
     atomicAdd(&nb.cnt->nkeys, (unsigned long long)len);
-    for (uint32_t i = 0; i < nch; ++i) {
+    for (uint32_t i = 0; write_chunks && i < nch; ++i) {
         ChunkDesc c;
         c.seg = s;
         c.pad = 0;
@@ -179,8 +179,20 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     return true;
 }
 
+// Level 0: one segment covering [0, n); its (many) chunks are written by all
+// threads of the grid.
 __global__ void init_level_kernel(LevelBufs nb, uint64_t n, uint64_t key_max, PlanParams p) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) emit_segment(nb, 0, n, 0, key_max, p);
+    if (threadIdx.x == 0 && blockIdx.x == 0) emit_segment(nb, 0, n, 0, key_max, p, false);
+    const uint32_t nch = (uint32_t)((n + p.chunk_elems - 1) / p.chunk_elems);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nch && i < nb.chunk_cap;
+         i += gridDim.x * blockDim.x) {
+        ChunkDesc c;
+        c.seg = 0;
+        c.pad = 0;
+        c.begin = (uint64_t)i * p.chunk_elems;
+        c.end = min(n, c.begin + p.chunk_elems);
+        nb.chunks[i] = c;
+    }
 }
 
 // ---------------------------------------------------------------------------
