@@ -386,7 +386,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
         QLAUNCH(led, kPhSample, 0,
                 sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur],
-                                                                  sorted[cur], lut[cur], seed, 16u));
+                                                                  sorted[cur], lut[cur], seed, 32u));
         QLAUNCH(led, kPhCount, level_keys * sizeof(K),
                 count_fn<<<std::min(nchunks, count_grid), TU::CT, 0, st>>>(
                     lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_count, src, tree[cur],
