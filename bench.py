@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: skip extras")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the distributed samplesort path even on one GPU (exercises NCCL)")
     return ap.parse_args()
 
 
@@ -198,7 +200,7 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
         from paper_1804_10062_b200 import sharded
         sharded.bench_main(args, METRIC, UNIT)
         return
