@@ -34,13 +34,15 @@ extern "C" {
 #define QMSORT_ENCCL 4     /* collective failure (sharded path)            */
 #define QMSORT_EINTERNAL 5 /* internal capacity overflow                   */
 
-/* ---- element types: the five BASELINE.json configs --------------------- */
+/* ---- element types: the five BASELINE.json configs plus int64 ---------- */
 typedef enum {
     QMSORT_DT_I32 = 0,   /* int32_t                                        */
     QMSORT_DT_U32 = 1,   /* uint32_t                                       */
     QMSORT_DT_U64 = 2,   /* uint64_t                                       */
     QMSORT_DT_F64 = 3,   /* double, NaN-free, no -0.0                       */
-    QMSORT_DT_REC32 = 4  /* 4 x uint64_t, lexicographic over w0..w3         */
+    QMSORT_DT_REC32 = 4, /* 4 x uint64_t, lexicographic over w0..w3         */
+    QMSORT_DT_I64 = 5    /* int64_t: the reference profile's key type
+                            (element.hpp:16, Vec in test_sort.cpp:22)        */
 } qmsort_dtype;
 
 /* ---- comparator: the reference's Less template argument ---------------- */
@@ -112,6 +114,34 @@ int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu
  * contiguous host range.  Device buffers are cached per thread. */
 int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
                          qmsort_gpu_metrics* metrics);
+
+/* ---- key + payload elements --------------------- */
+/* Replaces qmsort::sort over Element<PayloadBytes> (element.hpp:13-20:
+ * ordering on the key alone, payload moved with it; test_sort.cpp:328-339).
+ * Sorts n elements of elem_bytes bytes (a multiple of 4, <= 4096) by the key of
+ * key_dtype (I32/U32/U64/F64/I64) stored at byte offset key_offset, naturally
+ * aligned.  Equal keys keep their input order (stable), which is one of the
+ * arrangements the reference's unstable sort may produce; the key sequence is
+ * the reference's exactly. */
+size_t qmsort_gpu_elements_workspace_bytes(size_t n, size_t elem_bytes);
+int qmsort_gpu_sort_elements(int key_dtype, int cmp, void* d_data, size_t n, size_t elem_bytes,
+                             size_t key_offset, const qmsort_gpu_config* cfg, void* d_ws,
+                             size_t ws_bytes, qmsort_gpu_metrics* metrics, void* stream);
+int qmsort_gpu_sort_elements_host(int key_dtype, int cmp, void* h_data, size_t n,
+                                  size_t elem_bytes, size_t key_offset,
+                                  const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics);
+
+/* ---- selection ---------------------------------- */
+/* Replaces select_nth(first, last, k, cmp, m) (selection.hpp:207-212): k is
+ * 1-based; on return *pos = k-1 holds the k-th smallest element under cmp,
+ * every element left of it is <= it and every element right of it >= it
+ * (selection.hpp:124-126).  EINVAL unless 1 <= k <= n. */
+size_t qmsort_gpu_select_workspace_bytes(int dtype, size_t n);
+int qmsort_gpu_select_nth(int dtype, int cmp, void* d_data, size_t n, size_t k, size_t* pos,
+                          const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes,
+                          qmsort_gpu_metrics* metrics, void* stream);
+int qmsort_gpu_select_nth_host(int dtype, int cmp, void* h_data, size_t n, size_t k, size_t* pos,
+                               const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics);
 
 /* Description of the last failure on the calling thread ("" if none). */
 const char* qmsort_gpu_last_error(void);

@@ -5,7 +5,9 @@
 //     Metrics qmsort::sort(It first, It last, const SortConfig& cfg = {}, Less less = {},
 //                          SortObserver* obs = nullptr);          // sort.hpp:215-226
 // as qmsort::gpu::sort with the same argument meaning: a contiguous range of
-// int32 / uint32 / uint64 / double / 32-byte records, a SortConfig (ours, or the
+// int32 / int64 / uint32 / uint64 / double / 32-byte records, or of key +
+// payload elements (any standard-layout type with a scalar `key` member, such
+// as the reference's Element<PayloadBytes>, element.hpp:13-20), a SortConfig (ours, or the
 // reference's own qmsort::SortConfig -- any type with the same member names),
 // and std::less / std::greater.  The range is copied to the B200, sorted there
 // and copied back; failures throw std::runtime_error (as trial.hpp:116 does),
@@ -13,7 +15,9 @@
 // (the GPU pipeline has no QuickXsort steps to observe).
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
+#include <algorithm>
 #include <functional>
 #include <iterator>
 #include <stdexcept>
@@ -81,16 +85,31 @@ struct Metrics {  // metrics.hpp:14-24 (comparisons/moves are not counted on the
 template <class T>
 struct is_rec32 : std::false_type {};
 template <class T>
-constexpr int dtype_code() {
-    if constexpr (std::is_same_v<T, std::int32_t>) return QMSORT_DT_I32;
-    else if constexpr (std::is_same_v<T, std::uint32_t>) return QMSORT_DT_U32;
-    else if constexpr (std::is_same_v<T, std::uint64_t>) return QMSORT_DT_U64;
+constexpr int scalar_code() {
+    if constexpr (std::is_integral_v<T> && std::is_signed_v<T> && sizeof(T) == 4) return QMSORT_DT_I32;
+    else if constexpr (std::is_integral_v<T> && std::is_unsigned_v<T> && sizeof(T) == 4) return QMSORT_DT_U32;
+    else if constexpr (std::is_integral_v<T> && std::is_signed_v<T> && sizeof(T) == 8) return QMSORT_DT_I64;
+    else if constexpr (std::is_integral_v<T> && std::is_unsigned_v<T> && sizeof(T) == 8) return QMSORT_DT_U64;
     else if constexpr (std::is_same_v<T, double>) return QMSORT_DT_F64;
+    else return -1;
+}
+// Key + payload element: a standard-layout class with a scalar `key` member.
+template <class T, class = void>
+struct is_keyed_element : std::false_type {};
+template <class T>
+struct is_keyed_element<T, std::void_t<decltype(std::declval<const T&>().key)>>
+    : std::bool_constant<std::is_class_v<T> && std::is_standard_layout_v<T> &&
+                         std::is_trivially_copyable_v<T> &&
+                         scalar_code<std::remove_cv_t<decltype(std::declval<T&>().key)>>() >= 0> {};
+
+template <class T>
+constexpr int dtype_code() {
+    if constexpr (scalar_code<T>() >= 0) return scalar_code<T>();
     else if constexpr (is_rec32<T>::value) {
         static_assert(sizeof(T) == 32 && std::is_trivially_copyable_v<T>, "rec32 must be 32 trivially copyable bytes");
         return QMSORT_DT_REC32;
     } else {
-        static_assert(sizeof(T) == 0, "qmsort::gpu::sort supports int32, uint32, uint64, double and rec32");
+        static_assert(sizeof(T) == 0, "qmsort::gpu::sort supports int32, int64, uint32, uint64, double, rec32 and keyed elements");
         return -1;
     }
 }
@@ -143,11 +162,39 @@ Metrics sort(It first, It last, const Cfg& cfg = Cfg{}, Less = Less{}, Observer*
     if (n == 0) return m;
     qmsort_gpu_config c = to_c(cfg);
     qmsort_gpu_metrics gm{};
-    throw_on(qmsort_gpu_sort_host(dtype_code<T>(), cmp_code<Less, T>(), &*first, n, &c, &gm),
-             "qmsort_gpu_sort_host");
+    if constexpr (is_keyed_element<T>::value && !is_rec32<T>::value) {
+        // Element<PayloadBytes>: ordered on the key alone (element.hpp:17-18)
+        using Key = std::remove_cv_t<decltype(std::declval<T&>().key)>;
+        throw_on(qmsort_gpu_sort_elements_host(scalar_code<Key>(), cmp_code<Less, T>(), &*first, n,
+                                               sizeof(T), offsetof(T, key), &c, &gm),
+                 "qmsort_gpu_sort_elements_host");
+    } else {
+        throw_on(qmsort_gpu_sort_host(dtype_code<T>(), cmp_code<Less, T>(), &*first, n, &c, &gm),
+                 "qmsort_gpu_sort_host");
+    }
     m.max_depth = gm.max_depth;
     m.elapsed_ns = gm.elapsed_ns;
     return m;
+}
+
+// select_nth(first, last, k, cmp, m) (selection.hpp:207-212): k is 1-based;
+// returns the offset of the k-th smallest under Less, with the range
+// partitioned around it.  Less is std::less / std::greater.
+template <class It, class Less = std::less<>>
+std::size_t select_nth(It first, It last, std::size_t k, Less = Less{}, Metrics* m = nullptr,
+                       const SortConfig& cfg = SortConfig{}) {
+    using T = typename std::iterator_traits<It>::value_type;
+    const std::size_t n = static_cast<std::size_t>(last - first);
+    qmsort_gpu_config c = to_c(cfg);
+    qmsort_gpu_metrics gm{};
+    std::size_t pos = 0;
+    throw_on(qmsort_gpu_select_nth_host(dtype_code<T>(), cmp_code<Less, T>(), &*first, n, k, &pos, &c, &gm),
+             "qmsort_gpu_select_nth_host");
+    if (m) {
+        m->max_depth = std::max<std::uint64_t>(m->max_depth, gm.max_depth);
+        m->elapsed_ns += gm.elapsed_ns;
+    }
+    return pos;
 }
 
 // Device-range variant: d_first..d_last in GPU memory, optional stream.

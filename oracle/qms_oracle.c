@@ -26,13 +26,14 @@
 
 typedef struct { uint64_t w[4]; } qmso_rec32;
 
-enum { QMSO_I32 = 0, QMSO_U32 = 1, QMSO_U64 = 2, QMSO_F64 = 3, QMSO_REC32 = 4 };
+enum { QMSO_I32 = 0, QMSO_U32 = 1, QMSO_U64 = 2, QMSO_F64 = 3, QMSO_REC32 = 4, QMSO_I64 = 5 };
 enum { QMSO_PIVOT_MEDIAN_OF_3 = 0, QMSO_PIVOT_MEDIAN_OF_SQRT_N = 1 };
 
 /* ------------------------------------------------------------------------ */
 /* Comparators: "less" per element type; greater = swapped arguments.       */
 /* ------------------------------------------------------------------------ */
 static inline int lt_i32(const int32_t *a, const int32_t *b) { return *a < *b; }
+static inline int lt_i64(const int64_t *a, const int64_t *b) { return *a < *b; }
 static inline int lt_u32(const uint32_t *a, const uint32_t *b) { return *a < *b; }
 static inline int lt_u64(const uint64_t *a, const uint64_t *b) { return *a < *b; }
 static inline int lt_f64(const double *a, const double *b) { return *a < *b; }
@@ -228,6 +229,7 @@ static inline int lt_rec(const qmso_rec32 *a, const qmso_rec32 *b) {
     }
 
 QMSO_DEFINE(i32, int32_t, lt_i32)
+QMSO_DEFINE(i64, int64_t, lt_i64)
 QMSO_DEFINE(u32, uint32_t, lt_u32)
 QMSO_DEFINE(u64, uint64_t, lt_u64)
 QMSO_DEFINE(f64, double, lt_f64)
@@ -242,6 +244,7 @@ QMSO_DEFINE(rec, qmso_rec32, lt_rec)
 int qmso_sort(int dtype, int greater, int pivot, void *data, size_t n) {
     switch (dtype) {
         case QMSO_I32: qms_i32((int32_t *)data, n, greater, pivot); return 0;
+        case QMSO_I64: qms_i64((int64_t *)data, n, greater, pivot); return 0;
         case QMSO_U32: qms_u32((uint32_t *)data, n, greater, pivot); return 0;
         case QMSO_U64: qms_u64((uint64_t *)data, n, greater, pivot); return 0;
         case QMSO_F64: qms_f64((double *)data, n, greater, pivot); return 0;
@@ -253,10 +256,7 @@ int qmso_sort(int dtype, int greater, int pivot, void *data, size_t n) {
 /* swap_merge on int64 test vectors (test_merge.cpp:48-85 golden examples).
  * data holds the whole array; run1 = [b1,e1), out = [t,te) as indices. */
 void qmso_swap_merge_i64(int64_t *data, size_t b1, size_t e1, size_t t, size_t te) {
-    /* int64 instantiation via the u64 path is wrong for negatives; tests use
-     * non-negative values, matching the reference fixtures. */
-    swap_merge_u64((uint64_t *)data + b1, (uint64_t *)data + e1, (uint64_t *)data + t,
-                   (uint64_t *)data + te, 0);
+    swap_merge_i64(data + b1, data + e1, data + t, data + te, 0);
 }
 
 /* Is data[0..n) sorted (non-decreasing under less, or under greater)? */
@@ -265,6 +265,7 @@ int qmso_is_sorted(int dtype, int greater, const void *data, size_t n) {
         int bad = 0;
         switch (dtype) {
             case QMSO_I32: bad = cmp_i32((const int32_t *)data + i, (const int32_t *)data + i - 1, greater); break;
+            case QMSO_I64: bad = cmp_i64((const int64_t *)data + i, (const int64_t *)data + i - 1, greater); break;
             case QMSO_U32: bad = cmp_u32((const uint32_t *)data + i, (const uint32_t *)data + i - 1, greater); break;
             case QMSO_U64: bad = cmp_u64((const uint64_t *)data + i, (const uint64_t *)data + i - 1, greater); break;
             case QMSO_F64: bad = cmp_f64((const double *)data + i, (const double *)data + i - 1, greater); break;

@@ -109,6 +109,30 @@ std::uint64_t qmsref_splitmix(std::uint64_t seed, std::uint64_t j) {
     return x;
 }
 
+// qmsort::sort over Element<16> (element.hpp:13-20, test_sort.cpp:328-339):
+// data is n raw 24-byte elements {int64 key, 16 payload bytes}.
+int qmsref_sort_elem16(void* data, std::size_t n, int greater) {
+    using E = qmsort::Element<16>;
+    static_assert(sizeof(E) == 24, "Element<16> layout");
+    E* p = static_cast<E*>(data);
+    if (greater)
+        qmsort::sort(p, p + n, qmsort::qms(), [](const E& a, const E& b) { return b < a; });
+    else
+        qmsort::sort(p, p + n, qmsort::qms());
+    return 0;
+}
+
+// select_nth (selection.hpp:207-212) on an int64 array; returns the position.
+std::size_t qmsref_select_nth_i64(std::int64_t* a, std::size_t n, std::size_t k, int greater) {
+    qmsort::Metrics m;
+    if (greater) {
+        qmsort::CountingComparator<std::greater<>> cmp(m);
+        return qmsort::select_nth(a, a + n, k, cmp, m);
+    }
+    qmsort::CountingComparator<std::less<>> cmp(m);
+    return qmsort::select_nth(a, a + n, k, cmp, m);
+}
+
 // swap_merge (merge.hpp:64-97) on an int64 array, indices as in the tests.
 void qmsref_swap_merge_i64(std::int64_t* a, std::size_t b1, std::size_t e1, std::size_t t,
                            std::size_t te) {

@@ -15,6 +15,10 @@ reference (C++)                        here
 ``qmsort::sort(first, last, cfg,       :func:`sort` (device tensor in place, or host
   less)`` (sort.hpp:215-226)             array through the host drop-in call)
 ``sort_range_counted`` (:207-211)      :func:`sort_range_counted`
+``Element<PayloadBytes>``              :func:`sort_elements` (key-only ordering,
+  (element.hpp:13-20)                    payload moved; stable on the GPU)
+``select_nth(first, last, k, cmp, m)`` :func:`select_nth` (1-based k, returns the
+  (selection.hpp:207-212)                position; range partitioned around it)
 =====================================  ============================================
 
 All compute goes through the CUDA library (``libqmsort_gpu.so``) via the C-ABI
@@ -28,13 +32,13 @@ import enum
 from typing import Any
 
 from . import _lib
-from ._lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64, GREATER, LESS, QmsortError
+from ._lib import DT_F64, DT_I32, DT_I64, DT_REC32, DT_U32, DT_U64, GREATER, LESS, QmsortError
 
 __all__ = [
     "Variant", "PivotStrategy", "BaseCase", "MergesortSide", "BaseCasePolicy", "SortConfig",
     "Metrics", "qms", "qmqs", "momqms", "hqms", "sort", "sort_range_counted", "QmsortError",
-    "DT_I32", "DT_U32", "DT_U64", "DT_F64", "DT_REC32", "LESS", "GREATER",
-    "workspace_bytes", "generate", "check", "dtype_of",
+    "DT_I32", "DT_U32", "DT_U64", "DT_F64", "DT_REC32", "DT_I64", "LESS", "GREATER",
+    "workspace_bytes", "generate", "check", "dtype_of", "sort_elements", "select_nth",
 ]
 
 
@@ -179,8 +183,9 @@ def _cmp_code(less: Any) -> int:
 def dtype_of(data: Any) -> int:
     """Map a torch tensor / numpy array to a qmsort dtype code.
 
-    int32 -> I32, uint32 -> U32, uint64 -> U64, float64 -> F64, and an (n, 4)
-    array of 64-bit words -> REC32 (records compared lexicographically).
+    int32 -> I32, uint32 -> U32, uint64 -> U64, int64 -> I64, float64 -> F64,
+    and an (n, 4) array of 64-bit words -> REC32 (records compared
+    lexicographically).
     """
     name = str(data.dtype).replace("torch.", "")
     shape = tuple(data.shape)
@@ -188,7 +193,8 @@ def dtype_of(data: Any) -> int:
         return DT_REC32
     if len(shape) != 1:
         raise ValueError(f"expected a 1-D array or an (n, 4) record array, got shape {shape}")
-    table = {"int32": DT_I32, "uint32": DT_U32, "uint64": DT_U64, "float64": DT_F64}
+    table = {"int32": DT_I32, "uint32": DT_U32, "uint64": DT_U64, "int64": DT_I64,
+             "float64": DT_F64}
     if name not in table:
         raise ValueError(f"unsupported dtype {name}")
     return table[name]
@@ -258,6 +264,78 @@ def sort_range_counted(data: Any, cfg: SortConfig, metrics: Metrics, less: Any =
     metrics.merge_passes += r.merge_passes
     metrics.kernel_launches += r.kernel_launches
     metrics.host_syncs += r.host_syncs
+
+
+def _nbytes_rows(data: Any) -> tuple[int, int]:
+    """(n elements, bytes per element) of a record array: a numpy structured /
+    void array, or a 2-D uint8 array or tensor of shape (n, elem_bytes)."""
+    shape = tuple(data.shape)
+    if type(data).__module__.startswith("torch"):
+        if len(shape) != 2 or str(data.dtype) != "torch.uint8":
+            raise ValueError("element tensors must be uint8 of shape (n, elem_bytes)")
+        return shape[0], shape[1]
+    if len(shape) == 1:
+        return shape[0], int(data.dtype.itemsize)
+    if len(shape) == 2 and data.dtype.itemsize == 1:
+        return shape[0], shape[1]
+    raise ValueError(f"unsupported element array of shape {shape} and dtype {data.dtype}")
+
+
+def sort_elements(data: Any, key_dtype: int = DT_I64, cfg: SortConfig | None = None,
+                  less: Any = "less", *, key_offset: int = 0, stream: Any = None) -> Metrics:
+    """Sort key + payload elements in place by key alone (Element<PayloadBytes>,
+    element.hpp:13-20).  ``key_dtype`` is the type of the key at byte
+    ``key_offset`` of every element (int64 in the reference profile).  Equal
+    keys keep their input order; the key sequence equals the reference's."""
+    lib = _lib.load()
+    c = (cfg or SortConfig()).to_c()
+    m = _lib.GpuMetrics()
+    cmp = _cmp_code(less)
+    n, eb = _nbytes_rows(data)
+    if _is_torch_cuda(data):
+        if not data.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        rc = lib.qmsort_gpu_sort_elements(int(key_dtype), cmp, data.data_ptr(), n, eb, key_offset,
+                                          ctypes.byref(c), None, 0, ctypes.byref(m),
+                                          _stream_ptr(stream))
+        _lib.check(rc, "qmsort_gpu_sort_elements")
+    else:
+        rc = lib.qmsort_gpu_sort_elements_host(int(key_dtype), cmp, _host_ptr(data), n, eb,
+                                               key_offset, ctypes.byref(c), ctypes.byref(m))
+        _lib.check(rc, "qmsort_gpu_sort_elements_host")
+    return Metrics.from_c(m)
+
+
+def select_nth(data: Any, k: int, cmp: Any = "less", metrics: Metrics | None = None,
+               cfg: SortConfig | None = None, *, dtype: int | None = None,
+               stream: Any = None) -> int:
+    """selection.hpp:207-212: place the k-th smallest (1-based k) under ``cmp``
+    at its sorted position, with everything left of it <= and right of it >=,
+    and return that position (k - 1).  Accumulates into ``metrics`` if given."""
+    lib = _lib.load()
+    c = (cfg or SortConfig()).to_c()
+    m = _lib.GpuMetrics()
+    dt = dtype_of(data) if dtype is None else int(dtype)
+    n = int(data.shape[0])
+    pos = ctypes.c_size_t(0)
+    if _is_torch_cuda(data):
+        if not data.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        rc = lib.qmsort_gpu_select_nth(dt, _cmp_code(cmp), data.data_ptr(), n, int(k),
+                                       ctypes.byref(pos), ctypes.byref(c), None, 0,
+                                       ctypes.byref(m), _stream_ptr(stream))
+        _lib.check(rc, "qmsort_gpu_select_nth")
+    else:
+        rc = lib.qmsort_gpu_select_nth_host(dt, _cmp_code(cmp), _host_ptr(data), n, int(k),
+                                            ctypes.byref(pos), ctypes.byref(c), ctypes.byref(m))
+        _lib.check(rc, "qmsort_gpu_select_nth_host")
+    if metrics is not None:
+        r = Metrics.from_c(m)
+        metrics.elapsed_ns += r.elapsed_ns
+        metrics.max_depth = max(metrics.max_depth, r.max_depth)
+        metrics.levels += r.levels
+        metrics.kernel_launches += r.kernel_launches
+    return int(pos.value)
 
 
 def _host_ptr(data: Any) -> int:

@@ -19,7 +19,7 @@ QMSORT_ECUDA = 3
 QMSORT_ENCCL = 4
 QMSORT_EINTERNAL = 5
 
-DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32 = 0, 1, 2, 3, 4
+DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32, DT_I64 = 0, 1, 2, 3, 4, 5
 LESS, GREATER = 0, 1
 
 
@@ -83,6 +83,12 @@ EXPORTED = [
     "qmsort_gpu_check",
     "qmsort_gpu_version",
     "qmsort_gpu_abi_sizes",
+    "qmsort_gpu_elements_workspace_bytes",
+    "qmsort_gpu_sort_elements",
+    "qmsort_gpu_sort_elements_host",
+    "qmsort_gpu_select_workspace_bytes",
+    "qmsort_gpu_select_nth",
+    "qmsort_gpu_select_nth_host",
 ]
 
 _lib = None
@@ -117,6 +123,12 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_generate": (i, [i, vp, sz, u64, u64, u64, vp]),
         "qmsort_gpu_check": (i, [i, i, vp, sz, i, ctypes.POINTER(u64), vp]),
         "qmsort_gpu_version": (ctypes.c_char_p, []),
+        "qmsort_gpu_elements_workspace_bytes": (sz, [sz, sz]),
+        "qmsort_gpu_sort_elements": (i, [i, i, vp, sz, sz, sz, cfgp, vp, sz, mp, vp]),
+        "qmsort_gpu_sort_elements_host": (i, [i, i, vp, sz, sz, sz, cfgp, mp]),
+        "qmsort_gpu_select_workspace_bytes": (sz, [i, sz]),
+        "qmsort_gpu_select_nth": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, vp, sz, mp, vp]),
+        "qmsort_gpu_select_nth_host": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, mp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -20,6 +20,8 @@ enum TransformMode : int {
     kXfU64Greater = 4,   // ~x (also rec32 words)
     kXfF64Less = 5,      // sign-magnitude -> biased
     kXfF64Greater = 6,   // f64less then ~
+    kXfI64Less = 7,      // x ^ 0x8000000000000000
+    kXfI64Greater = 8,   // x ^ 0x7FFFFFFFFFFFFFFF
 };
 
 __device__ __forceinline__ uint64_t f64_fwd(uint64_t b) {
@@ -47,6 +49,8 @@ __global__ void transform64_kernel(uint64_t* p, uint64_t words, int mode, int in
         if (mode == kXfU64Greater) x = ~x;
         else if (mode == kXfF64Less) x = inverse ? f64_inv(x) : f64_fwd(x);
         else if (mode == kXfF64Greater) x = inverse ? f64_inv(~x) : ~f64_fwd(x);
+        else if (mode == kXfI64Less) x ^= 0x8000000000000000ull;
+        else if (mode == kXfI64Greater) x ^= 0x7FFFFFFFFFFFFFFFull;
         p[i] = x;
     }
 }

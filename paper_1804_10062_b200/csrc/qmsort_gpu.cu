@@ -28,6 +28,7 @@
 #include "aux_kernels.cuh"
 #include "blocksort.cuh"
 #include "common.cuh"
+#include "elements.cuh"
 #include "mergepass.cuh"
 #include "samplesort.cuh"
 
@@ -450,7 +451,7 @@ static int sort_core(K* A, size_t n, const qmsort_gpu_config& cfg, unsigned char
 
 static int core_dtype(int dt) {
     if (dt == QMSORT_DT_I32) return QMSORT_DT_U32;
-    if (dt == QMSORT_DT_F64) return QMSORT_DT_U64;
+    if (dt == QMSORT_DT_F64 || dt == QMSORT_DT_I64) return QMSORT_DT_U64;
     return dt;
 }
 
@@ -459,6 +460,7 @@ static size_t dtype_size(int dt) {
         case QMSORT_DT_I32:
         case QMSORT_DT_U32: return 4;
         case QMSORT_DT_U64:
+        case QMSORT_DT_I64:
         case QMSORT_DT_F64: return 8;
         case QMSORT_DT_REC32: return 32;
     }
@@ -485,6 +487,7 @@ static int run_transform(int dt, int cmp, void* d, size_t n, int inverse, cudaSt
         case QMSORT_DT_U32: mode = cmp ? kXfU32Greater : kXfNone; break;
         case QMSORT_DT_U64: mode = cmp ? kXfU64Greater : kXfNone; wide = true; break;
         case QMSORT_DT_F64: mode = cmp ? kXfF64Greater : kXfF64Less; wide = true; break;
+        case QMSORT_DT_I64: mode = cmp ? kXfI64Greater : kXfI64Less; wide = true; break;
         case QMSORT_DT_REC32: mode = cmp ? kXfU64Greater : kXfNone; wide = true; words = 4 * n; break;
     }
     if (mode == kXfNone || n == 0) return QMSORT_OK;
@@ -504,6 +507,23 @@ static int validate(int dt, int cmp, size_t n, const void* p) {
     if (n >= (1ull << 32)) return fail(QMSORT_EINVAL, "n must be < 2^32");
     if (n > 0 && p == nullptr) return fail(QMSORT_EINVAL, "null data pointer");
     return QMSORT_OK;
+}
+
+static void fill_metrics(qmsort_gpu_metrics* m, Ledger& led, float ms) {
+    if (!m) return;
+    std::memset(m, 0, sizeof(*m));
+    m->elapsed_ns = (uint64_t)((double)ms * 1e6);
+    m->max_depth = led.levels;
+    m->alg_bytes = led.alg_bytes;
+    m->levels = led.levels;
+    m->merge_passes = led.merge_passes;
+    m->kernel_launches = led.launches;
+    m->host_syncs = led.syncs + 1;
+    for (int i = 0; i < QMSORT_NUM_PHASES; ++i) {
+        m->phase_bytes[i] = led.ph_bytes[i];
+        m->phase_launches[i] = led.ph_launches[i];
+    }
+    led.collect(m->phase_ns);
 }
 
 static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_config* cfgp,
@@ -553,21 +573,7 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     if (own) cudaFreeAsync(ws, st);
     if (rc != QMSORT_OK) return rc;
     if (se != cudaSuccess) return fail(QMSORT_ECUDA, std::string("sort: ") + cudaGetErrorString(se));
-    if (m) {
-        std::memset(m, 0, sizeof(*m));
-        m->elapsed_ns = (uint64_t)((double)ms * 1e6);
-        m->max_depth = led.levels;
-        m->alg_bytes = led.alg_bytes;
-        m->levels = led.levels;
-        m->merge_passes = led.merge_passes;
-        m->kernel_launches = led.launches;
-        m->host_syncs = led.syncs + 1;
-        for (int i = 0; i < QMSORT_NUM_PHASES; ++i) {
-            m->phase_bytes[i] = led.ph_bytes[i];
-            m->phase_launches[i] = led.ph_launches[i];
-        }
-        led.collect(m->phase_ns);
-    }
+    fill_metrics(m, led, ms);
     g_err.clear();
     return QMSORT_OK;
 }
@@ -716,6 +722,287 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     return QMSORT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Call frame shared by the device entry points: optional library-owned
+// workspace, CUDA-event timing and the metrics record.
+// ---------------------------------------------------------------------------
+struct CallFrame {
+    cudaStream_t st;
+    Ledger led;
+    void* ws = nullptr;
+    bool own = false;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    explicit CallFrame(cudaStream_t s) : st(s) { led.st = s; }
+    int begin(const qmsort_gpu_config& cfg, void* wsp, size_t ws_bytes, size_t need) {
+        led.prof = cfg.profile != 0;
+        ws = wsp;
+        if (ws == nullptr && need > 0) {
+            QCK(cudaMallocAsync(&ws, need, st));
+            own = true;
+        } else if (need > 0 && ws_bytes < need) {
+            return fail(QMSORT_ENOWS, "workspace too small: need " + std::to_string(need) + " bytes");
+        }
+        QCK(cudaEventCreate(&e0));
+        QCK(cudaEventCreate(&e1));
+        QCK(cudaEventRecord(e0, st));
+        return QMSORT_OK;
+    }
+    // Synchronises the stream; rc is the status of the work in between.
+    int end(int rc, qmsort_gpu_metrics* m) {
+        float ms = 0.f;
+        cudaError_t se = cudaSuccess;
+        if (e1) {
+            cudaEventRecord(e1, st);
+            se = cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+        }
+        if (own) cudaFreeAsync(ws, st);
+        own = false;
+        if (rc != QMSORT_OK) return rc;
+        if (se != cudaSuccess) return fail(QMSORT_ECUDA, std::string("sync: ") + cudaGetErrorString(se));
+        fill_metrics(m, led, ms);
+        g_err.clear();
+        return QMSORT_OK;
+    }
+    ~CallFrame() {
+        if (e0) cudaEventDestroy(e0);
+        if (e1) cudaEventDestroy(e1);
+    }
+};
+
+static const qmsort_gpu_config& cfg_or_default(const qmsort_gpu_config* p, qmsort_gpu_config& tmp) {
+    if (p) return *p;
+    qmsort_gpu_config_init(&tmp, 0);
+    return tmp;
+}
+
+// ---------------------------------------------------------------------------
+// f3: key + payload elements (element.hpp:13-20).  Workspace: the 32-byte
+// records | the Rec32 samplesort workspace | the gathered elements.
+// ---------------------------------------------------------------------------
+struct ElemLayout {
+    size_t recs_off, sort_off, gather_off, total;
+};
+static ElemLayout elem_layout(size_t n, size_t elem_bytes) {
+    ElemLayout E;
+    E.recs_off = 0;
+    E.sort_off = align_up(n * sizeof(Rec32), 256);
+    E.gather_off = E.sort_off + align_up(make_layout<Rec32>(std::max<size_t>(n, 2)).total, 256);
+    E.total = E.gather_off + align_up(n * elem_bytes, 256);
+    return E;
+}
+
+static int validate_elems(int kdt, int cmp, const void* p, size_t n, size_t elem_bytes, size_t key_off) {
+    QTRY(validate(kdt, cmp, n, p));
+    if (kdt == QMSORT_DT_REC32) return fail(QMSORT_EINVAL, "element keys must be scalar");
+    const size_t kw = dtype_size(kdt);
+    if (elem_bytes == 0 || elem_bytes % 4 != 0 || elem_bytes > 4096)
+        return fail(QMSORT_EINVAL, "elem_bytes must be a multiple of 4 in [4, 4096]");
+    if (elem_bytes % kw != 0 || key_off % kw != 0 || key_off + kw > elem_bytes)
+        return fail(QMSORT_EINVAL, "key must be naturally aligned inside the element");
+    return QMSORT_OK;
+}
+
+static int sort_elements_device(int kdt, int cmp, void* d, size_t n, size_t elem_bytes,
+                                size_t key_off, const qmsort_gpu_config* cfgp, void* wsp,
+                                size_t ws_bytes, qmsort_gpu_metrics* m, cudaStream_t st) {
+    QTRY(validate_elems(kdt, cmp, d, n, elem_bytes, key_off));
+    qmsort_gpu_config tmp;
+    const qmsort_gpu_config& cfg = cfg_or_default(cfgp, tmp);
+    CallFrame f(st);
+    const ElemLayout E = elem_layout(n, elem_bytes);
+    QTRY(f.begin(cfg, wsp, ws_bytes, n > 1 ? E.total : 0));
+    int rc = QMSORT_OK;
+    if (n > 1) {
+        unsigned char* w = static_cast<unsigned char*>(f.ws);
+        Rec32* recs = reinterpret_cast<Rec32*>(w + E.recs_off);
+        unsigned char* out = w + E.gather_off;
+        const unsigned grid = (unsigned)std::min<size_t>((n + 255) / 256, 148 * 16);
+        QLAUNCH(f.led, kPhTransform, n * (elem_bytes + sizeof(Rec32)),
+                make_elem_recs_kernel<<<grid, 256, 0, st>>>(static_cast<const unsigned char*>(d), n,
+                                                            (uint32_t)elem_bytes, (uint32_t)key_off,
+                                                            kdt, cmp, recs));
+        rc = sort_core<Rec32>(recs, n, cfg, w + E.sort_off, make_layout<Rec32>(std::max<size_t>(n, 2)), st, f.led);
+        if (rc == QMSORT_OK) {
+            const unsigned g2 = (unsigned)std::min<size_t>((n * (elem_bytes / 4) + 255) / 256, 148 * 16);
+#define QGATHER(W)                                                                                  \
+    QLAUNCH(f.led, kPhTransform, n * (2 * elem_bytes + sizeof(Rec32)),                              \
+            gather_elems_kernel<W><<<g2, 256, 0, st>>>(static_cast<const W*>(d), reinterpret_cast<W*>(out), \
+                                                      recs, n, (uint32_t)(elem_bytes / sizeof(W))))
+            if (elem_bytes % 16 == 0) QGATHER(uint4);
+            else if (elem_bytes % 8 == 0) QGATHER(uint2);
+            else QGATHER(uint32_t);
+#undef QGATHER
+            QCK(cudaMemcpyAsync(d, out, n * elem_bytes, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    return f.end(rc, m);
+}
+
+// ---------------------------------------------------------------------------
+// f4: select_nth (selection.hpp:207-212).  The reference finds the k-th
+// smallest by median-of-medians three-way partitioning (select_kth,
+// selection.hpp:131-203) and leaves the range partitioned around it.  Here
+// every round draws a sample, brackets rank k between two sampled keys s1 <=
+// s2 and partitions the current window into  < s1 | == s1 | (s1, s2] | > s2
+// with one count + scatter pass (K2-K4, caller-given splitters); the window
+// shrinks to the bucket holding rank k (to a few percent of its size with
+// high probability, and always by at least the keys equal to s1).  A window
+// of equal keys ends the search; a small window is block-sorted.  Elements
+// left of position k-1 are <= it and those right of it >= it, as in the
+// reference.
+// ---------------------------------------------------------------------------
+template <class K>
+struct HostKey {
+    static bool is_min(const K& k) { return k == 0; }
+    static K pred(const K& k) { return k - 1; }
+    static bool eq(const K& a, const K& b) { return a == b; }
+};
+template <>
+struct HostKey<Rec32> {
+    static bool is_min(const Rec32& k) { return (k.w[0] | k.w[1] | k.w[2] | k.w[3]) == 0; }
+    static Rec32 pred(const Rec32& k) {
+        Rec32 r = k;
+        for (int i = 3; i >= 0; --i) {
+            if (r.w[i] != 0) {
+                --r.w[i];
+                break;
+            }
+            r.w[i] = ~0ull;
+        }
+        return r;
+    }
+    static bool eq(const Rec32& a, const Rec32& b) { return std::memcmp(&a, &b, sizeof(Rec32)) == 0; }
+};
+
+constexpr uint32_t kSelectSample = 4096;  // <= the smallest block-sort cap of every key type
+constexpr uint32_t kSelectBand = 48;      // sample ranks either side of k (~3 sigma at p = 1/2)
+constexpr size_t kSelectSortAt = 1u << 18;
+
+template <class K>
+static size_t select_extra_bytes() {
+    return align_up(kSelectSample * sizeof(K), 256) + 256 + 256;
+}
+
+template <class K>
+static int select_core(K* A, size_t n, size_t k0, const qmsort_gpu_config& cfg, unsigned char* ws,
+                       const WsLayout& L, cudaStream_t st, Ledger& led) {
+    static_assert(kSelectSample <= class_cap<K>(kNumClasses - 1), "sample must fit one block sort");
+    K* B = reinterpret_cast<K*>(ws + L.b_off);
+    K* smp = reinterpret_cast<K*>(ws + L.total);
+    K* dspl = reinterpret_cast<K*>(ws + L.total + align_up(kSelectSample * sizeof(K), 256));
+    uint64_t* dcnt = reinterpret_cast<uint64_t*>(ws + L.total + align_up(kSelectSample * sizeof(K), 256) + 256);
+    size_t lo = 0, hi = n;
+    for (uint32_t round = 0;; ++round) {
+        const size_t m = hi - lo;
+        if (m <= kSelectSortAt || round >= 64) return sort_core<K>(A + lo, m, cfg, ws, L, st, led);
+        const uint64_t seed = cfg.seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(round + 1));
+        QLAUNCH(led, kPhSample, 0,
+                gather_sample_kernel<K><<<(kSelectSample + 255) / 256, 256, 0, st>>>(A + lo, m, kSelectSample, seed, smp));
+        QTRY(blocksort_one<K>(smp, smp, 0, kSelectSample, st, led));
+        const double frac = (double)(k0 - lo) / (double)m;
+        const int64_t r = (int64_t)(frac * kSelectSample);
+        const size_t i1 = (size_t)std::max<int64_t>(0, r - (int64_t)kSelectBand);
+        const size_t i2 = (size_t)std::min<int64_t>(kSelectSample - 1, r + (int64_t)kSelectBand);
+        K h[2];
+        QCK(cudaMemcpyAsync(&h[0], smp + i1, sizeof(K), cudaMemcpyDeviceToHost, st));
+        QCK(cudaMemcpyAsync(&h[1], smp + i2, sizeof(K), cudaMemcpyDeviceToHost, st));
+        QCK(cudaStreamSynchronize(st));
+        ++led.syncs;
+        K sp[3];
+        uint32_t ns = 0;
+        if (!HostKey<K>::is_min(h[0])) sp[ns++] = HostKey<K>::pred(h[0]);  // bucket "< s1"
+        const uint32_t eqb = ns;                                            // bucket "== s1"
+        sp[ns++] = h[0];
+        if (!HostKey<K>::eq(h[0], h[1])) sp[ns++] = h[1];
+        QCK(cudaMemcpyAsync(dspl, sp, sizeof(K) * ns, cudaMemcpyHostToDevice, st));
+        QTRY(partition_given<K>(A + lo, m, dspl, ns, B + lo, dcnt, ws, L, st, led));
+        uint64_t cnt[4] = {0, 0, 0, 0};
+        QCK(cudaMemcpyAsync(cnt, dcnt, sizeof(uint64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
+        QCK(cudaMemcpyAsync(A + lo, B + lo, m * sizeof(K), cudaMemcpyDeviceToDevice, st));
+        QCK(cudaStreamSynchronize(st));
+        ++led.syncs;
+        ++led.levels;
+        const size_t want = k0 - lo;
+        size_t acc = 0;
+        uint32_t b = 0;
+        while (b < ns && want >= acc + cnt[b]) acc += cnt[b++];
+        if (b == eqb) return QMSORT_OK;  // rank k sits among keys equal to s1
+        lo += acc;
+        hi = lo + cnt[b];
+    }
+}
+
+static size_t select_ws_bytes(int dt, size_t n) {
+    const size_t nn = std::max<size_t>(n, 2);
+    switch (core_dtype(dt)) {
+        case QMSORT_DT_U32: return make_layout<uint32_t>(nn).total + select_extra_bytes<uint32_t>();
+        case QMSORT_DT_U64: return make_layout<uint64_t>(nn).total + select_extra_bytes<uint64_t>();
+        case QMSORT_DT_REC32: return make_layout<Rec32>(nn).total + select_extra_bytes<Rec32>();
+    }
+    return 0;
+}
+
+static int select_device(int dt, int cmp, void* d, size_t n, size_t k, size_t* pos,
+                         const qmsort_gpu_config* cfgp, void* wsp, size_t ws_bytes,
+                         qmsort_gpu_metrics* m, cudaStream_t st) {
+    QTRY(validate(dt, cmp, n, d));
+    if (k < 1 || k > n) return fail(QMSORT_EINVAL, "k must satisfy 1 <= k <= n (1-based rank)");
+    qmsort_gpu_config tmp;
+    const qmsort_gpu_config& cfg = cfg_or_default(cfgp, tmp);
+    CallFrame f(st);
+    QTRY(f.begin(cfg, wsp, ws_bytes, n > 1 ? select_ws_bytes(dt, n) : 0));
+    int rc = QMSORT_OK;
+    if (n > 1) {
+        rc = run_transform(dt, cmp, d, n, 0, st, f.led);
+        unsigned char* w = static_cast<unsigned char*>(f.ws);
+        const size_t nn = std::max<size_t>(n, 2);
+        if (rc == QMSORT_OK) {
+            switch (core_dtype(dt)) {
+                case QMSORT_DT_U32:
+                    rc = select_core<uint32_t>(static_cast<uint32_t*>(d), n, k - 1, cfg, w, make_layout<uint32_t>(nn), st, f.led);
+                    break;
+                case QMSORT_DT_U64:
+                    rc = select_core<uint64_t>(static_cast<uint64_t*>(d), n, k - 1, cfg, w, make_layout<uint64_t>(nn), st, f.led);
+                    break;
+                case QMSORT_DT_REC32:
+                    rc = select_core<Rec32>(static_cast<Rec32*>(d), n, k - 1, cfg, w, make_layout<Rec32>(nn), st, f.led);
+                    break;
+            }
+        }
+        if (rc == QMSORT_OK) rc = run_transform(dt, cmp, d, n, 1, st, f.led);
+    }
+    rc = f.end(rc, m);
+    if (rc == QMSORT_OK && pos) *pos = k - 1;
+    return rc;
+}
+
+// Per-thread cached device arena (grow-only) and stream for the host-array
+// entry points.
+struct HostArena {
+    void* buf = nullptr;
+    size_t bytes = 0;
+    cudaStream_t st = nullptr;
+    ~HostArena() {
+        if (buf) cudaFree(buf);
+        if (st) cudaStreamDestroy(st);
+    }
+};
+static int host_arena(size_t need, unsigned char** base, cudaStream_t* st) {
+    static thread_local HostArena ar;
+    if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
+    if (ar.bytes < need) {
+        if (ar.buf) QCK(cudaFree(ar.buf));
+        ar.buf = nullptr;
+        ar.bytes = 0;
+        QCK(cudaMalloc(&ar.buf, need));
+        ar.bytes = need;
+    }
+    *base = static_cast<unsigned char*>(ar.buf);
+    *st = ar.st;
+    return QMSORT_OK;
+}
+
 }  // namespace qmsort_b200
 
 using namespace qmsort_b200;
@@ -781,33 +1068,76 @@ int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsor
         if (metrics) std::memset(metrics, 0, sizeof(*metrics));
         return QMSORT_OK;
     }
-    // Per-thread cached device arena (grow-only) and stream.
-    struct Arena {
-        void* buf = nullptr;
-        size_t bytes = 0;
-        cudaStream_t st = nullptr;
-        ~Arena() {
-            if (buf) cudaFree(buf);
-            if (st) cudaStreamDestroy(st);
-        }
-    };
-    static thread_local Arena ar;
     const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
     const size_t need = data_bytes + ws_bytes_for(dtype, n);
-    if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
-    if (ar.bytes < need) {
-        if (ar.buf) QCK(cudaFree(ar.buf));
-        ar.buf = nullptr;
-        ar.bytes = 0;
-        QCK(cudaMalloc(&ar.buf, need));
-        ar.bytes = need;
-    }
-    unsigned char* base = static_cast<unsigned char*>(ar.buf);
-    QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, ar.st));
-    int rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, need - data_bytes, metrics, ar.st);
+    unsigned char* base = nullptr;
+    cudaStream_t st = nullptr;
+    QTRY(host_arena(need, &base, &st));
+    QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, st));
+    int rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, need - data_bytes, metrics, st);
     if (rc != QMSORT_OK) return rc;
-    QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, ar.st));
-    QCK(cudaStreamSynchronize(ar.st));
+    QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
+    return QMSORT_OK;
+}
+
+size_t qmsort_gpu_elements_workspace_bytes(size_t n, size_t elem_bytes) {
+    return elem_layout(n, elem_bytes).total;
+}
+
+int qmsort_gpu_sort_elements(int key_dtype, int cmp, void* d_data, size_t n, size_t elem_bytes,
+                             size_t key_offset, const qmsort_gpu_config* cfg, void* d_ws,
+                             size_t ws_bytes, qmsort_gpu_metrics* metrics, void* stream) {
+    return sort_elements_device(key_dtype, cmp, d_data, n, elem_bytes, key_offset, cfg, d_ws,
+                                ws_bytes, metrics, static_cast<cudaStream_t>(stream));
+}
+
+int qmsort_gpu_sort_elements_host(int key_dtype, int cmp, void* h_data, size_t n,
+                                  size_t elem_bytes, size_t key_offset,
+                                  const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics) {
+    QTRY(validate_elems(key_dtype, cmp, h_data, n, elem_bytes, key_offset));
+    if (n <= 1) {
+        if (metrics) std::memset(metrics, 0, sizeof(*metrics));
+        return QMSORT_OK;
+    }
+    const size_t data_bytes = align_up(n * elem_bytes, 256);
+    const size_t ws = elem_layout(n, elem_bytes).total;
+    unsigned char* base = nullptr;
+    cudaStream_t st = nullptr;
+    QTRY(host_arena(data_bytes + ws, &base, &st));
+    QCK(cudaMemcpyAsync(base, h_data, n * elem_bytes, cudaMemcpyHostToDevice, st));
+    QTRY(sort_elements_device(key_dtype, cmp, base, n, elem_bytes, key_offset, cfg, base + data_bytes,
+                              ws, metrics, st));
+    QCK(cudaMemcpyAsync(h_data, base, n * elem_bytes, cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
+    return QMSORT_OK;
+}
+
+size_t qmsort_gpu_select_workspace_bytes(int dtype, size_t n) {
+    if (dtype_size(dtype) == 0) return 0;
+    return select_ws_bytes(dtype, n);
+}
+
+int qmsort_gpu_select_nth(int dtype, int cmp, void* d_data, size_t n, size_t k, size_t* pos,
+                          const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes,
+                          qmsort_gpu_metrics* metrics, void* stream) {
+    return select_device(dtype, cmp, d_data, n, k, pos, cfg, d_ws, ws_bytes, metrics,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int qmsort_gpu_select_nth_host(int dtype, int cmp, void* h_data, size_t n, size_t k, size_t* pos,
+                               const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics) {
+    QTRY(validate(dtype, cmp, n, h_data));
+    if (k < 1 || k > n) return fail(QMSORT_EINVAL, "k must satisfy 1 <= k <= n (1-based rank)");
+    const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
+    const size_t ws = select_ws_bytes(dtype, n);
+    unsigned char* base = nullptr;
+    cudaStream_t st = nullptr;
+    QTRY(host_arena(data_bytes + ws, &base, &st));
+    QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, st));
+    QTRY(select_device(dtype, cmp, base, n, k, pos, cfg, base + data_bytes, ws, metrics, st));
+    QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
     return QMSORT_OK;
 }
 
@@ -911,6 +1241,7 @@ int qmsort_gpu_check(int dtype, int cmp, const void* d, size_t n, int check_orde
             case QMSORT_DT_U32: QCHK(uint32_t); break;
             case QMSORT_DT_U64: QCHK(uint64_t); break;
             case QMSORT_DT_F64: QCHK(double); break;
+            case QMSORT_DT_I64: QCHK(int64_t); break;
             case QMSORT_DT_REC32: QCHK(Rec32); break;
         }
 #undef QCHK

@@ -27,7 +27,7 @@ from typing import Any, Sequence
 from . import _lib
 
 CORE = {_lib.DT_I32: _lib.DT_U32, _lib.DT_U32: _lib.DT_U32, _lib.DT_U64: _lib.DT_U64,
-        _lib.DT_F64: _lib.DT_U64, _lib.DT_REC32: _lib.DT_REC32}
+        _lib.DT_F64: _lib.DT_U64, _lib.DT_REC32: _lib.DT_REC32, _lib.DT_I64: _lib.DT_U64}
 
 
 def _words(dt: int) -> int:

@@ -65,7 +65,52 @@ int main() {
     CHECK(std::is_sorted(r.begin(), r.end(), [](const Rec& a, const Rec& b) {
         return std::lexicographical_compare(a.w, a.w + 4, b.w, b.w + 4);
     }));
+    // int64 keys (the reference profile's Vec, test_sort.cpp:22)
+    std::vector<std::int64_t> q64(200000);
+    for (auto& x : q64) {
+        s = s * 6364136223846793005ull + 1442695040888963407ull;
+        x = (std::int64_t)s;
+    }
+    auto q64b = q64;
+    qmsort::gpu::sort(q64.begin(), q64.end());
+    std::sort(q64b.begin(), q64b.end());
+    CHECK(q64 == q64b);
+    // key + payload elements: ordered on the key alone, equal keys stay in input order
+    struct Elem {
+        std::int64_t key;
+        unsigned char payload[16];
+    };
+    std::vector<Elem> ev(30000);
+    for (std::size_t i = 0; i < ev.size(); ++i) {
+        ev[i].key = (std::int64_t)((i * 7919) % 97) - 48;
+        for (int b = 0; b < 16; ++b) ev[i].payload[b] = (unsigned char)(i >> (b % 3 * 8));
+    }
+    auto ev2 = ev;
+    qmsort::gpu::sort(ev.begin(), ev.end());
+    std::stable_sort(ev2.begin(), ev2.end(), [](const Elem& a, const Elem& b) { return a.key < b.key; });
+    CHECK(std::equal(ev.begin(), ev.end(), ev2.begin(), [](const Elem& a, const Elem& b) {
+        return a.key == b.key && std::equal(a.payload, a.payload + 16, b.payload);
+    }));
+    // select_nth (selection.hpp:207-212), 1-based k
+    {
+        auto a = q64b;
+        std::reverse(a.begin(), a.end());
+        const std::size_t p = qmsort::gpu::select_nth(a.begin(), a.end(), 777);
+        CHECK(p == 776 && a[p] == q64b[776]);
+        CHECK(std::all_of(a.begin(), a.begin() + p, [&](std::int64_t x) { return x <= a[p]; }));
+        CHECK(std::all_of(a.begin() + p + 1, a.end(), [&](std::int64_t x) { return x >= a[p]; }));
+    }
 #ifdef WITH_REFERENCE
+    {
+        // the reference's own Element<16> (test_sort.cpp:328-339)
+        std::vector<qmsort::Element<16>> re(5000);
+        for (std::size_t i = 0; i < re.size(); ++i) {
+            re[i].key = (std::int64_t)((i * 31) % 50);
+            re[i].payload[0] = std::byte{(unsigned char)i};
+        }
+        qmsort::gpu::sort(re.begin(), re.end(), qmsort::qms());
+        CHECK(std::is_sorted(re.begin(), re.end()));
+    }
     // the reference's own config objects and comparator types drop straight in
     std::vector<std::int32_t> v{7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8};
     qmsort::gpu::sort(v.begin(), v.end(), qmsort::hqms(), std::greater<>{});

@@ -20,14 +20,18 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(HERE))
-from oracle_lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64, Oracle  # noqa: E402
+from oracle_lib import DT_F64, DT_I32, DT_I64, DT_REC32, DT_U32, DT_U64, Oracle  # noqa: E402
 
 N_CFG = 1 << 16
 SEEDS = [42, 1, 2]
 CONFIGS = {
     "i32_perm": DT_I32, "u32": DT_U32, "u64": DT_U64, "f64_sorted": DT_F64, "f64_reverse": DT_F64,
     "f64_distinct16": DT_F64, "f64_gauss": DT_F64, "f64_organ": DT_F64, "rec32": DT_REC32,
+    "i64": DT_I64,
 }
+# select_nth cases (selection.hpp:207-212; test_selection.cpp:101-160): n, k, seed, greater
+SELECT_CASES = [(6, 1, 0, 0), (101, 51, 1, 0), (1000, 1, 2, 0), (1000, 1000, 3, 0),
+                (4096, 2048, 4, 0), (4096, 17, 5, 1), (65536, 30000, 6, 0), (65536, 65536, 7, 1)]
 VARIANTS = {"qms": 0, "qmqs": 1, "momqms": 2, "hqms": 3}
 
 
@@ -87,6 +91,26 @@ def main() -> None:
             rec["qms_greater_sha256"] = sha(o.ref_sort(dt, a, greater=True))
             cfgs[f"{name}/{seed}"] = rec
     out["configs"] = cfgs
+
+    # Element<16> (element.hpp:13-20; test_sort.cpp:328-339): the reference's key
+    # sequence and element multiset (its arrangement of equal keys is its own)
+    elems = []
+    for n, seed, greater in [(100, 8, 0), (2000, 9, 0), (2000, 10, 1), (1 << 14, 11, 0)]:
+        a = o.gen_elem16(n, seed)
+        r = o.ref_sort_elem16(a, greater=bool(greater))
+        canon = np.sort(r.view(np.uint8).reshape(n, 24).view("V24").reshape(n))
+        elems.append({"n": n, "seed": seed, "greater": greater, "input_sha256": sha(a),
+                      "keys_sha256": sha(np.ascontiguousarray(r["key"])),
+                      "multiset_sha256": sha(canon)})
+    out["elements16"] = elems
+
+    sel = []
+    for n, k, seed, greater in SELECT_CASES:
+        a = o.gen("i64", n, seed=seed)
+        p, b = o.ref_select_nth_i64(a, k, greater=bool(greater))
+        sel.append({"n": n, "k": k, "seed": seed, "greater": greater, "pos": p,
+                    "value": int(b[p])})
+    out["select_nth"] = sel
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print(f"wrote {len(cfgs)} config records")

@@ -59,9 +59,13 @@ def test_presets_mirror_sortconfig():
 
 def test_dtype_helpers_and_workspace():
     lib = _lib.load()
-    assert [lib.qmsort_gpu_dtype_size(d) for d in range(5)] == [4, 4, 8, 8, 32]
+    assert [lib.qmsort_gpu_dtype_size(d) for d in range(6)] == [4, 4, 8, 8, 32, 8]
     assert lib.qmsort_gpu_dtype_size(9) == 0
-    assert [lib.qmsort_gpu_core_dtype(d) for d in range(5)] == [1, 1, 2, 2, 4]
+    assert [lib.qmsort_gpu_core_dtype(d) for d in range(6)] == [1, 1, 2, 2, 4, 2]
+    # f3 / f4 workspaces: records + Rec32 samplesort + gathered elements; select
+    we = lib.qmsort_gpu_elements_workspace_bytes(1 << 20, 24)
+    assert we >= (1 << 20) * (32 + 32 + 24)
+    assert lib.qmsort_gpu_select_workspace_bytes(5, 1 << 20) > lib.qmsort_gpu_workspace_bytes(5, 1 << 20, None)
     w1 = lib.qmsort_gpu_workspace_bytes(1, 1 << 20, None)
     w2 = lib.qmsort_gpu_workspace_bytes(1, 1 << 24, None)
     assert (1 << 20) * 4 <= w1 < w2
@@ -81,6 +85,15 @@ def test_invalid_arguments_are_rejected_before_any_cuda_call():
     assert lib.qmsort_gpu_sort(1, 0, ctypes.addressof(buf), 1 << 32, ctypes.byref(c), None, 0, None, None) == _lib.QMSORT_EINVAL
     assert lib.qmsort_gpu_partition(0, ctypes.addressof(buf), 4, None, 5, None, None, None, 0, None) == _lib.QMSORT_EINVAL
     assert lib.qmsort_gpu_generate(99, ctypes.addressof(buf), 4, 0, 0, 0, None) == _lib.QMSORT_EINVAL
+    # elements: bad element size / misaligned key / record keys; select: k out of range
+    sz = ctypes.c_size_t(0)
+    for args in [(5, 2, 24, 0), (5, 0, 22, 0), (5, 0, 24, 4), (4, 0, 64, 0), (5, 0, 8, 4)]:
+        kd, cm, eb, ko = args
+        assert lib.qmsort_gpu_sort_elements_host(kd, cm, ctypes.addressof(buf), 2, eb, ko, None, None) == _lib.QMSORT_EINVAL, args
+    for k in (0, 5):
+        assert lib.qmsort_gpu_select_nth_host(1, 0, ctypes.addressof(buf), 4, k, ctypes.byref(sz), None, None) == _lib.QMSORT_EINVAL
+        assert lib.qmsort_gpu_select_nth(1, 0, ctypes.addressof(buf), 4, k, ctypes.byref(sz), None, None, 0, None, None) == _lib.QMSORT_EINVAL
+    assert b"1-based" in lib.qmsort_gpu_last_error()
     with pytest.raises(ValueError):
         q.sort(np.zeros(4, np.int16))
     with pytest.raises(ValueError):

@@ -9,12 +9,12 @@ import numpy as np
 import pytest
 
 import paper_1804_10062_b200 as q
-from oracle_lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64
+from oracle_lib import DT_F64, DT_I32, DT_I64, DT_REC32, DT_U32, DT_U64
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-DTYPES = [DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32]
+DTYPES = [DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32, DT_I64]
 
 
 def rand_input(dt, n, seed, dist="uniform"):
@@ -47,6 +47,8 @@ def rand_input(dt, n, seed, dist="uniform"):
         return (raw >> np.uint64(7) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
     if dt == DT_U64:
         return raw.astype(np.uint64)
+    if dt == DT_I64:  # the reference profile's key type (test_sort.cpp:22)
+        return (raw - np.uint64(1 << 62) if dist != "uniform" else raw).astype(np.uint64).view(np.int64)
     if dt == DT_F64:
         # finite doubles, no NaN / -0.0: scale signed integers
         s = (raw >> np.uint64(11)).astype(np.int64) - (1 << 51)
@@ -132,7 +134,7 @@ def test_fuzz_all_variants(oracle):
     rng = np.random.default_rng(1001)
     for trial in range(60):
         n = int(rng.integers(0, 3000))
-        dt = DTYPES[trial % 5]
+        dt = DTYPES[trial % len(DTYPES)]
         dist = ["uniform", "sorted", "reverse", "organpipe", "fewdistinct", "allequal"][trial % 6]
         a = rand_input(dt, n, seed=trial, dist=dist)
         for preset in (q.qms, q.qmqs, q.momqms, q.hqms):
@@ -141,12 +143,13 @@ def test_fuzz_all_variants(oracle):
 
 
 @pytest.mark.parametrize("cfgname", ["i32_perm", "u32", "u64", "f64_sorted", "f64_reverse",
-                                     "f64_distinct16", "f64_gauss", "f64_organ", "rec32"])
+                                     "f64_distinct16", "f64_gauss", "f64_organ", "rec32", "i64"])
 def test_config_shapes_reduced(oracle, cfgname):
     """The five BASELINE configs at 2^20 elements, seeded recipes of SURVEY.md 8(d)."""
     n = 1 << 20
     a = oracle.gen(cfgname, n, seed=42)
-    dt = {"i32_perm": DT_I32, "u32": DT_U32, "u64": DT_U64, "rec32": DT_REC32}.get(cfgname, DT_F64)
+    dt = {"i32_perm": DT_I32, "u32": DT_U32, "u64": DT_U64, "rec32": DT_REC32,
+          "i64": DT_I64}.get(cfgname, DT_F64)
     got, _ = gpu_sort(a)
     if cfgname == "i32_perm":
         np.testing.assert_array_equal(got, np.arange(n, dtype=np.int32))  # closed form

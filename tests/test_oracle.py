@@ -14,7 +14,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle_lib import DT_F64, DT_I32, DT_REC32, DT_U32, DT_U64
+from oracle_lib import DT_F64, DT_I32, DT_I64, DT_REC32, DT_U32, DT_U64, ELEM16
 
 GOLDEN = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
 
@@ -96,7 +96,8 @@ def test_fuzz_oracle_vs_reference(oracle):
         oracle.ref.qmsref_generate(kind, param, n, int(rng.integers(0, 2**62)),
                                    v.ctypes.data_as(ctypes.c_void_p))
         v = v[:n]
-        for dt, conv in [(DT_I32, np.int32), (DT_U32, np.uint32), (DT_U64, np.uint64), (DT_F64, np.float64)]:
+        for dt, conv in [(DT_I32, np.int32), (DT_U32, np.uint32), (DT_U64, np.uint64), (DT_F64, np.float64),
+                         (DT_I64, np.int64)]:
             a = v.astype(conv)
             for greater in (False, True):
                 np.testing.assert_array_equal(oracle.sort(dt, a, greater),
@@ -114,3 +115,48 @@ def test_is_sorted_helper(oracle):
     assert oracle.is_sorted(DT_U32, a)
     assert not oracle.is_sorted(DT_U32, a[::-1].copy())
     assert oracle.is_sorted(DT_U32, a[::-1].copy(), greater=True)
+
+
+def canon_elems(a):
+    """Element multiset in canonical (byte-sorted) form."""
+    n = a.shape[0]
+    return np.sort(np.ascontiguousarray(a).view(np.uint8).reshape(n, 24).view("V24").reshape(n))
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_elements16_golden(oracle, case):
+    """Element<16> (element.hpp:13-20): the oracle's qms over the keys gives the
+    reference's key sequence; the input recipe and multiset match the frozen
+    digests (test_sort.cpp:328-339)."""
+    g = GOLDEN["elements16"][case]
+    a = oracle.gen_elem16(g["n"], g["seed"])
+    assert a.dtype == ELEM16
+    assert sha(a) == g["input_sha256"]
+    keys = oracle.sort(DT_I64, np.ascontiguousarray(a["key"]), greater=bool(g["greater"]))
+    assert sha(keys) == g["keys_sha256"]
+    assert sha(canon_elems(a)) == g["multiset_sha256"]
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_select_nth_golden(oracle, case):
+    """select_nth (selection.hpp:207-212): the oracle's sorted order puts the
+    reference's k-th element at k-1 (test_selection.cpp:101-160)."""
+    g = GOLDEN["select_nth"][case]
+    a = oracle.gen("i64", g["n"], seed=g["seed"])
+    s = oracle.sort(DT_I64, a, greater=bool(g["greater"]))
+    assert g["pos"] == g["k"] - 1
+    assert int(s[g["k"] - 1]) == g["value"]
+
+
+@needs_ref
+def test_reference_select_partitions(oracle):
+    """The reference's select_nth leaves the range partitioned around k-1
+    (selection.hpp:124-126) -- the contract the GPU select keeps."""
+    rng = np.random.default_rng(5)
+    for n in (1, 7, 100, 5000):
+        a = rng.integers(-50, 50, n).astype(np.int64)
+        for k in (1, (n + 1) // 2, n):
+            p, b = oracle.ref_select_nth_i64(a, k)
+            assert p == k - 1
+            assert (b[:p] <= b[p]).all() and (b[p + 1:] >= b[p]).all()
+            np.testing.assert_array_equal(np.sort(b), np.sort(a))
