@@ -54,15 +54,20 @@ typedef enum {
 /* ---- SortConfig as C scalars (sort.hpp:17-34, merge.hpp:14-31) --------- */
 typedef struct {
     int variant;                     /* Variant: 0 qms 1 qmqs 2 momqms 3 hqms       */
-    int pivot;                       /* PivotStrategy: 0 median_of_3,
-                                        1 median_of_sqrt_n, 2 mom_of_thirds,
-                                        3 hybrid                                   */
+    int pivot;                       /* PivotStrategy: 0 median_of_3 and
+                                        1 median_of_sqrt_n -> seeded random sample;
+                                        2 mom_of_thirds -> strided triple-median
+                                        sample at every level; 3 hybrid -> random,
+                                        triple medians for buckets outside the
+                                        delta band                                 */
     int base_case_kind;              /* BaseCase: 0 insertion 1 hardcoded_small
                                         2 clever_quicksort                         */
     uint64_t base_case_size_threshold; /* BaseCasePolicy::size_threshold (10)     */
     int base_case_use_levels;        /* BaseCasePolicy::use_levels                 */
     double beta;                     /* 0.5                                        */
-    double delta;                    /* 1/16                                       */
+    double delta;                    /* 1/16; hybrid: a bucket larger than
+                                        (parent / buckets) / delta is re-split with
+                                        the triple-median sample next level         */
     int side;                        /* MergesortSide: 0 smaller_always,
                                         1 larger_when_feasible (ignored on GPU)     */
     int three_way;                   /* always on for equal splitters on the GPU    */
@@ -93,6 +98,8 @@ typedef struct {
     uint64_t phase_bytes[QMSORT_NUM_PHASES];   /* algorithmic bytes per family */
     uint64_t phase_ns[QMSORT_NUM_PHASES];      /* device ns (profile = 1 only)  */
     uint32_t phase_launches[QMSORT_NUM_PHASES];
+    uint32_t resplits;    /* hybrid pivot: buckets outside the delta band that
+                             were re-sampled with triple medians (sort.hpp:114-118) */
 } qmsort_gpu_metrics;
 
 /* Presets qms() / qmqs() / momqms() / hqms() (sort.hpp:37-66). */

@@ -157,6 +157,7 @@ class Metrics:
     phase_bytes: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
     phase_ns: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
     phase_launches: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
+    resplits: int = 0  # hybrid pivot: buckets re-sampled with triple medians (f1)
 
     @classmethod
     def from_c(cls, m: _lib.GpuMetrics) -> "Metrics":

@@ -64,6 +64,7 @@ class GpuMetrics(ctypes.Structure):
         ("phase_bytes", ctypes.c_uint64 * 8),
         ("phase_ns", ctypes.c_uint64 * 8),
         ("phase_launches", ctypes.c_uint32 * 8),
+        ("resplits", ctypes.c_uint32),
     ]
 
 

@@ -125,7 +125,7 @@ enum Phase {
 // CUDA-event device time of every launch.
 struct Ledger {
     uint64_t alg_bytes = 0;
-    uint32_t launches = 0, syncs = 0, levels = 0, merge_passes = 0;
+    uint32_t launches = 0, syncs = 0, levels = 0, merge_passes = 0, resplits = 0;
     uint64_t ph_bytes[QMSORT_NUM_PHASES] = {};
     uint32_t ph_launches[QMSORT_NUM_PHASES] = {};
     bool prof = false;
@@ -330,6 +330,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     p.task_cap = L.task_cap;
     p.fill_cap = L.fill_cap;
     p.dst_is_a = 0;
+    p.pivot = (uint32_t)std::max(0, cfg.pivot);
+    const double dl = std::min(1.0, std::max(1.0 / 65536.0, cfg.delta > 0 ? cfg.delta : 1.0 / 16.0));
+    p.delta_q16 = (uint32_t)(dl * 65536.0);
 
     LevelBufs lv[2];
     K* tree[2];
@@ -410,6 +413,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         if (hc[0].overflow || hc[1].overflow)
             return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
         ++led.levels;
+        led.resplits += hc[0].resplits;
         // block-sort every bucket of this level; the bytes are credited to the
         // level's first launch
         uint64_t bs_bytes = 2ull * hc[0].task_keys * sizeof(K);
@@ -519,6 +523,7 @@ static void fill_metrics(qmsort_gpu_metrics* m, Ledger& led, float ms) {
     m->merge_passes = led.merge_passes;
     m->kernel_launches = led.launches;
     m->host_syncs = led.syncs + 1;
+    m->resplits = led.resplits;
     for (int i = 0; i < QMSORT_NUM_PHASES; ++i) {
         m->phase_bytes[i] = led.ph_bytes[i];
         m->phase_launches[i] = led.ph_launches[i];
@@ -657,7 +662,8 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
         d.hist_base = 0;
         d.shift = shift;
         d.lutbits = lutbits;
-        d.pad[0] = d.pad[1] = d.pad[2] = 0;
+        d.sampler = kSampleRandom;
+        d.pad[0] = d.pad[1] = 0;
         *seg = d;
     }
 }

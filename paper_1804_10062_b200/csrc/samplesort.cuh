@@ -58,8 +58,17 @@ struct SegDesc {
                            // entry i = nchunks holds the bucket total, then its start
     uint32_t shift;        // LUT cell = (key - lo) >> shift
     uint32_t lutbits;      // 2^lutbits LUT cells
-    uint32_t pad[3];
+    uint32_t sampler;      // kSampleRandom or kSampleTriples (worst-case policy, f1)
+    uint32_t pad[2];
 };
+
+// K1 sampling rules.  kSampleRandom: seeded random
+// positions (median_of_3 / median_of_sqrt_n presets).  kSampleTriples: the
+// median of three adjacent keys at evenly strided positions, no seed -- the
+// sample analogue of triple_median_pivot (selection.hpp:219-229), used at
+// every level by mom_of_thirds and, under hybrid, for a bucket that came out
+// outside the delta band (pivot_outside_band, sort.hpp:114-118).
+enum : uint32_t { kSampleRandom = 0, kSampleTriples = 1 };
 
 struct ChunkDesc {
     uint32_t seg;
@@ -90,7 +99,7 @@ struct LevelCounters {
     uint32_t ntasks[kNumClasses];
     uint32_t overflow;  // capacity exceeded somewhere (host reports an error)
     uint32_t work_count, work_scatter;  // dynamic chunk dispensers of this level's kernels
-    uint32_t pad;
+    uint32_t resplits;  // hybrid: children re-sampled with triple medians (f1)
     unsigned long long nkeys;      // keys in this level's segments (pass ledger)
     unsigned long long task_keys;  // keys handed to the block sorter
     unsigned long long fill_keys;  // keys written by equal-bucket fills
@@ -111,6 +120,8 @@ struct PlanParams {
     uint32_t class_cap[kNumClasses];
     uint32_t task_cap, fill_cap;
     int dst_is_a;           // this level's scatter writes the caller's buffer
+    uint32_t pivot;         // PivotStrategy (sort.hpp:19): 2 mom_of_thirds, 3 hybrid
+    uint32_t delta_q16;     // SortConfig::delta in 1/65536 (hybrid skew band)
 };
 
 __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
@@ -135,7 +146,8 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
 // Append a segment (and, unless write_chunks is false, its chunk table) to
 // the next level.  Called by one thread.  Returns false on capacity overflow.
 __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len, uint64_t lo,
-                                    uint64_t hi, const PlanParams& p, bool write_chunks = true) {
+                                    uint64_t hi, const PlanParams& p, uint32_t sampler,
+                                    bool write_chunks = true) {
     const uint32_t logk = choose_logk(len, p.target, p.log_kmax);
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
     const uint32_t hwords = (nch + 1) * (2u << logk);
@@ -165,7 +177,8 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     uint32_t bl = 0;
     while (bl < 64 && (span >> bl) != 0) ++bl;  // bit length of span
     d.shift = bl > d.lutbits ? bl - d.lutbits : 0;
-    d.pad[0] = d.pad[1] = d.pad[2] = 0;
+    d.sampler = sampler;
+    d.pad[0] = d.pad[1] = 0;
     nb.segs[s] = d;
     atomicAdd(&nb.cnt->nkeys, (unsigned long long)len);
     for (uint32_t i = 0; write_chunks && i < nch; ++i) {
@@ -182,7 +195,8 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
 // Level 0: one segment covering [0, n); its (many) chunks are written by all
 // threads of the grid.
 __global__ void init_level_kernel(LevelBufs nb, uint64_t n, uint64_t key_max, PlanParams p) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) emit_segment(nb, 0, n, 0, key_max, p, false);
+    if (threadIdx.x == 0 && blockIdx.x == 0)
+        emit_segment(nb, 0, n, 0, key_max, p, p.pivot == 2 ? kSampleTriples : kSampleRandom, false);
     const uint32_t nch = (uint32_t)((n + p.chunk_elems - 1) / p.chunk_elems);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nch && i < nb.chunk_cap;
          i += gridDim.x * blockDim.x) {
@@ -307,17 +321,26 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
     const uint32_t K_ = 1u << d.logk;
     const int S = (int)min((uint32_t)BS::kCap, max(1024u, oversample * K_));
 
-    // Seeded sample with replacement (counter-based SplitMix64 of the sample
-    // index; uniform position via a 64x64 high multiply).
+    // kSampleRandom: seeded sample with replacement (counter-based SplitMix64
+    // of the sample index; uniform position via a 64x64 high multiply).
+    // kSampleTriples: median of the three keys at stride position idx.
     K k[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int idx = (int)threadIdx.x * ITEMS + i;
-        if (idx < S) {
+        if (idx >= S) {
+            k[i] = KT::max_key();
+        } else if (d.sampler == kSampleTriples) {
+            const uint64_t p0 = ((uint64_t)idx * d.len) / (uint64_t)S;
+            const K* t = src + d.off + min(p0, d.len - 3);
+            K a = t[0], b = t[1], c = t[2];
+            KT::cas(a, b);  // a <= b
+            KT::cas(b, c);  // c = max; b = median candidate
+            KT::cas(a, b);  // b = median of three
+            k[i] = b;
+        } else {
             const uint64_t h = sm_mix(seed + (d.off + 1) * kGamma + (uint64_t)(idx + 1) * 0xD1B54A32D192ED03ull);
             k[i] = src[d.off + __umul64hi(h, d.len)];
-        } else {
-            k[i] = KT::max_key();
         }
     }
     BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
@@ -589,7 +612,16 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 if (j > 0) clo = KeyTraits<K>::bits(sp[j - 1]) + 1;
                 if (j < d.m) chi = KeyTraits<K>::bits(sp[j]);
             }
-            emit_segment(next, off, len, clo, chi, p);
+            // worst-case policy (f1): mom_of_thirds always samples triple
+            // medians; hybrid does so for a child outside the delta band,
+            // i.e. larger than (parent / buckets) / delta
+            uint32_t sampler = p.pivot == 2 ? kSampleTriples : kSampleRandom;
+            if (p.pivot == 3 &&
+                (uint64_t)len * (uint64_t)(1u << d.logk) * p.delta_q16 > d.len * 65536ull) {
+                sampler = kSampleTriples;
+                atomicAdd(&cur_cnt->resplits, 1u);
+            }
+            emit_segment(next, off, len, clo, chi, p, sampler);
         }
     }
 }
