@@ -109,6 +109,39 @@ std::uint64_t qmsref_splitmix(std::uint64_t seed, std::uint64_t j) {
     return x;
 }
 
+// mix_seed (rng.hpp:41-44), the per-trial seed stream of the CLI harness.
+std::uint64_t qmsref_mix_seed(std::uint64_t seed, std::uint64_t stream) {
+    return qmsort::mix_seed(seed, stream);
+}
+
+// kCsvHeader and to_csv (trial.hpp:62-77) of a record with the given fields;
+// returns the length written into buf (cap bytes).
+int qmsref_csv(char* buf, int cap, const char* algo, std::size_t n, const char* dist,
+               std::uint64_t seed, std::uint64_t trial, std::uint64_t comparisons,
+               std::uint64_t moves, std::uint64_t time_ns, std::uint64_t depth, double lin,
+               double ratio, int header) {
+    std::string s;
+    if (header) {
+        s = qmsort::kCsvHeader;
+    } else {
+        qmsort::TrialRecord r;
+        r.algorithm = algo;
+        r.n = n;
+        r.distribution = dist;
+        r.seed = seed;
+        r.trial = trial;
+        r.metrics.comparisons = comparisons;
+        r.metrics.moves = moves;
+        r.metrics.elapsed_ns = time_ns;
+        r.metrics.max_depth = depth;
+        r.cmp_norm_linear = lin;
+        r.cmp_over_nlogn = ratio;
+        s = qmsort::to_csv(r);
+    }
+    std::snprintf(buf, (std::size_t)cap, "%s", s.c_str());
+    return (int)s.size();
+}
+
 // qmsort::sort over Element<16> (element.hpp:13-20, test_sort.cpp:328-339):
 // data is n raw 24-byte elements {int64 key, 16 payload bytes}.
 int qmsref_sort_elem16(void* data, std::size_t n, int greater) {

@@ -111,6 +111,34 @@ def main() -> None:
         sel.append({"n": n, "k": k, "seed": seed, "greater": greater, "pos": p,
                     "value": int(b[p])})
     out["select_nth"] = sel
+
+    # CLI harness: kCsvHeader / to_csv (trial.hpp:62-77)
+    # and the per-trial input streams of `bench` (qmsort.cpp:51-53, 112-113)
+    ref.qmsref_mix_seed.restype = ctypes.c_uint64
+    ref.qmsref_mix_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
+    ref.qmsref_csv.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_char_p, ctypes.c_size_t,
+                               ctypes.c_char_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                               ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_int]
+    buf = ctypes.create_string_buffer(512)
+    ref.qmsref_csv(buf, 512, b"", 0, b"", 0, 0, 0, 0, 0, 0, 0.0, 0.0, 1)
+    cli = {"header": buf.value.decode(), "lines": [], "trial_inputs": []}
+    for fields in [("gpu", 65536, "random", 1, 0, 0, 0, 1234567, 2, -16.0, 0.0),
+                   ("gpu-hqms", 1000, "fewdistinct:8", 7, 3, 0, 0, 99, 1, -9.965784284662087, 0.0),
+                   ("qms", 2, "randomdup:64", 18446744073709551615, 9, 1, 0, 5, 0, 0.0, 0.5)]:
+        a, n, d, sd, t, c, mv, tm, dep, lin, rat = fields
+        ref.qmsref_csv(buf, 512, a.encode(), n, d.encode(), sd, t, c, mv, tm, dep, lin, rat, 0)
+        cli["lines"].append({"fields": list(fields), "csv": buf.value.decode()})
+    for dist, kind, param, n, seed, t in [("random", 0, 0, 1000, 1, 0), ("random", 0, 0, 65536, 1, 2),
+                                          ("randomdup:64", 5, 64, 5000, 3, 1),
+                                          ("fewdistinct:8", 4, 8, 777, 1, 0),
+                                          ("organpipe", 3, 0, 1001, 1, 0)]:
+        ts = int(ref.qmsref_mix_seed(seed, n * 1000003 + t))
+        v = np.empty(n, np.int64)
+        ref.qmsref_generate(kind, param, n, ts, v.ctypes.data_as(ctypes.c_void_p))
+        cli["trial_inputs"].append({"dist": dist, "n": n, "seed": seed, "trial": t,
+                                    "trial_seed": ts, "sha256": sha(v)})
+    out["cli"] = cli
     with open(os.path.join(HERE, "golden.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     print(f"wrote {len(cfgs)} config records")
