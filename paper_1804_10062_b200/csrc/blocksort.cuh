@@ -13,6 +13,7 @@
 //      swap_merge (merge.hpp:76), so the merge is stable.
 // The tile is loaded once from HBM and written once (2 n w bytes per pass).
 #pragma once
+#include <type_traits>
 #include <utility>
 
 #include "common.cuh"
@@ -55,9 +56,17 @@ struct OddEvenNet {
     static constexpr Pairs kPairs = make();
 };
 
+// uint32 keys: compare-and-swaps finish on the FMA pipe
+// (KeyTraits<uint32_t>::cas_alt), relieving the ALU pipe the kernel is bound by.
+template <class K>
+__device__ __forceinline__ void net_cas(K& a, K& b, int) {
+    if constexpr (std::is_same_v<K, uint32_t>) KeyTraits<K>::cas_alt(a, b);
+    else KeyTraits<K>::cas(a, b);
+}
+
 template <class K, int N, size_t... I>
 __device__ __forceinline__ void apply_net(K (&k)[N], std::index_sequence<I...>) {
-    (KeyTraits<K>::cas(k[OddEvenNet<N>::kPairs.a[I]], k[OddEvenNet<N>::kPairs.b[I]]), ...);
+    (net_cas<K>(k[OddEvenNet<N>::kPairs.a[I]], k[OddEvenNet<N>::kPairs.b[I]], (int)I), ...);
 }
 
 template <class K, int N>
@@ -153,7 +162,7 @@ __device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
     for (int s = ITEMS / 2; s >= 1; s >>= 1) {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j)
-            if ((j & s) == 0) KT::cas(k[j], k[j + s]);
+            if ((j & s) == 0) net_cas<K>(k[j], k[j + s], j + s);
     }
 }
 

@@ -21,6 +21,13 @@ struct alignas(16) Rec32 {
 template <class K>
 struct KeyTraits;
 
+// Constants the compiler cannot fold (constant bank).  They let a
+// compare-and-swap finish on the FMA pipe -- max = (a - min) + b with two
+// IMADs -- so sorting networks, which are otherwise pure ALU-pipe min/max,
+// split their work over both integer pipes (B300_MICROARCH.md "Pipe rates").
+__constant__ uint32_t c_neg1 = 0xFFFFFFFFu;
+__constant__ uint32_t c_one = 1u;
+
 template <>
 struct KeyTraits<uint32_t> {
     static constexpr int kBytes = 4;
@@ -32,6 +39,13 @@ struct KeyTraits<uint32_t> {
         uint32_t lo = min(a, b), hi = max(a, b);
         a = lo;
         b = hi;
+    }
+    // same result; min on the ALU pipe, max by two IMADs on the FMA pipe
+    __device__ __forceinline__ static void cas_alt(uint32_t& a, uint32_t& b) {
+        const uint32_t lo = min(a, b);
+        const uint32_t t = lo * c_neg1 + a;  // a - lo
+        b = t * c_one + b;                   // a + b - lo = max (mod 2^32)
+        a = lo;
     }
     __device__ __forceinline__ static uint64_t hash(uint32_t a) { return a; }
     __device__ __forceinline__ static uint32_t shfl_xor(uint32_t a, int m) {
