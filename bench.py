@@ -304,23 +304,41 @@ def run_ours(args) -> None:
 
 
 def e2e(q, torch, n, pristine, cfg, args) -> dict:
-    """Same metric through the host-array drop-in (qmsort_gpu_sort_host): pinned
-    host input, H2D + sort + D2H inside the timed region."""
+    """Same metric through the host-array API: every step sorts its own pinned
+    host copy of the input and H2D + sort + D2H of every step lie inside the
+    timed region.  The steps go through qmsort_gpu_sort_host_batch (a stream of
+    independent sort requests): its two workers overlap one step's D2H with the
+    next step's H2D on the two PCIe copy engines.  The single-call latency of
+    qmsort_gpu_sort_host is reported alongside (sync_ms_per_step)."""
     host_src = pristine.cpu()
-    host = torch.empty(n, dtype=torch.uint32, pin_memory=True)
-    times = []
-    steps = max(1, min(args.steps, 5))
-    for i in range(1 + steps):  # first call warms the cached device arena
-        host.copy_(host_src)
-        t = time.perf_counter()
-        q.sort(host, cfg)
-        dt = time.perf_counter() - t
-        if i > 0:
-            times.append(dt)
-    ms = statistics.mean(times) * 1e3
+    steps = max(2, min(args.steps, 6))
+    bufs = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(steps)]
+    for b in bufs:
+        b.copy_(host_src)
+    warm = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(2)]
+    for w in warm:
+        w.copy_(host_src)
+    q.sort_batch(warm, cfg)  # warms both workers' device arenas
+    t = time.perf_counter()
+    q.sort_batch(bufs, cfg)
+    ms = (time.perf_counter() - t) / steps * 1e3
+    # correctness of what came back: sorted + same multiset as the input
+    for b in bufs[:2]:
+        d = b.cuda()
+        viol, s_out, x_out = q.check(d)
+        _, s_in, x_in = q.check(pristine, order=False)
+        if viol or s_out != s_in or x_out != x_in:
+            raise RuntimeError("e2e sort returned a wrong result")
+    # single-call latency (one thread, nothing overlapped)
+    warm[0].copy_(host_src)
+    t = time.perf_counter()
+    q.sort(warm[0], cfg)
+    sync_ms = (time.perf_counter() - t) * 1e3
     return {"value": n / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms,
             "h2d_bytes_per_step": n * 4, "d2h_bytes_per_step": n * 4,
-            "api": "qmsort_gpu_sort_host (C-ABI host drop-in), pinned host buffer"}
+            "steps": steps, "sync_ms_per_step": sync_ms,
+            "api": "qmsort_gpu_sort_host_batch (C-ABI, host arrays) over pinned host buffers, "
+                   "one array per step"}
 
 
 def main():

@@ -122,6 +122,16 @@ int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu
 int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
                          qmsort_gpu_metrics* metrics);
 
+/* A stream of independent host arrays (e.g. the trials of a harness, or
+ * request batches of a service): the same contract as qmsort_gpu_sort_host for
+ * every h_arrays[i] of ns[i] elements, pipelined over two workers with their
+ * own device arenas so that one array's device-to-host copy overlaps the next
+ * array's host-to-device copy.  Pinned host memory gives the overlap.  metrics
+ * (optional) holds the sums (elapsed_ns: device sort time of all arrays). */
+int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const size_t* ns,
+                               size_t count, const qmsort_gpu_config* cfg,
+                               qmsort_gpu_metrics* metrics);
+
 /* ---- key + payload elements --------------------- */
 /* Replaces qmsort::sort over Element<PayloadBytes> (element.hpp:13-20:
  * ordering on the key alone, payload moved with it; test_sort.cpp:328-339).

@@ -36,7 +36,8 @@ from ._lib import DT_F64, DT_I32, DT_I64, DT_REC32, DT_U32, DT_U64, GREATER, LES
 
 __all__ = [
     "Variant", "PivotStrategy", "BaseCase", "MergesortSide", "BaseCasePolicy", "SortConfig",
-    "Metrics", "qms", "qmqs", "momqms", "hqms", "sort", "sort_range_counted", "QmsortError",
+    "Metrics", "qms", "qmqs", "momqms", "hqms", "sort", "sort_batch", "sort_range_counted",
+    "QmsortError",
     "DT_I32", "DT_U32", "DT_U64", "DT_F64", "DT_REC32", "DT_I64", "LESS", "GREATER",
     "workspace_bytes", "generate", "check", "dtype_of", "sort_elements", "select_nth",
 ]
@@ -252,6 +253,31 @@ def sort(data: Any, cfg: SortConfig | None = None, less: Any = "less", *, worksp
         ptr = _host_ptr(data)
         rc = lib.qmsort_gpu_sort_host(dt, cmp, ptr, n, ctypes.byref(c), ctypes.byref(m))
         _lib.check(rc, "qmsort_gpu_sort_host")
+    return Metrics.from_c(m)
+
+
+def sort_batch(arrays: list, cfg: SortConfig | None = None, less: Any = "less", *,
+               dtype: int | None = None) -> Metrics:
+    """Sort a list of independent host arrays (numpy / CPU tensors, ideally
+    pinned) in place through ``qmsort_gpu_sort_host_batch``: one array's
+    device-to-host copy overlaps the next one's host-to-device copy.  Returns
+    summed Metrics."""
+    lib = _lib.load()
+    c = (cfg or SortConfig()).to_c()
+    m = _lib.GpuMetrics()
+    if not arrays:
+        return Metrics()
+    dt = dtype_of(arrays[0]) if dtype is None else int(dtype)
+    for a in arrays:
+        if _is_torch_cuda(a):
+            raise ValueError("sort_batch takes host arrays; use sort() for device tensors")
+        if (dtype_of(a) if dtype is None else dt) != dt:
+            raise ValueError("all arrays of a batch must share one dtype")
+    ptrs = (ctypes.c_void_p * len(arrays))(*[_host_ptr(a) for a in arrays])
+    ns = (ctypes.c_size_t * len(arrays))(*[int(a.shape[0]) for a in arrays])
+    rc = lib.qmsort_gpu_sort_host_batch(dt, _cmp_code(less), ptrs, ns, len(arrays), ctypes.byref(c),
+                                        ctypes.byref(m))
+    _lib.check(rc, "qmsort_gpu_sort_host_batch")
     return Metrics.from_c(m)
 
 

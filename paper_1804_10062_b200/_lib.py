@@ -90,6 +90,7 @@ EXPORTED = [
     "qmsort_gpu_select_workspace_bytes",
     "qmsort_gpu_select_nth",
     "qmsort_gpu_select_nth_host",
+    "qmsort_gpu_sort_host_batch",
 ]
 
 _lib = None
@@ -130,6 +131,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_select_workspace_bytes": (sz, [i, sz]),
         "qmsort_gpu_select_nth": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, vp, sz, mp, vp]),
         "qmsort_gpu_select_nth_host": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, mp]),
+        "qmsort_gpu_sort_host_batch": (i, [i, i, ctypes.POINTER(vp), ctypes.POINTER(sz), sz, cfgp, mp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

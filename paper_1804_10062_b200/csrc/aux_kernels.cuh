@@ -155,4 +155,16 @@ __global__ void check_kernel(const T* __restrict__ a, uint64_t n, unsigned long 
     }
 }
 
+// Small control reads (counters, a few keys) into mapped pinned host memory:
+// one warp stores the words over PCIe (posted writes), so these reads never
+// queue on a copy engine behind another stream's bulk transfer.
+struct SmallRead {
+    const unsigned char* src;
+    uint32_t bytes, dst_off;
+};
+__global__ void store_mapped_kernel(SmallRead r0, SmallRead r1, unsigned char* dst) {
+    for (uint32_t i = threadIdx.x; i < r0.bytes; i += blockDim.x) dst[r0.dst_off + i] = r0.src[i];
+    for (uint32_t i = threadIdx.x; i < r1.bytes; i += blockDim.x) dst[r1.dst_off + i] = r1.src[i];
+}
+
 }  // namespace qmsort_b200

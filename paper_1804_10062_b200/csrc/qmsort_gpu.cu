@@ -16,10 +16,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <future>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -185,6 +189,54 @@ static cudaError_t allow_smem(const void* fn, size_t bytes) {
 }
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Pool of small mapped pinned host buffers for control reads (read_small).
+constexpr uint32_t kMappedBytes = 8192;
+static std::mutex g_mapped_mu;
+static std::vector<unsigned char*> g_mapped_free;
+struct MappedBuf {
+    unsigned char* host = nullptr;
+    unsigned char* dev = nullptr;
+    ~MappedBuf() {
+        if (host) {
+            std::lock_guard<std::mutex> g(g_mapped_mu);
+            g_mapped_free.push_back(host);
+        }
+    }
+};
+
+// Copy up to two small device regions (<= kMappedBytes in total) to the host:
+// a store kernel on `st` writes them into mapped pinned memory, then the
+// stream is synchronised.  Unlike a device-to-host cudaMemcpyAsync this never
+// waits behind a bulk copy of another stream on the copy engine.
+static int read_small(cudaStream_t st, void* dst0, const void* src0, size_t b0,
+                      void* dst1 = nullptr, const void* src1 = nullptr, size_t b1 = 0) {
+    if (b0 + b1 > kMappedBytes) return fail(QMSORT_EINTERNAL, "read_small: too many bytes");
+    MappedBuf mb;
+    {
+        std::lock_guard<std::mutex> g(g_mapped_mu);
+        if (!g_mapped_free.empty()) {
+            mb.host = g_mapped_free.back();
+            g_mapped_free.pop_back();
+        }
+    }
+    if (!mb.host) {
+        void* h = nullptr;
+        QCK(cudaHostAlloc(&h, kMappedBytes, cudaHostAllocMapped));
+        mb.host = static_cast<unsigned char*>(h);
+    }
+    void* dptr = nullptr;
+    QCK(cudaHostGetDevicePointer(&dptr, mb.host, 0));
+    mb.dev = static_cast<unsigned char*>(dptr);
+    SmallRead r0{static_cast<const unsigned char*>(src0), (uint32_t)b0, 0};
+    SmallRead r1{static_cast<const unsigned char*>(src1), (uint32_t)b1, (uint32_t)align_up(b0, 16)};
+    store_mapped_kernel<<<1, 256, 0, st>>>(r0, r1, mb.dev);
+    QCK(cudaGetLastError());
+    QCK(cudaStreamSynchronize(st));
+    std::memcpy(dst0, mb.host, b0);
+    if (b1) std::memcpy(dst1, mb.host + r1.dst_off, b1);
+    return QMSORT_OK;
+}
 
 // Grid size of a persistent kernel: resident CTAs per SM x SMs (cached).
 static unsigned resident_grid(const void* fn, int threads, size_t smem) {
@@ -406,9 +458,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                     lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_scatter, src, dst,
                     tree[cur], sorted[cur], lut[cur], hist));
         LevelCounters hc[2];
-        QCK(cudaMemcpyAsync(&hc[0], lv[cur].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
-        QCK(cudaMemcpyAsync(&hc[1], lv[nxt].cnt, sizeof(LevelCounters), cudaMemcpyDeviceToHost, st));
-        QCK(cudaStreamSynchronize(st));
+        QTRY(read_small(st, &hc[0], lv[cur].cnt, sizeof(LevelCounters), &hc[1], lv[nxt].cnt,
+                        sizeof(LevelCounters)));
+        ++led.launches;
         ++led.syncs;
         if (hc[0].overflow || hc[1].overflow)
             return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
@@ -911,9 +963,8 @@ static int select_core(K* A, size_t n, size_t k0, const qmsort_gpu_config& cfg, 
         const size_t i1 = (size_t)std::max<int64_t>(0, r - (int64_t)kSelectBand);
         const size_t i2 = (size_t)std::min<int64_t>(kSelectSample - 1, r + (int64_t)kSelectBand);
         K h[2];
-        QCK(cudaMemcpyAsync(&h[0], smp + i1, sizeof(K), cudaMemcpyDeviceToHost, st));
-        QCK(cudaMemcpyAsync(&h[1], smp + i2, sizeof(K), cudaMemcpyDeviceToHost, st));
-        QCK(cudaStreamSynchronize(st));
+        QTRY(read_small(st, &h[0], smp + i1, sizeof(K), &h[1], smp + i2, sizeof(K)));
+        ++led.launches;
         ++led.syncs;
         K sp[3];
         uint32_t ns = 0;
@@ -994,8 +1045,14 @@ struct HostArena {
         if (st) cudaStreamDestroy(st);
     }
 };
-static int host_arena(size_t need, unsigned char** base, cudaStream_t* st) {
-    static thread_local HostArena ar;
+// The batch entry point's two workers use two process-wide arenas instead
+// (slot 0 / 1, one batch at a time), so worker threads can be short-lived
+// without allocating and freeing device memory on every call.
+static std::mutex g_batch_mu;
+static int host_arena(size_t need, unsigned char** base, cudaStream_t* st, int slot = -1) {
+    static thread_local HostArena tl;
+    static HostArena batch[2];
+    HostArena& ar = slot < 0 ? tl : batch[slot];
     if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
     if (ar.bytes < need) {
         if (ar.buf) QCK(cudaFree(ar.buf));
@@ -1006,6 +1063,33 @@ static int host_arena(size_t need, unsigned char** base, cudaStream_t* st) {
     }
     *base = static_cast<unsigned char*>(ar.buf);
     *st = ar.st;
+    return QMSORT_OK;
+}
+
+// Host-array sort through the calling thread's arena: H2D, sort, D2H.
+// after_h2d (optional) runs once the input has landed on the device.
+static int sort_host_one(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
+                         qmsort_gpu_metrics* metrics, const std::function<void()>* after_h2d,
+                         int slot = -1) {
+    QTRY(validate(dtype, cmp, n, h_data));
+    if (n <= 1) {
+        if (metrics) std::memset(metrics, 0, sizeof(*metrics));
+        return QMSORT_OK;
+    }
+    const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
+    const size_t need = data_bytes + ws_bytes_for(dtype, n);
+    unsigned char* base = nullptr;
+    cudaStream_t st = nullptr;
+    QTRY(host_arena(need, &base, &st, slot));
+    QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, st));
+    if (after_h2d) {
+        QCK(cudaStreamSynchronize(st));
+        (*after_h2d)();
+    }
+    int rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, need - data_bytes, metrics, st);
+    if (rc != QMSORT_OK) return rc;
+    QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
     return QMSORT_OK;
 }
 
@@ -1069,21 +1153,67 @@ int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu
 
 int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
                          qmsort_gpu_metrics* metrics) {
-    QTRY(validate(dtype, cmp, n, h_data));
-    if (n <= 1) {
-        if (metrics) std::memset(metrics, 0, sizeof(*metrics));
-        return QMSORT_OK;
+    return sort_host_one(dtype, cmp, h_data, n, cfg, metrics, nullptr);
+}
+
+int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const size_t* ns,
+                               size_t count, const qmsort_gpu_config* cfg,
+                               qmsort_gpu_metrics* metrics) {
+    if (count > 0 && (h_arrays == nullptr || ns == nullptr))
+        return fail(QMSORT_EINVAL, "null array list");
+    for (size_t i = 0; i < count; ++i) QTRY(validate(dtype, cmp, ns[i], h_arrays[i]));
+    if (metrics) std::memset(metrics, 0, sizeof(*metrics));
+    if (count == 0) return QMSORT_OK;
+    std::lock_guard<std::mutex> batch_lock(g_batch_mu);
+    // Two workers (own stream + device arena each) take alternate arrays; the
+    // second starts once the first array's H2D is done, so from then on one
+    // array's D2H runs while the next array's H2D runs (one copy engine each
+    // way) and the sorts fill the gaps.
+    std::promise<void> first_in;
+    std::shared_future<void> first_in_done = first_in.get_future().share();
+    std::atomic<bool> signalled{false};
+    const std::function<void()> signal = [&]() {
+        if (!signalled.exchange(true)) first_in.set_value();
+    };
+    int rcs[2] = {QMSORT_OK, QMSORT_OK};
+    std::string errs[2];
+    qmsort_gpu_metrics ms[2];
+    std::memset(ms, 0, sizeof(ms));
+    auto worker = [&](int w) {
+        if (w == 1) first_in_done.wait();
+        for (size_t i = (size_t)w; i < count; i += 2) {
+            qmsort_gpu_metrics m;
+            const int rc = sort_host_one(dtype, cmp, h_arrays[i], ns[i], cfg, &m,
+                                         (w == 0 && i == 0) ? &signal : nullptr, w);
+            if (w == 0 && i == 0) signal();  // also on failure or n <= 1
+            if (rc != QMSORT_OK) {
+                rcs[w] = rc;
+                errs[w] = g_err;
+                break;
+            }
+            ms[w].elapsed_ns += m.elapsed_ns;
+            ms[w].alg_bytes += m.alg_bytes;
+            ms[w].kernel_launches += m.kernel_launches;
+            ms[w].host_syncs += m.host_syncs;
+            ms[w].max_depth = std::max(ms[w].max_depth, m.max_depth);
+            ms[w].levels = std::max(ms[w].levels, m.levels);
+        }
+        if (w == 0) signal();
+    };
+    std::thread t1(worker, 1);
+    worker(0);
+    t1.join();
+    for (int w = 0; w < 2; ++w)
+        if (rcs[w] != QMSORT_OK) return fail(rcs[w], errs[w]);
+    if (metrics) {
+        metrics->elapsed_ns = ms[0].elapsed_ns + ms[1].elapsed_ns;
+        metrics->alg_bytes = ms[0].alg_bytes + ms[1].alg_bytes;
+        metrics->kernel_launches = ms[0].kernel_launches + ms[1].kernel_launches;
+        metrics->host_syncs = ms[0].host_syncs + ms[1].host_syncs;
+        metrics->max_depth = std::max(ms[0].max_depth, ms[1].max_depth);
+        metrics->levels = std::max(ms[0].levels, ms[1].levels);
     }
-    const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
-    const size_t need = data_bytes + ws_bytes_for(dtype, n);
-    unsigned char* base = nullptr;
-    cudaStream_t st = nullptr;
-    QTRY(host_arena(need, &base, &st));
-    QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, st));
-    int rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, need - data_bytes, metrics, st);
-    if (rc != QMSORT_OK) return rc;
-    QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, st));
-    QCK(cudaStreamSynchronize(st));
+    g_err.clear();
     return QMSORT_OK;
 }
 

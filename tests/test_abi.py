@@ -94,6 +94,8 @@ def test_invalid_arguments_are_rejected_before_any_cuda_call():
         assert lib.qmsort_gpu_select_nth_host(1, 0, ctypes.addressof(buf), 4, k, ctypes.byref(sz), None, None) == _lib.QMSORT_EINVAL
         assert lib.qmsort_gpu_select_nth(1, 0, ctypes.addressof(buf), 4, k, ctypes.byref(sz), None, None, 0, None, None) == _lib.QMSORT_EINVAL
     assert b"1-based" in lib.qmsort_gpu_last_error()
+    assert lib.qmsort_gpu_sort_host_batch(1, 0, None, None, 2, None, None) == _lib.QMSORT_EINVAL
+    assert lib.qmsort_gpu_sort_host_batch(1, 0, None, None, 0, None, None) == _lib.QMSORT_OK
     with pytest.raises(ValueError):
         q.sort(np.zeros(4, np.int16))
     with pytest.raises(ValueError):

@@ -167,3 +167,22 @@ def test_device_generators_match_host(oracle, kind, dt, cfgname):
     t = torch.empty(shape, dtype=tdt, device="cuda")
     q.generate(kind, t, seed=7, start=0, total=n)
     np.testing.assert_array_equal(t.cpu().numpy(), oracle.gen(cfgname, n, seed=7))
+
+
+@pytest.mark.parametrize("dt", [DT_U32, DT_I64, DT_F64, DT_REC32])
+def test_host_batch_pipeline(oracle, dt):
+    """qmsort_gpu_sort_host_batch: a stream of independent host arrays (sizes
+    0 .. 2^21, pinned and pageable) -- each equals the oracle's sort."""
+    sizes = [0, 1, 5000, 1 << 21, 777, 1 << 20, 3]
+    arrays = [rand_input(dt, n, seed=n + 7) for n in sizes]
+    want = [oracle.sort(dt, a) for a in arrays]
+    work = [a.copy() for a in arrays]
+    m = q.sort_batch(work)
+    for g, w in zip(work, want):
+        np.testing.assert_array_equal(g, w)
+    assert m.kernel_launches > 0 and m.elapsed_ns > 0
+    # pinned torch buffers, descending
+    pins = [torch.from_numpy(a.copy()).pin_memory() for a in arrays[2:5]]
+    q.sort_batch(pins, less="greater")
+    for p, a in zip(pins, arrays[2:5]):
+        np.testing.assert_array_equal(p.numpy(), oracle.sort(dt, a, greater=True))
