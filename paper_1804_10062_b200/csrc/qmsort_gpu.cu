@@ -79,8 +79,8 @@ template <>
 struct Tune<uint32_t> {
     static constexpr int LOGKMAX = 9;
     static constexpr int BI = 32;                                 // block sort keys / thread
-    static constexpr int CLS_T[kNumClasses] = {32, 64, 128, 256};  // block sort classes
-    static constexpr int TARGET_DIV = 2;                          // target bucket = cap / 2
+    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};  // block sort classes
+    static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     static constexpr int ST = 512, SI = 16;  // sampler
     static constexpr int XT = 256, XI = 16;  // scatter tile
     static constexpr int CT = 256, CU = 16;  // count

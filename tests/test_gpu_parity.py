@@ -71,7 +71,7 @@ def gpu_sort(a, cfg=None, less="less"):
 
 
 SIZES = [0, 1, 2, 3, 9, 10, 100, 511, 512, 513, 1000, 1024, 2047, 4096, 4097, 8191, 8192,
-         8193, 20000, 65536, 100003, 1 << 20]
+         8193, 16383, 16384, 16385, 20000, 65536, 100003, 1 << 20]
 
 
 @pytest.mark.parametrize("dt", DTYPES)
@@ -83,7 +83,7 @@ def test_uniform_sizes_samplesort(oracle, dt, n):
 
 
 @pytest.mark.parametrize("dt", DTYPES)
-@pytest.mark.parametrize("n", [8193, 100003, 1 << 19])
+@pytest.mark.parametrize("n", [40001, 100003, 1 << 19])  # above every block-sort cap
 def test_uniform_sizes_mergesort(oracle, dt, n):
     a = rand_input(dt, n, seed=n + 3 * dt)
     cfg = q.qms()
