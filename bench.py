@@ -35,6 +35,18 @@ UNIT = "Gkeys/s"
 N_DEFAULT = 1 << 28
 SEED = 42
 CPU_SAMPLE = 1 << 24  # bounded CPU sample (~3 s per qms() sort on one core)
+# BASELINE.json configs runnable with device generators: (dtype attr, torch dtype,
+# row shape, generator attr, n, key bytes, description)
+CONFIGS = {
+    "c2": ("DT_U32", "uint32", (), "GEN_U32", 1 << 28, 4, "C2: sort n=2^28 uint32 i.i.d. uniform"),
+    "c3": ("DT_U64", "uint64", (), "GEN_U64", 1 << 30, 8, "C3: sort n=2^30 uint64 i.i.d. uniform"),
+    "c4a": ("DT_F64", "float64", (), "GEN_F64_SORTED", 1 << 27, 8, "C4a: 2^27 float64 sorted"),
+    "c4b": ("DT_F64", "float64", (), "GEN_F64_REVERSE", 1 << 27, 8, "C4b: 2^27 float64 reverse"),
+    "c4c": ("DT_F64", "float64", (), "GEN_F64_DISTINCT16", 1 << 27, 8, "C4c: 2^27 float64 16 distinct"),
+    "c4d": ("DT_F64", "float64", (), "GEN_F64_GAUSS", 1 << 27, 8, "C4d: 2^27 float64 gaussian"),
+    "c4e": ("DT_F64", "float64", (), "GEN_F64_ORGAN", 1 << 27, 8, "C4e: 2^27 float64 organ-pipe"),
+    "c5": ("DT_REC32", "uint64", (4,), "GEN_REC32", 1 << 26, 32, "C5: 2^26 32-byte records"),
+}
 
 
 def parse():
@@ -48,6 +60,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: skip extras")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",
+                    help="BASELINE config (c2 is the headline; the others are informational)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the distributed samplesort path even on one GPU (exercises NCCL)")
     return ap.parse_args()
@@ -205,15 +219,19 @@ def run_ours(args) -> None:
         sharded.bench_main(args, METRIC, UNIT)
         return
 
-    n = args.n
+    dt_name, tdt, rowshape, gen_name, n_cfg, kb, desc = CONFIGS[args.config]
+    dt = getattr(q, dt_name)
+    n = args.n if args.config == "c2" else (n_cfg if args.n == N_DEFAULT else args.n)
+    if args.config != "c2":  # informational configs: device numbers only
+        args.no_e2e = args.no_cpu_baseline = True
     dev = torch.device("cuda", local)
-    pristine = torch.empty(n, dtype=torch.uint32, device=dev)
-    q.generate(q.GEN_U32, pristine, seed=SEED)
+    pristine = torch.empty((n,) + rowshape, dtype=getattr(torch, tdt), device=dev)
+    q.generate(getattr(q, gen_name), pristine, seed=SEED)
     x = torch.empty_like(pristine)
     cfg = q.qms()
     if args.algorithm == "mergesort":
         cfg.algorithm = q.Algorithm.mergesort
-    ws = torch.empty(q.workspace_bytes(q.DT_U32, n, cfg), dtype=torch.uint8, device=dev)
+    ws = torch.empty(q.workspace_bytes(dt, n, cfg), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -278,20 +296,22 @@ def run_ours(args) -> None:
                 "peak_source": peak_src}
     sort_roofline = {"alg_bytes": sort_bytes, "achieved": sort_gbs, "peak": peak, "unit": "GB/s",
                      "frac": sort_gbs / peak,
-                     "floor_frac": 4 * n * 4 / (ms * 1e6) / peak,
-                     "ledger_bytes_over_nw": sort_bytes / (n * 4),
+                     "floor_frac": 4 * n * kb / (ms * 1e6) / peak,
+                     "ledger_bytes_over_nw": sort_bytes / (n * kb),
                      "levels": metrics.levels,
                      "phases": {k: {"launches": v[0], "alg_bytes": v[1], "us": v[2] / 1e3,
                                     "GBps": (v[1] / v[2]) if v[2] else None}
                                 for k, v in phases.items()}}
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+    metric = METRIC if args.config == "c2" else f"sorted Gkeys/s, {desc} (informational)"
+    line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe, seed 42)",
-            "config": {"workload": "C2: sort n=2^28 uint32 i.i.d. uniform, qms() preset, 1 B200",
-                       "n": n, "key_bytes": 4, "algorithm": args.algorithm,
-                       "l2": "flushed (256 MiB write) before every timed step; input 1 GiB > L2",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": {"DT_U32": "u32", "DT_U64": "u64", "DT_F64": "f64", "DT_REC32": "4xu64"}[dt_name],
+            "data": f"synthetic (seeded SplitMix64, SURVEY.md 8(d) {args.config.upper()} recipe, seed 42)",
+            "config": {"workload": f"{desc}, qms() preset, 1 B200",
+                       "n": n, "key_bytes": kb, "algorithm": args.algorithm,
+                       "l2": "flushed (256 MiB write) before every timed step; input > L2",
                        "parallelism": "single GPU"},
             "gpu_launches": launches, "clocks": clk, "roofline": roofline,
             "sort_roofline": sort_roofline}

@@ -385,6 +385,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     p.pivot = (uint32_t)std::max(0, cfg.pivot);
     const double dl = std::min(1.0, std::max(1.0 / 65536.0, cfg.delta > 0 ? cfg.delta : 1.0 / 16.0));
     p.delta_q16 = (uint32_t)(dl * 65536.0);
+    p.slack = (p.cap / p.target >= 4) ? 1u : 0u;
 
     LevelBufs lv[2];
     K* tree[2];

@@ -122,6 +122,7 @@ struct PlanParams {
     int dst_is_a;           // this level's scatter writes the caller's buffer
     uint32_t pivot;         // PivotStrategy (sort.hpp:19): 2 mom_of_thirds, 3 hybrid
     uint32_t delta_q16;     // SortConfig::delta in 1/65536 (hybrid skew band)
+    uint32_t slack;         // 1 if the last level may leave buckets of 2x target
 };
 
 __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
@@ -132,11 +133,16 @@ __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
 
 // Number of buckets for a segment of len keys: spread the remaining
 // log2(len/target) bits evenly over the fewest levels of at most 2^log_kmax.
-__host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, uint32_t log_kmax) {
+// When the block sorter's cap is 4x the target or more, the last level may
+// leave buckets of up to twice the target (one "slack" bit), which saves a
+// whole partition level for segments just above K_max * target.
+__host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, uint32_t log_kmax,
+                                                uint32_t slack = 0) {
     const uint64_t ratio = (len + target - 1) / target;
     uint32_t r = ceil_log2_u64(ratio);
     if (r < 1) r = 1;
-    const uint32_t levels = (r + log_kmax - 1) / log_kmax;
+    const uint32_t rs = r > slack ? r - slack : 1;
+    const uint32_t levels = (rs + log_kmax - 1) / log_kmax;
     uint32_t k = (r + levels - 1) / levels;
     if (k < 1) k = 1;
     if (k > log_kmax) k = log_kmax;
@@ -148,7 +154,7 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
 __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len, uint64_t lo,
                                     uint64_t hi, const PlanParams& p, uint32_t sampler,
                                     bool write_chunks = true) {
-    const uint32_t logk = choose_logk(len, p.target, p.log_kmax);
+    const uint32_t logk = choose_logk(len, p.target, p.log_kmax, p.slack);
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
     const uint32_t hwords = (nch + 1) * (2u << logk);
     const uint32_t s = atomicAdd(&nb.cnt->nsegs, 1u);
