@@ -44,7 +44,8 @@ def test_momqms_triple_median_sampling(oracle, dt, dist):
 
 @pytest.mark.parametrize("dt", [DT_U32, DT_U64, DT_REC32])
 def test_hybrid_resplits_buckets_outside_the_band(oracle, dt):
-    a = rand_input(dt, 1 << 22, seed=5)  # two partition levels: children exist
+    n = (1 << 24) if dt == DT_U32 else (1 << 22)  # two partition levels: children exist
+    a = rand_input(dt, n, seed=5)
     got, m = gpu_sort(a, q.hqms())
     np.testing.assert_array_equal(got, oracle.sort(dt, a))
     assert m.resplits == 0  # delta = 1/16: random samples never leave the band
@@ -74,7 +75,8 @@ def test_every_pivot_strategy(oracle, pivot, dt):
 @pytest.mark.parametrize("max_levels", [1, 2])
 def test_merge_fallback_after_max_levels(oracle, dt, max_levels):
     """K8: buckets still too large after max_levels are merge-sorted."""
-    a = rand_input(dt, 3 << 20, seed=max_levels)
+    n = (12 << 20) if dt == DT_U32 else (3 << 20)  # needs two partition levels
+    a = rand_input(dt, n, seed=max_levels)
     cfg = q.qms()
     cfg.max_levels = max_levels
     got, m = gpu_sort(a, cfg)
