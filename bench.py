@@ -64,6 +64,9 @@ def parse():
                     help="BASELINE config (c2 is the headline; the others are informational)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the distributed samplesort path even on one GPU (exercises NCCL)")
+    ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
+                    help="sharded path: exchange fused into the scatter (CUDA IPC peer stores) "
+                         "or a NCCL all-to-all after the partition")
     return ap.parse_args()
 
 

@@ -189,6 +189,30 @@ int qmsort_gpu_partition(int core_dtype, const void* d_in, size_t n, const void*
                          uint32_t nsplit, void* d_out, uint64_t* d_counts, void* d_ws,
                          size_t ws_bytes, void* stream);
 
+/* The same partition split in two so that the exchange is fused into the
+ * scatter: partition_count classifies and counts (bucket
+ * sizes into d_counts) and keeps its plan in d_ws; partition_scatter_peers
+ * then writes bucket b's keys, in bucket order, straight to
+ * dests[b] + dest_offsets[b] elements -- rank b's receive buffer, a peer GPU's
+ * memory mapped with qmsort_gpu_ipc_open (NVLink), or this GPU's own -- with
+ * no staging copy and no collective on the data.  nsplit + 1 <= 8.  Both
+ * calls take the same d_in, n and caller workspace. */
+int qmsort_gpu_partition_count(int core_dtype, const void* d_in, size_t n, const void* d_splitters,
+                               uint32_t nsplit, uint64_t* d_counts, void* d_ws, size_t ws_bytes,
+                               void* stream);
+int qmsort_gpu_partition_scatter_peers(int core_dtype, const void* d_in, size_t n, uint32_t nsplit,
+                                       void* const* dests, const uint64_t* dest_offsets,
+                                       void* d_ws, size_t ws_bytes, void* stream);
+
+/* CUDA IPC for the receive buffers of the fused exchange (one process per
+ * GPU): export the allocation holding d_ptr (handle + d_ptr's byte offset in
+ * it), open a peer's (d_ptr for the kernels, d_base for the close; peer access
+ * over NVLink enabled lazily), close it. */
+#define QMSORT_IPC_HANDLE_BYTES 64
+int qmsort_gpu_ipc_handle(void* d_ptr, void* handle_out, uint64_t* offset_out);
+int qmsort_gpu_ipc_open(const void* handle, uint64_t offset, void** d_ptr, void** d_base);
+int qmsort_gpu_ipc_close(void* d_base);
+
 /* ---- harness (K9 generators, verification) ----------------------------- */
 /* kind: 0 u32 uniform, 1 u64 uniform, 2 rec32, 10..14 f64 sorted / reverse /
  * 16-distinct / gaussian / organ-pipe.  Element i is global element start+i

@@ -91,6 +91,11 @@ EXPORTED = [
     "qmsort_gpu_select_nth",
     "qmsort_gpu_select_nth_host",
     "qmsort_gpu_sort_host_batch",
+    "qmsort_gpu_partition_count",
+    "qmsort_gpu_partition_scatter_peers",
+    "qmsort_gpu_ipc_handle",
+    "qmsort_gpu_ipc_open",
+    "qmsort_gpu_ipc_close",
 ]
 
 _lib = None
@@ -132,6 +137,12 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_select_nth": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, vp, sz, mp, vp]),
         "qmsort_gpu_select_nth_host": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, mp]),
         "qmsort_gpu_sort_host_batch": (i, [i, i, ctypes.POINTER(vp), ctypes.POINTER(sz), sz, cfgp, mp]),
+        "qmsort_gpu_partition_count": (i, [i, vp, sz, vp, ctypes.c_uint32, vp, vp, sz, vp]),
+        "qmsort_gpu_partition_scatter_peers": (i, [i, vp, sz, ctypes.c_uint32, ctypes.POINTER(vp),
+                                                   ctypes.POINTER(u64), vp, sz, vp]),
+        "qmsort_gpu_ipc_handle": (i, [vp, vp, ctypes.POINTER(u64)]),
+        "qmsort_gpu_ipc_open": (i, [vp, u64, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
+        "qmsort_gpu_ipc_close": (i, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -13,6 +13,7 @@
 // used ping-pong.  Every scatter writes each bucket at its FINAL offset, so the
 // two buffers share one coordinate system and the sorted result always ends
 // in A.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -457,7 +458,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         QLAUNCH(led, kPhScatter, 2 * level_keys * sizeof(K),
                 scatter_fn<<<std::min(nchunks, scatter_grid), TU::XT, sizeof(SM), st>>>(
                     lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_scatter, src, dst,
-                    tree[cur], sorted[cur], lut[cur], hist));
+                    tree[cur], sorted[cur], lut[cur], hist, PeerArgs{}));
         LevelCounters hc[2];
         QTRY(read_small(st, &hc[0], lv[cur].cnt, sizeof(LevelCounters), &hc[1], lv[nxt].cnt,
                         sizeof(LevelCounters)));
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(T) given_plan_kernel(const SegDesc* __restrict
 template <class K>
 static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit, K* out,
                            uint64_t* counts, unsigned char* ws, const WsLayout& L, cudaStream_t st,
-                           Ledger& led) {
+                           Ledger& led, int parts = 3, const PeerArgs* peers = nullptr) {
     using TU = Tune<K>;
     const uint32_t logk = std::max<uint32_t>(1, ceil_log2_u64((uint64_t)nsplit + 1));
     if (logk > (uint32_t)TU::LOGKMAX) return fail(QMSORT_EINVAL, "too many splitters");
@@ -758,26 +759,38 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.hist_off);
     const uint64_t key_max = ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K)));
     const uint32_t nchunks = (uint32_t)std::max<uint64_t>(1, (n + L.chunk_elems - 1) / L.chunk_elems);
-    QLAUNCH(led, kPhSample, 0,
-            given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, lut,
-                                                         n, nchunks, chunks, L.chunk_elems, key_max));
-    QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
-    if (n == 0) return QMSORT_OK;
     LevelCounters* cnt = reinterpret_cast<LevelCounters*>(ws + L.cnt_off[0]);
-    QCK(cudaMemsetAsync(cnt, 0, sizeof(LevelCounters), st));
-    auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
-    QLAUNCH(led, kPhCount, n * sizeof(K),
-            count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
-                       st>>>(seg, chunks, nchunks, &cnt->work_count, in, tree, sorted, lut, hist));
-    QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(1, 64), 512, 0, st>>>(seg, hist));
-    QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
+    if (parts & 1) {  // classify + count + plan (bucket sizes into counts)
+        QLAUNCH(led, kPhSample, 0,
+                given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, lut,
+                                                             n, nchunks, chunks, L.chunk_elems, key_max));
+        QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
+        if (n == 0) return QMSORT_OK;
+        QCK(cudaMemsetAsync(cnt, 0, sizeof(LevelCounters), st));
+        auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
+        QLAUNCH(led, kPhCount, n * sizeof(K),
+                count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
+                           st>>>(seg, chunks, nchunks, &cnt->work_count, in, tree, sorted, lut, hist));
+        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(1, 64), 512, 0, st>>>(seg, hist));
+        QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
+    }
+    if (!(parts & 2) || n == 0) return QMSORT_OK;
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
+    if (peers) {  // the exchange fused into the scatter: bucket b -> rank b's buffer
+        auto fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX, true>;
+        QCK(allow_smem((const void*)fn, sizeof(SM)));
+        QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
+                fn<<<std::min(nchunks, resident_grid((const void*)fn, TU::XT, sizeof(SM))), TU::XT,
+                     sizeof(SM), st>>>(seg, chunks, nchunks, &cnt->work_scatter, in, out, tree, sorted,
+                                       lut, hist, *peers));
+        return QMSORT_OK;
+    }
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
     QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
             scatter_fn<<<std::min(nchunks, resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM))),
                          TU::XT, sizeof(SM), st>>>(seg, chunks, nchunks, &cnt->work_scatter, in, out,
-                                                   tree, sorted, lut, hist));
+                                                   tree, sorted, lut, hist, PeerArgs{}));
     return QMSORT_OK;
 }
 
@@ -1308,8 +1321,9 @@ size_t qmsort_gpu_partition_workspace_bytes(int core, size_t n) {
     return ws_bytes_for(core, n);
 }
 
-int qmsort_gpu_partition(int core, const void* d_in, size_t n, const void* spl, uint32_t nsplit,
-                         void* d_out, uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream) {
+static int partition_entry(int core, const void* d_in, size_t n, const void* spl, uint32_t nsplit,
+                           void* d_out, uint64_t* d_counts, void* d_ws, size_t ws_bytes,
+                           void* stream, int parts, const PeerArgs* peers) {
     QTRY(validate(core, 0, n, d_in));
     if (core != core_dtype(core)) return fail(QMSORT_EINVAL, "partition expects a core dtype");
     if (nsplit > 1023) return fail(QMSORT_EINVAL, "nsplit must be <= 1023");
@@ -1318,6 +1332,7 @@ int qmsort_gpu_partition(int core, const void* d_in, size_t n, const void* spl, 
     void* ws = d_ws;
     bool own = false;
     if (!ws) {
+        if (parts != 3) return fail(QMSORT_EINVAL, "split partition calls need a caller workspace");
         QCK(cudaMallocAsync(&ws, need, st));
         own = true;
     } else if (ws_bytes < need) {
@@ -1330,21 +1345,94 @@ int qmsort_gpu_partition(int core, const void* d_in, size_t n, const void* spl, 
     switch (core) {
         case QMSORT_DT_U32:
             rc = partition_given<uint32_t>((const uint32_t*)d_in, n, (const uint32_t*)spl, nsplit,
-                                           (uint32_t*)d_out, d_counts, w, make_layout<uint32_t>(nn), st, led);
+                                           (uint32_t*)d_out, d_counts, w, make_layout<uint32_t>(nn), st,
+                                           led, parts, peers);
             break;
         case QMSORT_DT_U64:
             rc = partition_given<uint64_t>((const uint64_t*)d_in, n, (const uint64_t*)spl, nsplit,
-                                           (uint64_t*)d_out, d_counts, w, make_layout<uint64_t>(nn), st, led);
+                                           (uint64_t*)d_out, d_counts, w, make_layout<uint64_t>(nn), st,
+                                           led, parts, peers);
             break;
         case QMSORT_DT_REC32:
             if (nsplit > 255) rc = fail(QMSORT_EINVAL, "rec32 partition supports <= 255 splitters");
             else
                 rc = partition_given<Rec32>((const Rec32*)d_in, n, (const Rec32*)spl, nsplit,
-                                            (Rec32*)d_out, d_counts, w, make_layout<Rec32>(nn), st, led);
+                                            (Rec32*)d_out, d_counts, w, make_layout<Rec32>(nn), st,
+                                            led, parts, peers);
             break;
     }
     if (own) cudaFreeAsync(ws, st);
     return rc;
+}
+
+int qmsort_gpu_partition(int core, const void* d_in, size_t n, const void* spl, uint32_t nsplit,
+                         void* d_out, uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream) {
+    return partition_entry(core, d_in, n, spl, nsplit, d_out, d_counts, d_ws, ws_bytes, stream, 3,
+                           nullptr);
+}
+
+int qmsort_gpu_partition_count(int core, const void* d_in, size_t n, const void* d_splitters,
+                               uint32_t nsplit, uint64_t* d_counts, void* d_ws, size_t ws_bytes,
+                               void* stream) {
+    return partition_entry(core, d_in, n, d_splitters, nsplit, nullptr, d_counts, d_ws, ws_bytes,
+                           stream, 1, nullptr);
+}
+
+int qmsort_gpu_partition_scatter_peers(int core, const void* d_in, size_t n, uint32_t nsplit,
+                                       void* const* dests, const uint64_t* dest_offsets,
+                                       void* d_ws, size_t ws_bytes, void* stream) {
+    if (nsplit + 1 > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "at most 8 destination ranks");
+    if (n > 0 && (dests == nullptr || dest_offsets == nullptr))
+        return fail(QMSORT_EINVAL, "null destination list");
+    PeerArgs pa{};
+    pa.nb = nsplit + 1;
+    for (uint32_t b = 0; b < pa.nb; ++b) {
+        pa.dest[b] = reinterpret_cast<unsigned long long>(dests[b]);
+        pa.off[b] = dest_offsets[b];
+    }
+    return partition_entry(core, d_in, n, nullptr, nsplit, nullptr, nullptr, d_ws, ws_bytes, stream,
+                           2, &pa);
+}
+
+// A handle names the whole allocation (e.g. a block of a caching allocator);
+// the offset of d_ptr inside it travels with the handle.
+int qmsort_gpu_ipc_handle(void* d_ptr, void* handle_out, uint64_t* offset_out) {
+    if (!d_ptr || !handle_out || !offset_out) return fail(QMSORT_EINVAL, "null pointer");
+    // the driver entry point through cudart: no link-time dependency on libcuda
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range_fn = nullptr;
+    if (!range_fn) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        QCK(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(QMSORT_ECUDA, "cuMemGetAddressRange unavailable");
+        range_fn = reinterpret_cast<RangeFn>(fn);
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+        return fail(QMSORT_ECUDA, "cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    QCK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) == QMSORT_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+    return QMSORT_OK;
+}
+
+int qmsort_gpu_ipc_open(const void* handle, uint64_t offset, void** d_ptr, void** d_base) {
+    if (!handle || !d_ptr || !d_base) return fail(QMSORT_EINVAL, "null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    QCK(cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess));
+    *d_ptr = static_cast<unsigned char*>(*d_base) + offset;
+    return QMSORT_OK;
+}
+
+int qmsort_gpu_ipc_close(void* d_base) {
+    if (!d_base) return fail(QMSORT_EINVAL, "null pointer");
+    QCK(cudaIpcCloseMemHandle(d_base));
+    return QMSORT_OK;
 }
 
 int qmsort_gpu_generate(int kind, void* d_out, size_t n, uint64_t seed, uint64_t start,

@@ -686,10 +686,38 @@ __device__ __forceinline__ void vec_store(uint32_t* p, const uint32_t (&v)[N]) {
 // thread owns BPT consecutive bins and keeps their write cursors in
 // registers), group by bucket in shared memory, then write every bucket run
 // with coalesced stores.
-template <class K, int T, int U, int LOG_KMAX, bool FULL>
+// Where a scatter writes: the segment's range of the destination buffer
+// (every level of the sort), or -- the sharded exchange fused into the
+// partition -- bucket b's keys straight into rank b's receive buffer, a peer
+// GPU's memory mapped through CUDA IPC, at that rank's offset for this sender.
+constexpr int kMaxPeers = 8;
+struct PeerArgs {
+    unsigned long long dest[kMaxPeers];  // receive buffer of rank b (device pointer)
+    unsigned long long off[kMaxPeers];   // element offset of this sender's part in it
+    uint32_t nb;                         // number of ranks (buckets)
+};
+template <class K>
+struct LocalSink {
+    K* out;
+    __device__ __forceinline__ void store(uint32_t dest, const K& key) const { out[dest] = key; }
+};
+template <class K>
+struct PeerSink {
+    const unsigned long long* base;  // shared memory: dest[b] + (off[b] - start[b]) * sizeof(K)
+    const uint32_t* start;           // shared memory: bucket starts in the local grouping
+    uint32_t nb;
+    __device__ __forceinline__ void store(uint32_t dest, const K& key) const {
+        uint32_t b = 0;
+#pragma unroll
+        for (int j = 1; j < kMaxPeers; ++j) b += (j < (int)nb && dest >= start[j]) ? 1u : 0u;
+        *reinterpret_cast<K*>(base[b] + (unsigned long long)dest * sizeof(K)) = key;
+    }
+};
+
+template <class K, int T, int U, int LOG_KMAX, bool FULL, class Sink>
 __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm, const SegDesc& d,
                                              const K* __restrict__ p, uint32_t m,
-                                             K* __restrict__ out,
+                                             const Sink& out,
                                              uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT]) {
     using SM = ScatterSmem<K, T, U, LOG_KMAX>;
     constexpr int BPT = SM::BPT;
@@ -756,13 +784,13 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         const uint32_t i = u * T + tid;
         if (FULL || i < m) {
             const typename SM::Rec r = stage[i];
-            out[r.dest] = r.key;
+            out.store(r.dest, r.key);
         }
     }
     __syncthreads();
 }
 
-template <class K, int T, int U, int LOG_KMAX>
+template <class K, int T, int U, int LOG_KMAX, bool PEER = false>
 __global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict__ segs,
                                                     const ChunkDesc* __restrict__ chunks,
                                                     uint32_t nchunks, uint32_t* __restrict__ work,
@@ -770,13 +798,23 @@ __global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict
                                                     const K* __restrict__ tree_store,
                                                     const K* __restrict__ sorted_store,
                                                     const uint32_t* __restrict__ lut_store,
-                                                    const uint32_t* __restrict__ hist) {
+                                                    const uint32_t* __restrict__ hist,
+                                                    PeerArgs peers = PeerArgs{}) {
     using SM = ScatterSmem<K, T, U, LOG_KMAX>;
     constexpr uint32_t TILE = SM::TILE;
     constexpr int BPT = SM::BPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
     __shared__ uint32_t next_chunk;
+    __shared__ unsigned long long peer_base[kMaxPeers];
+    __shared__ uint32_t peer_start[kMaxPeers];
+    if (PEER && threadIdx.x < kMaxPeers) {  // single segment: bucket starts from the plan
+        const SegDesc d0 = segs[0];
+        const uint32_t b = threadIdx.x;
+        const uint32_t st = b < peers.nb ? hist[d0.hist_base + b * (d0.nchunks + 1) + d0.nchunks] : 0u;
+        peer_start[b] = st;
+        peer_base[b] = b < peers.nb ? peers.dest[b] + (peers.off[b] - st) * sizeof(K) : 0ull;
+    }
     uint32_t cur_seg = 0xFFFFFFFFu;
     // persistent CTAs fetch chunks dynamically (no tail of idle SMs)
     for (;;) {
@@ -807,12 +845,19 @@ __global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict
         __syncthreads();
 
         const K* p = src + c.begin;
-        K* out = dst + d.off;
         const uint32_t len = (uint32_t)(c.end - c.begin);
         uint32_t t0 = 0;
-        for (; t0 + TILE <= len; t0 += TILE)
-            scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
-        if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+        if constexpr (PEER) {
+            const PeerSink<K> out{peer_base, peer_start, peers.nb};
+            for (; t0 + TILE <= len; t0 += TILE)
+                scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
+            if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+        } else {
+            const LocalSink<K> out{dst + d.off};
+            for (; t0 + TILE <= len; t0 += TILE)
+                scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
+            if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+        }
     }
 }
 

@@ -95,6 +95,35 @@ class GpuOps:
             _lib.check(rc, "qmsort_gpu_partition")
         return out, counts
 
+    # -- the exchange fused into the partition's scatter ------------------
+    def partition_count(self, t, core: int, splitters):
+        """Classify + count against the splitters; the plan stays in the workspace
+        for scatter_peers.  Returns the bucket sizes (int64 device tensor)."""
+        torch = self.torch
+        nsplit = splitters.shape[0]
+        counts = torch.zeros(nsplit + 1, dtype=torch.int64, device=t.device)
+        n = t.shape[0]
+        if n:
+            ws = self._ws(self.lib.qmsort_gpu_partition_workspace_bytes(core, n), t.device)
+            rc = self.lib.qmsort_gpu_partition_count(core, t.data_ptr(), n, splitters.data_ptr(), nsplit,
+                                                     counts.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                     self._s())
+            _lib.check(rc, "qmsort_gpu_partition_count")
+        return counts
+
+    def scatter_peers(self, t, core: int, nsplit: int, dests: Sequence[int], offsets: Sequence[int]) -> None:
+        """Bucket b of t (planned by partition_count) -> dests[b] + offsets[b] keys."""
+        n = t.shape[0]
+        if not n:
+            return
+        ws = self.wsbuf
+        P = nsplit + 1
+        d = (ctypes.c_void_p * P)(*[int(x) for x in dests])
+        o = (ctypes.c_uint64 * P)(*[int(x) for x in offsets])
+        rc = self.lib.qmsort_gpu_partition_scatter_peers(core, t.data_ptr(), n, nsplit, d, o,
+                                                         ws.data_ptr(), ws.numel(), self._s())
+        _lib.check(rc, "qmsort_gpu_partition_scatter_peers")
+
 
 # ---------------------------------------------------------------------------
 # exchanges
@@ -127,6 +156,61 @@ class TorchExchange:
         self.dist.all_to_all_single(out, t, output_split_sizes=list(recv), input_split_sizes=list(send),
                                     group=self.group)
         return out
+
+
+class PeerExchange(TorchExchange):
+    """The data exchange fused into the partition (one process per GPU): every
+    rank exports a receive buffer through CUDA IPC once; senders' scatter
+    kernels then store their bucket for rank j straight into rank j's buffer
+    over NVLink (qmsort_gpu_partition_scatter_peers).  torch.distributed only
+    carries the handles, the P x P bucket-size matrix and two barriers -- no
+    collective touches the keys."""
+
+    fused = True
+
+    def __init__(self, group: Any = None):
+        super().__init__(group)
+        self.lib = _lib.load()
+        self.recv = None       # this rank's receive buffer (uint8 device tensor)
+        self.cap = 0           # its capacity in bytes
+        self.ptrs: list = []   # device pointers of every rank's buffer, opened here
+        self.opened: list = []  # mapping bases to close
+
+    def ensure_capacity(self, nbytes: int, device) -> None:
+        """Collective: (re)allocate every rank's buffer to >= nbytes and swap handles."""
+        import torch
+        if self.recv is not None and self.cap >= nbytes:
+            return
+        for p in self.opened:
+            _lib.check(self.lib.qmsort_gpu_ipc_close(ctypes.c_void_p(p)), "qmsort_gpu_ipc_close")
+        self.opened = []
+        self.cap = max(int(nbytes * 1.25) + 4096, 1 << 20)
+        self.recv = torch.empty(self.cap, dtype=torch.uint8, device=device)
+        h = (ctypes.c_uint8 * _IPC_BYTES)()
+        off = ctypes.c_uint64()
+        _lib.check(self.lib.qmsort_gpu_ipc_handle(ctypes.c_void_p(self.recv.data_ptr()), h,
+                                                  ctypes.byref(off)), "qmsort_gpu_ipc_handle")
+        handles: list = [None] * self.P
+        self.dist.all_gather_object(handles, (bytes(h), int(off.value)), group=self.group)
+        self.ptrs = []
+        for j, (hb, ho) in enumerate(handles):
+            if j == self.rank:
+                self.ptrs.append(self.recv.data_ptr())
+                continue
+            buf = (ctypes.c_uint8 * _IPC_BYTES).from_buffer_copy(hb)
+            p, base = ctypes.c_void_p(), ctypes.c_void_p()
+            _lib.check(self.lib.qmsort_gpu_ipc_open(buf, ho, ctypes.byref(p), ctypes.byref(base)),
+                       "qmsort_gpu_ipc_open")
+            self.ptrs.append(int(p.value))
+            self.opened.append(int(base.value))
+
+    def barrier(self) -> None:
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
+
+
+_IPC_BYTES = 64  # QMSORT_IPC_HANDLE_BYTES
 
 
 def _wire(t, dt: int):
@@ -182,6 +266,8 @@ def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchang
     all_smp = ex.all_gather(smp).contiguous()
     ops.sort(all_smp, core)
     spl = pick_splitters(all_smp, P)
+    if getattr(ex, "fused", False):
+        return _exchange_fused(w, local, dt, core, cmp, spl, ex, ops)
     parted, counts = ops.partition(w, core, spl)
     recv_counts = ex.all_to_all_counts(counts)
     send = [int(x) for x in counts.tolist()]
@@ -190,6 +276,82 @@ def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchang
     ops.sort(got, core)
     ops.to_core(got, dt, cmp, inverse=True)
     return _unwire(got, core, local)
+
+
+_KEY_BYTES = {_lib.DT_U32: 4, _lib.DT_U64: 8, _lib.DT_REC32: 32}
+
+
+def _bucket_offsets(C: list, P: int, r: int) -> tuple[list, list]:
+    """From the P x P bucket-size matrix (row s = sender s): every rank's receive
+    total and where sender r's bucket j starts inside rank j's buffer."""
+    totals = [sum(C[s][j] for s in range(P)) for j in range(P)]
+    offs = [sum(C[s][j] for s in range(r)) for j in range(P)]
+    return totals, offs
+
+
+def _exchange_fused(w, local, dt: int, core: int, cmp: int, spl, ex, ops):
+    """Partition + exchange in one scatter pass: bucket j lands in rank j's buffer."""
+    import torch
+    P, r = ex.P, ex.rank
+    counts = ops.partition_count(w, core, spl)
+    cpu_group = ex.dist.get_backend(ex.group) == "gloo"
+    allc = ex.all_gather(counts.cpu() if cpu_group else counts)
+    C = allc.view(P, P).cpu().tolist()
+    totals, offs = _bucket_offsets(C, P, r)
+    kb = _KEY_BYTES[core]
+    ex.ensure_capacity(max(totals) * kb, w.device)
+    ex.barrier()  # every receiver is done with its buffer and holds the handles
+    ops.scatter_peers(w, core, P - 1, ex.ptrs, offs)
+    ex.barrier()  # every sender's stores into this rank's buffer have completed
+    rows = (totals[r],) + tuple(w.shape[1:])
+    got = ex.recv[: totals[r] * kb].view(w.dtype).view(rows)
+    ops.sort(got, core)
+    ops.to_core(got, dt, cmp, inverse=True)
+    return _unwire(got, core, local)
+
+
+def sort_sharded_emulated_fused(shards: list, less: Any = "less", *, dtype: int | None = None,
+                                ops: Any = None, oversample: int = 64, seed: int = 42) -> list:
+    """The fused exchange with P ranks emulated in one process on one GPU: each
+    rank's scatter stores its buckets straight into the other ranks' receive
+    buffers (plain device pointers instead of IPC-mapped peers)."""
+    import torch
+    from . import _cmp_code, dtype_of
+    dt = dtype_of(shards[0]) if dtype is None else dtype
+    core = CORE[dt]
+    cmp = _cmp_code(less)
+    P = len(shards)
+    like = shards[0]
+    # one workspace per emulated rank: each keeps its partition plan until its scatter
+    opss = [GpuOps() for _ in range(P)]
+    shards = [_wire(t, core) for t in shards]
+    for t, o in zip(shards, opss):
+        o.to_core(t, dt, cmp)
+    s = oversample * P
+    smps = []
+    for r, t in enumerate(shards):
+        smp = opss[r].sample(t, core, s, seed ^ (0x9E3779B97F4A7C15 * (r + 1) & 0xFFFFFFFFFFFFFFFF))
+        if smp.shape[0] < s:
+            pad = torch.full((s - smp.shape[0],) + tuple(t.shape[1:]), -1, dtype=t.dtype, device=t.device)
+            smp = torch.cat([smp, pad])
+        smps.append(smp)
+    all_smp = torch.cat(smps).contiguous()
+    opss[0].sort(all_smp, core)
+    spl = pick_splitters(all_smp, P)
+    C = [[int(x) for x in opss[r].partition_count(t, core, spl).tolist()] for r, t in enumerate(shards)]
+    totals = [sum(C[s_][j] for s_ in range(P)) for j in range(P)]
+    recvs = [torch.empty((totals[j],) + tuple(shards[0].shape[1:]), dtype=shards[0].dtype,
+                         device=shards[0].device) for j in range(P)]
+    ptrs = [t.data_ptr() for t in recvs]
+    for r, t in enumerate(shards):  # ops[r] still holds rank r's plan in its workspace
+        _, offs = _bucket_offsets(C, P, r)
+        opss[r].scatter_peers(t, core, P - 1, ptrs, offs)
+    out = []
+    for j in range(P):
+        opss[j].sort(recvs[j], core)
+        opss[j].to_core(recvs[j], dt, cmp, inverse=True)
+        out.append(_unwire(recvs[j], core, like))
+    return out
 
 
 def sort_sharded_emulated(shards: list, less: Any = "less", *, dtype: int | None = None,
@@ -260,7 +422,7 @@ def bench_main(args: Any, metric: str, unit: str) -> None:
     pristine = torch.empty(n, dtype=torch.uint32, device=dev)
     q.generate(q.GEN_U32, pristine, seed=42, start=rank * n, total=n * P)
     x = torch.empty_like(pristine)
-    ex = TorchExchange()
+    ex = PeerExchange() if getattr(args, "exchange", "peer") == "peer" else TorchExchange()
     ops = GpuOps()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
@@ -332,7 +494,7 @@ def bench_main(args: Any, metric: str, unit: str) -> None:
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
                 "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe, seed 42)",
                 "config": {"workload": f"distributed samplesort of {P} x 2^{n.bit_length() - 1} "
-                                       "uint32 keys (one NCCL all-to-all)",
+                                       "uint32 keys (" + ("exchange fused into the scatter: IPC peer stores over NVLink" if getattr(args, "exchange", "peer") == "peer" else "one NCCL all-to-all") + ")",
                            "n_per_gpu": n, "parallelism": f"sharded samplesort x{P}",
                            "l2": "input 1 GiB per GPU > L2"},
                 "gpu_launches": launches,

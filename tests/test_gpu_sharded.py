@@ -68,3 +68,76 @@ def test_partition_by_splitters(nsplit):
     for j, c in enumerate(counts.cpu().numpy()):
         np.testing.assert_array_equal(np.sort(got[off:off + c]), np.sort(a[b == j]))
         off += c
+
+
+# ---- the exchange fused into the partition's scatter (peer stores) ----------
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("cfg,dt", [("u32", DT_U32), ("u64", DT_U64), ("rec32", DT_REC32),
+                                    ("f64_distinct16", DT_F64)])
+def test_emulated_fused_exchange_matches_oracle(oracle, P, cfg, dt):
+    """Every rank's scatter kernel stores its bucket j straight into rank j's
+    receive buffer (qmsort_gpu_partition_scatter_peers); no exchange copy."""
+    n = (1 << 20) + 12345
+    a = oracle.gen(cfg, n, seed=7)
+    out = sharded.sort_sharded_emulated_fused(shards_of(a, P), "less", dtype=dt)
+    torch.cuda.synchronize()
+    got = np.concatenate([o.cpu().numpy() for o in out])
+    np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+def test_emulated_fused_exchange_descending_and_ragged(oracle):
+    a = oracle.gen("u64", 200001, seed=3)
+    shards = [torch.from_numpy(x.copy()).cuda() for x in (a[:5], a[5:150000], a[150000:150000], a[150000:])]
+    out = sharded.sort_sharded_emulated_fused(shards, "greater", dtype=DT_U64)
+    got = np.concatenate([o.cpu().numpy() for o in out])
+    np.testing.assert_array_equal(got, oracle.sort(DT_U64, a, greater=True))
+
+
+def _peer_worker(rank, world, port, n, seed, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = np.random.default_rng(seed).integers(0, 2**63, n * world, dtype=np.uint64)
+        shard = torch.from_numpy(full[rank * n:(rank + 1) * n].copy()).cuda()
+        ex = sharded.PeerExchange()
+        res = []
+        for rep in range(2):  # the second call reuses the opened peer buffers
+            out = sharded.sort_sharded(shard.clone(), "less", dtype=DT_U64, exchange=ex,
+                                       ops=sharded.GpuOps(), force_exchange=True)
+            res.append(out.cpu().numpy().copy())
+            ex.barrier()
+        parts = [None] * world
+        dist.all_gather_object(parts, res)
+        if rank == 0:
+            q.put((full, parts))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ipc_peer_exchange_processes(world):
+    """One process per rank (here all on GPU 0): receive buffers exported with
+    qmsort_gpu_ipc_handle, opened by the peers, written by the peers' scatter
+    kernels.  Host collectives over gloo; no kernel waits on another."""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    qq = ctx.Queue()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 300000, 9, qq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    full, parts = qq.get(timeout=600)
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    want = np.sort(full)
+    for rep in range(2):
+        got = np.concatenate([parts[r][rep] for r in range(world)])
+        np.testing.assert_array_equal(got, want)

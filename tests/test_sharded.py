@@ -108,3 +108,18 @@ def test_duplicate_heavy_keys_emulated():
     shards = [torch.from_numpy(x.copy()) for x in np.array_split(full, 4)]
     out = sharded.sort_sharded_emulated(shards, "less", dtype=_lib.DT_F64, ops=NumpyOps())
     np.testing.assert_array_equal(np.concatenate([o.numpy() for o in out]), np.sort(full))
+
+
+@pytest.mark.parametrize("P", [1, 2, 5])
+def test_fused_exchange_offsets_tile_every_receive_buffer(P):
+    """_bucket_offsets: sender r's bucket j occupies [offs_r[j], offs_r[j] + C[r][j])
+    of rank j's buffer; the pieces tile [0, total_j) in sender order."""
+    rng = np.random.default_rng(P)
+    C = rng.integers(0, 50, (P, P)).tolist()
+    for j in range(P):
+        pos = 0
+        for r in range(P):
+            totals, offs = sharded._bucket_offsets(C, P, r)
+            assert offs[j] == pos
+            pos += C[r][j]
+        assert pos == totals[j]
