@@ -56,12 +56,11 @@ struct OddEvenNet {
     static constexpr Pairs kPairs = make();
 };
 
-// uint32 keys: compare-and-swaps finish on the FMA pipe
-// (KeyTraits<uint32_t>::cas_alt), relieving the ALU pipe the kernel is bound by.
+// Network compare-and-swaps finish on the FMA pipe (KeyTraits<K>::cas_alt:
+// the maximum's words by IMADs), relieving the ALU pipe the kernel is bound by.
 template <class K>
 __device__ __forceinline__ void net_cas(K& a, K& b, int) {
-    if constexpr (std::is_same_v<K, uint32_t>) KeyTraits<K>::cas_alt(a, b);
-    else KeyTraits<K>::cas(a, b);
+    KeyTraits<K>::cas_alt(a, b);
 }
 
 template <class K, int N, size_t... I>

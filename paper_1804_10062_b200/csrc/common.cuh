@@ -28,6 +28,14 @@ struct KeyTraits;
 __constant__ uint32_t c_neg1 = 0xFFFFFFFFu;
 __constant__ uint32_t c_one = 1u;
 
+// x + y - m (mod 2^32) with two IMADs: given the 32-bit word m of the smaller
+// of two keys, the same word of the larger one (the words of {min, max} are a
+// permutation of the words of {a, b}, so their sums agree mod 2^32).
+__device__ __forceinline__ uint32_t other_word(uint32_t x, uint32_t y, uint32_t m) {
+    const uint32_t t = m * c_neg1 + x;  // x - m
+    return t * c_one + y;
+}
+
 template <>
 struct KeyTraits<uint32_t> {
     static constexpr int kBytes = 4;
@@ -69,6 +77,15 @@ struct KeyTraits<uint64_t> {
         a = lo;
         b = hi;
     }
+    // same result: the minimum selected on the ALU pipe, the maximum's two
+    // words by IMADs on the FMA pipe (other_word)
+    __device__ __forceinline__ static void cas_alt(uint64_t& a, uint64_t& b) {
+        const uint64_t mn = (b < a) ? b : a;
+        const uint32_t xl = other_word((uint32_t)a, (uint32_t)b, (uint32_t)mn);
+        const uint32_t xh = other_word((uint32_t)(a >> 32), (uint32_t)(b >> 32), (uint32_t)(mn >> 32));
+        b = ((uint64_t)xh << 32) | xl;
+        a = mn;
+    }
     __device__ __forceinline__ static uint64_t hash(uint64_t a) { return a; }
     __device__ __forceinline__ static uint64_t shfl_xor(uint64_t a, int m) {
         return __shfl_xor_sync(0xffffffffu, a, m);
@@ -106,6 +123,20 @@ struct KeyTraits<Rec32> {
         }
         a = lo;
         b = hi;
+    }
+    __device__ __forceinline__ static void cas_alt(Rec32& a, Rec32& b) {
+        const bool s = lt(b, a);
+        Rec32 mn, mx;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            mn.w[i] = s ? b.w[i] : a.w[i];
+            const uint32_t xl = other_word((uint32_t)a.w[i], (uint32_t)b.w[i], (uint32_t)mn.w[i]);
+            const uint32_t xh = other_word((uint32_t)(a.w[i] >> 32), (uint32_t)(b.w[i] >> 32),
+                                           (uint32_t)(mn.w[i] >> 32));
+            mx.w[i] = ((uint64_t)xh << 32) | xl;
+        }
+        a = mn;
+        b = mx;
     }
     __device__ __forceinline__ static Rec32 shfl_xor(const Rec32& a, int m) {
         Rec32 r;
