@@ -100,13 +100,16 @@ def _peer_worker(rank, world, port, n, seed, q):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        full = np.random.default_rng(seed).integers(0, 2**63, n * world, dtype=np.uint64)
-        shard = torch.from_numpy(full[rank * n:(rank + 1) * n].copy()).cuda()
+        full = np.random.default_rng(seed).integers(0, 2**63, 3 * n * world, dtype=np.uint64)
         ex = sharded.PeerExchange()
+        ops = sharded.GpuOps()
         res = []
-        for rep in range(2):  # the second call reuses the opened peer buffers
-            out = sharded.sort_sharded(shard.clone(), "less", dtype=DT_U64, exchange=ex,
-                                       ops=sharded.GpuOps(), force_exchange=True)
+        # call 2 reuses the opened peer buffers; call 3 has 3x the keys, so every
+        # rank grows its receive buffer and the handles are swapped again
+        for rep, m in enumerate((n, n, 3 * n)):
+            shard = torch.from_numpy(full[rank * m:(rank + 1) * m].copy()).cuda()
+            out = sharded.sort_sharded(shard, "less", dtype=DT_U64, exchange=ex, ops=ops,
+                                       force_exchange=True)
             res.append(out.cpu().numpy().copy())
             ex.barrier()
         parts = [None] * world
@@ -137,7 +140,7 @@ def test_ipc_peer_exchange_processes(world):
     for p in procs:
         p.join(timeout=600)
         assert p.exitcode == 0
-    want = np.sort(full)
-    for rep in range(2):
+    n = 300000
+    for rep, m in enumerate((n, n, 3 * n)):
         got = np.concatenate([parts[r][rep] for r in range(world)])
-        np.testing.assert_array_equal(got, want)
+        np.testing.assert_array_equal(got, np.sort(full[:m * world]))
