@@ -119,6 +119,15 @@ __device__ __forceinline__ void serial_merge_smem(const K* s, int ai, int aend, 
     }
 }
 
+// The same ITEMS outputs without a serial dependency chain: the thread's
+// window is A[ai, ai+x) (ascending) and B[bi, bi+ITEMS-x) (also ascending,
+// loaded reversed), i.e. a bitonic sequence, which a log2(ITEMS)-stage
+// half-cleaner network sorts in registers.  All loads are independent, and the
+// compare-and-swaps split over the ALU and FMA pipes (net_cas).  Keys only: the
+// output equals the serial merge's (equal keys are indistinguishable).
+template <class K, int ITEMS>
+__device__ __forceinline__ void bitonic_merge_window(const K* s, int ai, int x, int bi, K (&out)[ITEMS]);
+
 // min (lower = true) or max of a and b.
 template <class K>
 __device__ __forceinline__ K select_minmax(const K& a, const K& b, bool lower) {
@@ -162,6 +171,22 @@ __device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j)
             if ((j & s) == 0) net_cas<K>(k[j], k[j + s], j + s);
+    }
+}
+
+template <class K, int ITEMS>
+__device__ __forceinline__ void bitonic_merge_window(const K* s, int ai, int x, int bi, K (&out)[ITEMS]) {
+    using P = SmemPad<K>;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int idx = i < x ? ai + i : bi + (ITEMS - 1 - i);
+        out[i] = s[P::idx((unsigned)idx)];
+    }
+#pragma unroll
+    for (int st = ITEMS / 2; st >= 1; st >>= 1) {
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j)
+            if ((j & st) == 0) net_cas<K>(out[j], out[j + st], j + st);
     }
 }
 
@@ -243,7 +268,12 @@ struct BlockSorter {
                 const int alen = min(run, mp - a0);
                 const int blen = max(0, min(run, mp - b0));
                 const int a = merge_path_smem<K>(s, a0, alen, b0, blen, diag);
-                serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + alen, b0 + diag - a, b0 + blen, k);
+                if constexpr (sizeof(K) > 8) {  // records: the wide serial merge is select-heavy
+                    const int a_end = merge_path_smem<K>(s, a0, alen, b0, blen, diag + ITEMS);
+                    bitonic_merge_window<K, ITEMS>(s, a0 + a, a_end - a, b0 + diag - a, k);
+                } else {
+                    serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + alen, b0 + diag - a, b0 + blen, k);
+                }
             }
             __syncthreads();
         }

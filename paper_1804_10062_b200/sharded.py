@@ -266,7 +266,7 @@ def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchang
     all_smp = ex.all_gather(smp).contiguous()
     ops.sort(all_smp, core)
     spl = pick_splitters(all_smp, P)
-    if getattr(ex, "fused", False):
+    if getattr(ex, "fused", False) and P <= 8:  # the peer scatter addresses up to 8 ranks
         return _exchange_fused(w, local, dt, core, cmp, spl, ex, ops)
     parted, counts = ops.partition(w, core, spl)
     recv_counts = ex.all_to_all_counts(counts)
