@@ -316,6 +316,7 @@ def run_ours(args) -> None:
                        "n": n, "key_bytes": kb, "algorithm": args.algorithm,
                        "l2": "flushed (256 MiB write) before every timed step; input > L2",
                        "parallelism": "single GPU"},
+            "step_ms": [round(t, 4) for t in times],
             "gpu_launches": launches, "clocks": clk, "roofline": roofline,
             "sort_roofline": sort_roofline}
 

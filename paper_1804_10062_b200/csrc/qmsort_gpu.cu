@@ -191,6 +191,22 @@ static cudaError_t allow_smem(const void* fn, size_t bytes) {
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// Waits inside a sort poll instead of blocking: the host thread never sleeps,
+// so the launches that follow a control read go out at once (the wake-up of a
+// blocking wait occasionally left milliseconds of idle GPU between kernels).
+static cudaError_t spin_sync(cudaStream_t st) {
+    cudaError_t e;
+    while ((e = cudaStreamQuery(st)) == cudaErrorNotReady) {
+    }
+    return e;
+}
+static cudaError_t spin_event(cudaEvent_t ev) {
+    cudaError_t e;
+    while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    }
+    return e;
+}
+
 // Pool of small mapped pinned host buffers for control reads (read_small).
 constexpr uint32_t kMappedBytes = 8192;
 static std::mutex g_mapped_mu;
@@ -233,7 +249,7 @@ static int read_small(cudaStream_t st, void* dst0, const void* src0, size_t b0,
     SmallRead r1{static_cast<const unsigned char*>(src1), (uint32_t)b1, (uint32_t)align_up(b0, 16)};
     store_mapped_kernel<<<1, 256, 0, st>>>(r0, r1, mb.dev);
     QCK(cudaGetLastError());
-    QCK(cudaStreamSynchronize(st));
+    QCK(spin_sync(st));
     std::memcpy(dst0, mb.host, b0);
     if (b1) std::memcpy(dst1, mb.host + r1.dst_off, b1);
     return QMSORT_OK;
@@ -256,6 +272,8 @@ static unsigned resident_grid(const void* fn, int threads, size_t smem) {
     return r;
 }
 
+constexpr int kCntSlots = 18;  // LevelCounters of one sort: one per partition level (+1)
+
 struct WsLayout {
     size_t b_off = 0, segs_off[2] = {0, 0}, chunks_off[2] = {0, 0}, cnt_off[2] = {0, 0};
     size_t tree_off[2] = {0, 0}, sorted_off[2] = {0, 0}, lut_off[2] = {0, 0};
@@ -277,7 +295,7 @@ static WsLayout make_layout(size_t n) {
     L.seg_cap = (uint32_t)(n / cap + 2);
     L.chunk_cap = (uint32_t)(L.seg_cap + n / ch + 2);
     L.split_cap = (uint32_t)(2 * n / target + 2 * (uint64_t)L.seg_cap + 2 * (1u << TU::LOGKMAX) + 64);
-    L.task_cap = 2 * L.split_cap + 64;
+    L.task_cap = 4 * L.split_cap + 64;  // per class, all levels of one sort
     L.fill_cap = L.split_cap;
     L.hist_cap = (uint32_t)(2ull * (1u << TU::LOGKMAX) * (n / ch + 2) + 2ull * L.split_cap);
     size_t o = 0;
@@ -290,7 +308,7 @@ static WsLayout make_layout(size_t n) {
     for (int i = 0; i < 2; ++i) {
         L.segs_off[i] = take(sizeof(SegDesc) * L.seg_cap);
         L.chunks_off[i] = take(sizeof(ChunkDesc) * L.chunk_cap);
-        L.cnt_off[i] = take(sizeof(LevelCounters));
+        L.cnt_off[i] = take(sizeof(LevelCounters) * (i == 0 ? kCntSlots : 1));
         L.tree_off[i] = take(sizeof(K) * L.split_cap);
         L.sorted_off[i] = take(sizeof(K) * L.split_cap);
         L.lut_off[i] = take(KeyTraits<K>::kLut ? sizeof(uint32_t) * kLutPerSplitter * (size_t)L.split_cap : 0);
@@ -327,17 +345,31 @@ static int blocksort_one(const K* src, K* dst, uint64_t off, uint64_t len, cudaS
     return launch_tiles<K, TU::CLS_T[3], TU::BI>(src, dst, off, len, st, led);
 }
 
-// Block-sort every task of size class C (src -> dst at the same offsets).
+// Block-sort the `count` tasks of size class C into A: one CTA per task.
 template <class K, int C>
-static int launch_class(const SortTask* tasks, uint32_t count, const K* src, K* dst,
-                        uint64_t bytes, cudaStream_t st, Ledger& led) {
+static int launch_class(const SortTask* tasks, uint32_t count, K* A, const K* B, cudaStream_t st,
+                        Ledger& led) {
     using TU = Tune<K>;
     constexpr int T = TU::CLS_T[C];
     using BS = BlockSorter<K, T, TU::BI>;
+    if (count == 0) return QMSORT_OK;
     auto fn = blocksort_tasks_kernel<K, T, TU::BI>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
-    QLAUNCH(led, kPhBlocksort, bytes, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, src, dst));
+    QLAUNCH(led, kPhBlocksort, 0, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, A, B));
     return QMSORT_OK;
+}
+
+// Partition levels a balanced split needs before every bucket fits the block
+// sorter: the levels enqueued at once, without a host round trip between them.
+static int estimate_levels(uint64_t n, const PlanParams& p) {
+    int lv = 0;
+    uint64_t len = n;
+    while (len > p.cap && lv < 16) {
+        const uint32_t k = choose_logk(len, p.target, p.log_kmax, p.slack);
+        len = (len + (1ull << k) - 1) >> k;
+        ++lv;
+    }
+    return lv;
 }
 
 // Block-sort tiles + merge-path passes over [off, off+len); the range currently
@@ -392,10 +424,15 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     K* tree[2];
     K* sorted[2];
     uint32_t* lut[2];
+    LevelCounters* cnts = reinterpret_cast<LevelCounters*>(ws + L.cnt_off[0]);
+    // sort-wide block-sort tasks and equal-key fills: every level's small
+    // buckets keep their place (later levels never touch them), so they are
+    // all sorted once, after the last partition level
+    LevelCounters* tot = &cnts[kCntSlots - 1];
     for (int i = 0; i < 2; ++i) {
         lv[i].segs = reinterpret_cast<SegDesc*>(ws + L.segs_off[i]);
         lv[i].chunks = reinterpret_cast<ChunkDesc*>(ws + L.chunks_off[i]);
-        lv[i].cnt = reinterpret_cast<LevelCounters*>(ws + L.cnt_off[i]);
+        lv[i].cnt = &cnts[i];
         lv[i].seg_cap = L.seg_cap;
         lv[i].chunk_cap = L.chunk_cap;
         lv[i].split_cap = L.split_cap;
@@ -408,7 +445,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     SortTask* tasks = reinterpret_cast<SortTask*>(ws + L.tasks_off);
     FillTask* fills = reinterpret_cast<FillTask*>(ws + L.fills_off);
 
-    QCK(cudaMemsetAsync(lv[0].cnt, 0, sizeof(LevelCounters), st));
+    // every level's counters start at zero; level l reads its segment and
+    // chunk counts from cnts[l] (written by level l-1) on the device
+    QCK(cudaMemsetAsync(cnts, 0, sizeof(LevelCounters) * kCntSlots, st));
     QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<16, 256, 0, st>>>(lv[0], n, ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K))), p));
 
     using BSS = BlockSorter<K, TU::ST, TU::SI>;
@@ -420,78 +459,93 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
     const unsigned scatter_grid = resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM));
     const unsigned count_grid = resident_grid((const void*)count_fn, TU::CT, 0);
+    const unsigned sample_grid = resident_grid((const void*)sample_fn, TU::ST, BSS::kSmemBytes);
+    auto plan_fn = plan_kernel<K, 512, TU::LOGKMAX>;
+    const unsigned plan_grid = resident_grid((const void*)plan_fn, 512, 0);
+    const unsigned colsum_grid = resident_grid((const void*)colsum_kernel, 512, 0);
 
-    uint64_t level_keys = n;
-    uint32_t nsegs = 1;
-    uint32_t nchunks = (uint32_t)((n + L.chunk_elems - 1) / L.chunk_elems);
-    int cur = 0;
     K* src = A;
     K* dst = B;
-    const int max_levels = cfg.max_levels > 0 ? cfg.max_levels : 8;
-    for (int level = 0; nsegs > 0; ++level) {
-        const int nxt = cur ^ 1;
+    const int max_levels = std::min(cfg.max_levels > 0 ? cfg.max_levels : 8, kCntSlots - 2);
+    int level = 0;
+    int batch = std::max(1, estimate_levels(n, p));
+    LevelCounters hc[kCntSlots];
+    for (;;) {
+        // enqueue a batch of levels back to back: every grid is persistent
+        // and reads its work counts on the device
+        const int stop = std::min(level + batch, max_levels);
+        for (; level < stop; ++level) {
+            const int cur = level & 1, nxt = cur ^ 1;
+            lv[cur].cnt = &cnts[level];
+            lv[nxt].cnt = &cnts[level + 1];
+            LevelCounters* c = &cnts[level];
+            p.dst_is_a = (dst == A) ? 1 : 0;
+            const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
+            QLAUNCH(led, kPhSample, 0,
+                    sample_fn<<<sample_grid, TU::ST, BSS::kSmemBytes, st>>>(
+                        lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u));
+            QLAUNCH(led, kPhCount, 0,
+                    count_fn<<<count_grid, TU::CT, 0, st>>>(lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks,
+                                                            &c->work_count, src, tree[cur], sorted[cur],
+                                                            lut[cur], hist));
+            QLAUNCH(led, kPhPlan, 0,
+                    colsum_kernel<<<colsum_grid, 512, 0, st>>>(lv[cur].segs, hist, 0u, &c->nsegs));
+            QLAUNCH(led, kPhPlan, 0,
+                    plan_fn<<<plan_grid, 512, 0, st>>>(lv[cur].segs, hist, sorted[cur], lv[nxt], p, tasks,
+                                                      fills, c, tot));
+            QLAUNCH(led, kPhScatter, 0,
+                    scatter_fn<<<scatter_grid, TU::XT, sizeof(SM), st>>>(
+                        lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks, &c->work_scatter, src, dst,
+                        tree[cur], sorted[cur], lut[cur], hist, PeerArgs{}));
+            std::swap(src, dst);
+        }
+        // one control read per batch
+        QTRY(read_small(st, hc, cnts, sizeof(LevelCounters) * (size_t)(level + 1), &hc[kCntSlots - 1],
+                        tot, sizeof(LevelCounters)));
+        ++led.launches;
+        ++led.syncs;
+        for (int l = 0; l <= level; ++l)
+            if (hc[l].overflow) return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
+        if (hc[level].nsegs == 0) break;
         if (level >= max_levels) {
             // K8 fallback: the remaining oversized buckets are merge-sorted.
-            std::vector<SegDesc> h(nsegs);
-            QCK(cudaMemcpyAsync(h.data(), lv[cur].segs, sizeof(SegDesc) * nsegs,
+            std::vector<SegDesc> h(hc[level].nsegs);
+            QCK(cudaMemcpyAsync(h.data(), lv[level & 1].segs, sizeof(SegDesc) * h.size(),
                                 cudaMemcpyDeviceToHost, st));
-            QCK(cudaStreamSynchronize(st));
+            QCK(spin_sync(st));
             ++led.syncs;
             for (const SegDesc& d : h) QTRY(mergesort_range<K>(src, A, B, d.off, d.len, st, led));
             break;
         }
-        p.dst_is_a = (dst == A) ? 1 : 0;
-        const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
-        QLAUNCH(led, kPhSample, 0,
-                sample_fn<<<nsegs, TU::ST, BSS::kSmemBytes, st>>>(lv[cur].segs, src, tree[cur],
-                                                                  sorted[cur], lut[cur], seed, 32u));
-        QLAUNCH(led, kPhCount, level_keys * sizeof(K),
-                count_fn<<<std::min(nchunks, count_grid), TU::CT, 0, st>>>(
-                    lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_count, src, tree[cur],
-                    sorted[cur], lut[cur], hist));
-        const unsigned gy = (unsigned)std::max<uint32_t>(1, std::min<uint32_t>(128, nchunks / nsegs / 4));
-        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(nsegs, gy), 512, 0, st>>>(lv[cur].segs, hist));
-        QCK(cudaMemsetAsync(lv[nxt].cnt, 0, sizeof(LevelCounters), st));
-        QLAUNCH(led, kPhPlan, 0,
-                plan_kernel<K, 512, TU::LOGKMAX><<<nsegs, 512, 0, st>>>(
-                    lv[cur].segs, hist, sorted[cur], lv[nxt], p, tasks, fills, lv[cur].cnt));
-        QLAUNCH(led, kPhScatter, 2 * level_keys * sizeof(K),
-                scatter_fn<<<std::min(nchunks, scatter_grid), TU::XT, sizeof(SM), st>>>(
-                    lv[cur].segs, lv[cur].chunks, nchunks, &lv[cur].cnt->work_scatter, src, dst,
-                    tree[cur], sorted[cur], lut[cur], hist, PeerArgs{}));
-        LevelCounters hc[2];
-        QTRY(read_small(st, &hc[0], lv[cur].cnt, sizeof(LevelCounters), &hc[1], lv[nxt].cnt,
-                        sizeof(LevelCounters)));
-        ++led.launches;
-        ++led.syncs;
-        if (hc[0].overflow || hc[1].overflow)
-            return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
+        batch = 1;  // more levels than a balanced split needs: continue one at a time
+    }
+    // block-sort every bucket that fits one CTA (all levels; counts from the
+    // control read), then the fills
+    const uint32_t* nt = hc[kCntSlots - 1].ntasks;
+    for (int c = 0; c < kNumClasses; ++c)
+        if (nt[c] > L.task_cap) return fail(QMSORT_EINTERNAL, "block-sort task list capacity exceeded");
+    QTRY((launch_class<K, 0>(tasks + 0 * (size_t)L.task_cap, nt[0], A, B, st, led)));
+    QTRY((launch_class<K, 1>(tasks + 1 * (size_t)L.task_cap, nt[1], A, B, st, led)));
+    QTRY((launch_class<K, 2>(tasks + 2 * (size_t)L.task_cap, nt[2], A, B, st, led)));
+    QTRY((launch_class<K, 3>(tasks + 3 * (size_t)L.task_cap, nt[3], A, B, st, led)));
+    if (hc[kCntSlots - 1].nfill)
+        QLAUNCH(led, kPhFill, 0, fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, L.fill_cap, A));
+    // pass ledger from the device counters (count 1, scatter 2, block sort 2, fill 1)
+    const uint64_t w = sizeof(K);
+    for (int l = 0; l < level; ++l) {
+        const LevelCounters& c = hc[l];
+        if (c.nsegs == 0) continue;
         ++led.levels;
-        led.resplits += hc[0].resplits;
-        // block-sort every bucket of this level; the bytes are credited to the
-        // level's first launch
-        uint64_t bs_bytes = 2ull * hc[0].task_keys * sizeof(K);
-        const uint32_t* nt = hc[0].ntasks;
-#define QCLASS(c)                                                                              \
-    if (nt[c]) {                                                                               \
-        QTRY((launch_class<K, c>(tasks + (size_t)(c) * L.task_cap, nt[c], dst, A, bs_bytes, st, led))); \
-        bs_bytes = 0;                                                                          \
+        led.resplits += c.resplits;
+        led.ph_bytes[kPhCount] += c.nkeys * w;
+        led.ph_bytes[kPhScatter] += 2 * c.nkeys * w;
+        led.alg_bytes += 3 * c.nkeys * w;
     }
-        QCLASS(0)
-        QCLASS(1)
-        QCLASS(2)
-        QCLASS(3)
-#undef QCLASS
-        if (hc[0].nfill) {
-            QLAUNCH(led, kPhFill, hc[0].fill_keys * sizeof(K),
-                    fill_kernel<K><<<1184, 256, 0, st>>>(fills, hc[0].nfill, lv[cur].segs, sorted[cur], A));
-        }
-        level_keys = hc[1].nkeys;
-        nsegs = hc[1].nsegs;
-        nchunks = hc[1].nchunks;
-        cur = nxt;
-        std::swap(src, dst);
-    }
+    const LevelCounters& t = hc[kCntSlots - 1];
+    if (t.overflow) return fail(QMSORT_EINTERNAL, "samplesort work-list capacity exceeded");
+    led.ph_bytes[kPhBlocksort] += 2 * t.task_keys * w;
+    led.ph_bytes[kPhFill] += t.fill_keys * w;
+    led.alg_bytes += 2 * t.task_keys * w + t.fill_keys * w;
     return QMSORT_OK;
 }
 
@@ -624,7 +678,7 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     }
     if (rc == QMSORT_OK) rc = run_transform(dt, cmp, d, n, 1, st, led);
     cudaEventRecord(e1, st);
-    cudaError_t se = cudaEventSynchronize(e1);
+    cudaError_t se = spin_event(e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e0);
@@ -770,8 +824,8 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
         auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
         QLAUNCH(led, kPhCount, n * sizeof(K),
                 count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
-                           st>>>(seg, chunks, nchunks, &cnt->work_count, in, tree, sorted, lut, hist));
-        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<dim3(1, 64), 512, 0, st>>>(seg, hist));
+                           st>>>(seg, chunks, nchunks, nullptr, &cnt->work_count, in, tree, sorted, lut, hist));
+        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<64, 512, 0, st>>>(seg, hist, 1u, nullptr));
         QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
     }
     if (!(parts & 2) || n == 0) return QMSORT_OK;
@@ -781,16 +835,16 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
         QCK(allow_smem((const void*)fn, sizeof(SM)));
         QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
                 fn<<<std::min(nchunks, resident_grid((const void*)fn, TU::XT, sizeof(SM))), TU::XT,
-                     sizeof(SM), st>>>(seg, chunks, nchunks, &cnt->work_scatter, in, out, tree, sorted,
-                                       lut, hist, *peers));
+                     sizeof(SM), st>>>(seg, chunks, nchunks, nullptr, &cnt->work_scatter, in, out, tree,
+                                       sorted, lut, hist, *peers));
         return QMSORT_OK;
     }
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
     QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
             scatter_fn<<<std::min(nchunks, resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM))),
-                         TU::XT, sizeof(SM), st>>>(seg, chunks, nchunks, &cnt->work_scatter, in, out,
-                                                   tree, sorted, lut, hist, PeerArgs{}));
+                         TU::XT, sizeof(SM), st>>>(seg, chunks, nchunks, nullptr, &cnt->work_scatter, in,
+                                                   out, tree, sorted, lut, hist, PeerArgs{}));
     return QMSORT_OK;
 }
 
@@ -825,7 +879,7 @@ struct CallFrame {
         cudaError_t se = cudaSuccess;
         if (e1) {
             cudaEventRecord(e1, st);
-            se = cudaEventSynchronize(e1);
+            se = spin_event(e1);
             cudaEventElapsedTime(&ms, e0, e1);
         }
         if (own) cudaFreeAsync(ws, st);
@@ -991,7 +1045,7 @@ static int select_core(K* A, size_t n, size_t k0, const qmsort_gpu_config& cfg, 
         uint64_t cnt[4] = {0, 0, 0, 0};
         QCK(cudaMemcpyAsync(cnt, dcnt, sizeof(uint64_t) * (ns + 1), cudaMemcpyDeviceToHost, st));
         QCK(cudaMemcpyAsync(A + lo, B + lo, m * sizeof(K), cudaMemcpyDeviceToDevice, st));
-        QCK(cudaStreamSynchronize(st));
+        QCK(spin_sync(st));
         ++led.syncs;
         ++led.levels;
         const size_t want = k0 - lo;

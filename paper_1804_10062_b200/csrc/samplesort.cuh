@@ -80,14 +80,13 @@ struct ChunkDesc {
 struct SortTask {  // one bucket for the block sorter
     uint64_t off;
     uint32_t len;
-    uint32_t pad;
+    uint32_t in_a;  // the bucket was scattered into A (else into B); it is sorted into A
 };
 
-struct FillTask {  // equal-key bucket: every key equals the segment's splitter j
+struct FillTask {  // equal-key bucket: every key equals the segment's splitter
     uint64_t off;
     uint64_t len;
-    uint32_t seg;
-    uint32_t j;
+    alignas(16) unsigned char value[32];  // that key (sizeof(K) bytes)
 };
 
 struct LevelCounters {
@@ -310,10 +309,10 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
 // K1: per-segment sample + splitter selection.  One CTA per segment.
 // ---------------------------------------------------------------------------
 template <class K, int T, int ITEMS>
-__global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __restrict__ src,
-                                                   K* tree_store, K* sorted_store,
-                                                   uint32_t* lut_store, uint64_t seed,
-                                                   uint32_t oversample) {
+__device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, const K* __restrict__ src,
+                                               K* tree_store, K* sorted_store,
+                                               uint32_t* lut_store, uint64_t seed,
+                                               uint32_t oversample) {
     using BS = BlockSorter<K, T, ITEMS>;
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
@@ -322,7 +321,6 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
     __shared__ uint32_t flags[1024 + 1];
     __shared__ uint32_t warp_sums[32];
 
-    const uint32_t seg = blockIdx.x;
     const SegDesc d = segs[seg];
     const uint32_t K_ = 1u << d.logk;
     const int S = (int)min((uint32_t)BS::kCap, max(1024u, oversample * K_));
@@ -412,6 +410,21 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const K* __res
     }
 }
 
+// The level's segment count is read on the device (written by the previous
+// level's plan), so a whole sort is enqueued without host round trips.
+template <class K, int T, int ITEMS>
+__global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const uint32_t* __restrict__ nsegs,
+                                                   const K* __restrict__ src, K* tree_store,
+                                                   K* sorted_store, uint32_t* lut_store,
+                                                   uint64_t seed, uint32_t oversample) {
+    const uint32_t ns = *nsegs;
+    for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
+        sample_segment<K, T, ITEMS>(seg, segs, src, tree_store, sorted_store, lut_store, seed,
+                                    oversample);
+        __syncthreads();  // shared memory is reused by the next segment
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K2: per-chunk bucket histogram.
 // ---------------------------------------------------------------------------
@@ -459,9 +472,10 @@ __device__ __forceinline__ void count_chunk(const ClassifierSmem<K, LOG_KMAX>& c
 // Persistent CTAs fetch chunks dynamically from *work (no tail of idle SMs);
 // the classifier is reloaded only when the segment changes.
 template <class K, int T, int U, int LOG_KMAX>
-__global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ segs,
+__global__ void __launch_bounds__(T, 4) count_kernel(const SegDesc* __restrict__ segs,
                                                   const ChunkDesc* __restrict__ chunks,
-                                                  uint32_t nchunks, uint32_t* __restrict__ work,
+                                                  uint32_t nchunks, const uint32_t* __restrict__ nchunks_dev,
+                                                  uint32_t* __restrict__ work,
                                                   const K* __restrict__ src,
                                                   const K* __restrict__ tree_store,
                                                   const K* __restrict__ sorted_store,
@@ -471,12 +485,13 @@ __global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ se
     __shared__ ClassifierSmem<K, LOG_KMAX> cls;
     __shared__ uint32_t shist[2 * KMAX];
     __shared__ uint32_t next_chunk;
+    const uint32_t nck = nchunks_dev ? *nchunks_dev : nchunks;  // device count: no host round trip
     uint32_t cur_seg = 0xFFFFFFFFu;
     for (;;) {
         if (threadIdx.x == 0) next_chunk = atomicAdd(work, 1u);
         __syncthreads();
         const uint32_t ck = next_chunk;
-        if (ck >= nchunks) break;
+        if (ck >= nck) break;
         const ChunkDesc c = chunks[ck];
         const SegDesc d = segs[c.seg];
         if (c.seg != cur_seg) {
@@ -491,13 +506,22 @@ __global__ void __launch_bounds__(T) count_kernel(const SegDesc* __restrict__ se
 // K3a: per (segment, bin): exclusive prefix over the segment's chunks (in
 // place) and the bin total (entry nchunks).  One warp per bin.
 // ---------------------------------------------------------------------------
+// One warp per (segment, bin) pair, flattened over the level's segments (the
+// segment count is read on the device; null nsegs_dev = the host's nsegs).
 __global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__ segs,
-                                                     uint32_t* __restrict__ hist) {
-    const SegDesc d = segs[blockIdx.x];
-    const uint32_t nb = (1u << d.logk) << d.eq;
+                                                     uint32_t* __restrict__ hist, uint32_t nsegs,
+                                                     const uint32_t* __restrict__ nsegs_dev) {
+    constexpr uint32_t NBMAX = 1024;  // 2 << LOG_KMAX for every key type
+    const uint32_t ns = nsegs_dev ? *nsegs_dev : nsegs;
     const int lane = threadIdx.x & 31;
-    const uint32_t stride = d.nchunks + 1;
-    for (uint32_t b = blockIdx.y * 16 + (threadIdx.x >> 5); b < nb; b += gridDim.y * 16) {
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t idx = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+         idx < (uint64_t)ns * NBMAX; idx += nw) {
+        const SegDesc d = segs[idx / NBMAX];
+        const uint32_t b = (uint32_t)(idx % NBMAX);
+        const uint32_t nb = (1u << d.logk) << d.eq;
+        if (b >= nb) continue;
+        const uint32_t stride = d.nchunks + 1;
         uint32_t* col = hist + d.hist_base + b * stride;
         uint32_t carry = 0;
         for (uint32_t c0 = 0; c0 < d.nchunks; c0 += 128) {
@@ -534,7 +558,8 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                                                  LevelBufs next, PlanParams p,
                                                  SortTask* __restrict__ tasks,
                                                  FillTask* __restrict__ fills,
-                                                 LevelCounters* __restrict__ cur_cnt) {
+                                                 LevelCounters* __restrict__ cur_cnt,
+                                                 LevelCounters* __restrict__ sort_cnt) {
     constexpr int NB = 2 << LOG_KMAX;
     __shared__ uint32_t tot[NB];
     __shared__ uint32_t start[NB];
@@ -542,7 +567,9 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t cls_count[kNumClasses], cls_base[kNumClasses];
     __shared__ unsigned long long cls_keys;
-    const uint32_t seg = blockIdx.x;
+    const uint32_t ns = cur_cnt->nsegs;  // device count: no host round trip
+    for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
+    __syncthreads();  // the previous segment's shared arrays are no longer read
     const SegDesc d = segs[seg];
     const uint32_t nb = (1u << d.logk) << d.eq;
     const uint32_t stride = d.nchunks + 1;
@@ -571,9 +598,9 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     __syncthreads();
     if (threadIdx.x < kNumClasses)
         cls_base[threadIdx.x] = cls_count[threadIdx.x]
-                                    ? atomicAdd(&cur_cnt->ntasks[threadIdx.x], cls_count[threadIdx.x])
+                                    ? atomicAdd(&sort_cnt->ntasks[threadIdx.x], cls_count[threadIdx.x])
                                     : 0u;
-    if (threadIdx.x == 0 && cls_keys) atomicAdd(&cur_cnt->task_keys, cls_keys);
+    if (threadIdx.x == 0 && cls_keys) atomicAdd(&sort_cnt->task_keys, cls_keys);
     __syncthreads();
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
         hist[d.hist_base + b * stride + d.nchunks] = start[b];
@@ -582,15 +609,15 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
         const uint64_t off = d.off + start[b];
         if (d.eq && (b & 1)) {  // equal-key bucket: final once it is in the caller's buffer
             if (!p.dst_is_a) {
-                const uint32_t f = atomicAdd(&cur_cnt->nfill, 1u);
+                const uint32_t f = atomicAdd(&sort_cnt->nfill, 1u);
                 if (f < p.fill_cap) {
                     FillTask ft;
                     ft.off = off;
                     ft.len = len;
-                    ft.seg = seg;
-                    ft.j = b >> 1;
+                    const K v = sorted_store[d.sp + (b >> 1)];
+                    memcpy(ft.value, &v, sizeof(K));
                     fills[f] = ft;
-                    atomicAdd(&cur_cnt->fill_keys, (unsigned long long)len);
+                    atomicAdd(&sort_cnt->fill_keys, (unsigned long long)len);
                 } else {
                     atomicExch(&cur_cnt->overflow, 1u);
                 }
@@ -604,7 +631,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 SortTask st;
                 st.off = off;
                 st.len = len;
-                st.pad = 0;
+                st.in_a = p.dst_is_a ? 1u : 0u;
                 tasks[(size_t)cls * p.task_cap + t] = st;
             } else {
                 atomicExch(&cur_cnt->overflow, 1u);
@@ -630,6 +657,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
             emit_segment(next, off, len, clo, chi, p, sampler);
         }
     }
+    }  // segments
 }
 
 // ---------------------------------------------------------------------------
@@ -793,7 +821,8 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
 template <class K, int T, int U, int LOG_KMAX, bool PEER = false>
 __global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict__ segs,
                                                     const ChunkDesc* __restrict__ chunks,
-                                                    uint32_t nchunks, uint32_t* __restrict__ work,
+                                                    uint32_t nchunks, const uint32_t* __restrict__ nchunks_dev,
+                                                    uint32_t* __restrict__ work,
                                                     const K* __restrict__ src, K* __restrict__ dst,
                                                     const K* __restrict__ tree_store,
                                                     const K* __restrict__ sorted_store,
@@ -815,13 +844,14 @@ __global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict
         peer_start[b] = st;
         peer_base[b] = b < peers.nb ? peers.dest[b] + (peers.off[b] - st) * sizeof(K) : 0ull;
     }
+    const uint32_t nck = nchunks_dev ? *nchunks_dev : nchunks;  // device count: no host round trip
     uint32_t cur_seg = 0xFFFFFFFFu;
     // persistent CTAs fetch chunks dynamically (no tail of idle SMs)
     for (;;) {
         if (threadIdx.x == 0) next_chunk = atomicAdd(work, 1u);
         __syncthreads();
         const uint32_t ck = next_chunk;
-        if (ck >= nchunks) break;
+        if (ck >= nck) break;
         const ChunkDesc c = chunks[ck];
         const SegDesc d = segs[c.seg];
         const uint32_t nb = (1u << d.logk) << d.eq;
@@ -862,28 +892,31 @@ __global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict
 }
 
 // Equal-key buckets that landed in the workspace: write the splitter value.
+// The fill count is read on the device (written by the level's plan).
 template <class K>
-__global__ void fill_kernel(const FillTask* __restrict__ fills, uint32_t nfill,
-                            const SegDesc* __restrict__ segs, const K* __restrict__ sorted_store,
-                            K* __restrict__ dst) {
-    for (uint32_t f = 0; f < nfill; ++f) {
+__global__ void fill_kernel(const FillTask* __restrict__ fills, const uint32_t* __restrict__ nfill,
+                            uint32_t fill_cap, K* __restrict__ dst) {
+    const uint32_t nf = min(*nfill, fill_cap);
+    for (uint32_t f = 0; f < nf; ++f) {
         const FillTask ft = fills[f];
-        const K v = sorted_store[segs[ft.seg].sp + ft.j];
+        K v;
+        memcpy(&v, ft.value, sizeof(K));
         for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ft.len;
              i += (uint64_t)gridDim.x * blockDim.x)
             dst[ft.off + i] = v;
     }
 }
 
-// Block-sort every task of one size class: src -> dst at the same offsets.
+// Block-sort every task of one size class into A (from A or B, at the same
+// offsets): one CTA per task (launched with the sort's task count).
 template <class K, int T, int ITEMS>
-__global__ void __launch_bounds__(T) blocksort_tasks_kernel(const SortTask* __restrict__ tasks,
-                                                            const K* src, K* dst) {
+__global__ void __launch_bounds__(T) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
+                                                            const K* B) {
     using BS = BlockSorter<K, T, ITEMS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s = reinterpret_cast<K*>(smem_raw);
     const SortTask t = tasks[blockIdx.x];
-    BS::sort_tile(src + t.off, dst + t.off, (int)t.len, s);
+    BS::sort_tile((t.in_a ? A : B) + t.off, A + t.off, (int)t.len, s);
 }
 
 // Block-sort consecutive tiles of a range (merge-sort front end / fallback).
