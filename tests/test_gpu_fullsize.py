@@ -68,3 +68,32 @@ def test_c2_descending_full_size():
     q.sort(x, q.qms(), "greater")
     viol, s_out, x_out = q.check(x, "greater")
     assert viol == 0 and (s_out, x_out) == (s_in, x_in)
+
+
+@pytest.mark.parametrize("name,k_frac", [("u32", 0.5), ("u32", 1e-6), ("u64", 0.9), ("rec32", 0.3)])
+def test_full_size_select_nth(name, k_frac):
+    """select_nth at the full config size: the k-th key equals position k-1 of
+    the full sort, whose digest matches the reference's (test above)."""
+    g = GOLD[name]
+    n = g["n"]
+    kind, tdt, tail = GEN[name]
+    x = torch.empty((n,) + tail, dtype=tdt, device="cuda")
+    q.generate(kind, x, seed=g["seed"], total=n)
+    y = x.clone()
+    k = max(1, int(n * k_frac))
+    _, s_in, x_in = q.check(x, order=False)
+    p = q.select_nth(x, k)
+    assert p == k - 1
+    _, s_out, x_out = q.check(x, order=False)
+    assert (s_out, x_out) == (s_in, x_in)  # a permutation of the input
+    q.sort(y, q.qms())
+    assert sha_tensor(y) == g["sorted_sha256"]
+    assert torch.equal(x[p], y[p])
+    del y
+    # partition around position k-1 (unsigned order for the integer configs)
+    if not tail:
+        xv = x.view(torch.int64 if x.element_size() == 8 else torch.int32)
+        pv = int(xv[p].item()) & ((1 << (8 * x.element_size())) - 1)
+        lo = x[:p].cpu().numpy()
+        hi = x[p + 1:].cpu().numpy()
+        assert (lo <= np.array(pv, dtype=lo.dtype)).all() and (hi >= np.array(pv, dtype=hi.dtype)).all()
