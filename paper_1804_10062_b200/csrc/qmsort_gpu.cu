@@ -1113,13 +1113,14 @@ struct HostArena {
         if (st) cudaStreamDestroy(st);
     }
 };
-// The batch entry point's two workers use two process-wide arenas instead
-// (slot 0 / 1, one batch at a time), so worker threads can be short-lived
+constexpr int kBatchWorkers = 2;
+// The batch entry point's workers use process-wide arenas instead
+// (one per worker, one batch at a time), so worker threads can be short-lived
 // without allocating and freeing device memory on every call.
 static std::mutex g_batch_mu;
 static int host_arena(size_t need, unsigned char** base, cudaStream_t* st, int slot = -1) {
     static thread_local HostArena tl;
-    static HostArena batch[2];
+    static HostArena batch[kBatchWorkers];
     HostArena& ar = slot < 0 ? tl : batch[slot];
     if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
     if (ar.bytes < need) {
@@ -1233,27 +1234,36 @@ int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const 
     if (metrics) std::memset(metrics, 0, sizeof(*metrics));
     if (count == 0) return QMSORT_OK;
     std::lock_guard<std::mutex> batch_lock(g_batch_mu);
-    // Two workers (own stream + device arena each) take alternate arrays; the
-    // second starts once the first array's H2D is done, so from then on one
-    // array's D2H runs while the next array's H2D runs (one copy engine each
-    // way) and the sorts fill the gaps.
-    std::promise<void> first_in;
-    std::shared_future<void> first_in_done = first_in.get_future().share();
-    std::atomic<bool> signalled{false};
-    const std::function<void()> signal = [&]() {
-        if (!signalled.exchange(true)) first_in.set_value();
-    };
-    int rcs[2] = {QMSORT_OK, QMSORT_OK};
-    std::string errs[2];
-    qmsort_gpu_metrics ms[2];
+    // kBatchWorkers workers (own stream + device arena each) take arrays round
+    // robin.  Worker w starts once worker w-1's first H2D has landed, so the
+    // host-to-device engine streams one array after another while earlier
+    // arrays sort and come back on the device-to-host engine.
+    constexpr int W = kBatchWorkers;
+    std::promise<void> started[W];
+    std::shared_future<void> ready[W];
+    std::atomic<bool> signalled[W];
+    std::function<void()> signal[W];
+    for (int w = 0; w < W; ++w) {
+        ready[w] = started[w].get_future().share();
+        signalled[w] = false;
+        signal[w] = [&, w]() {
+            if (!signalled[w].exchange(true)) started[w].set_value();
+        };
+    }
+    int rcs[W];
+    std::string errs[W];
+    qmsort_gpu_metrics ms[W];
     std::memset(ms, 0, sizeof(ms));
     auto worker = [&](int w) {
-        if (w == 1) first_in_done.wait();
-        for (size_t i = (size_t)w; i < count; i += 2) {
+        rcs[w] = QMSORT_OK;
+        if (w > 0) ready[w - 1].wait();
+        bool first = true;
+        for (size_t i = (size_t)w; i < count; i += W) {
             qmsort_gpu_metrics m;
             const int rc = sort_host_one(dtype, cmp, h_arrays[i], ns[i], cfg, &m,
-                                         (w == 0 && i == 0) ? &signal : nullptr, w);
-            if (w == 0 && i == 0) signal();  // also on failure or n <= 1
+                                         first ? &signal[w] : nullptr, w);
+            if (first) signal[w]();  // also on failure or n <= 1
+            first = false;
             if (rc != QMSORT_OK) {
                 rcs[w] = rc;
                 errs[w] = g_err;
@@ -1266,20 +1276,23 @@ int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const 
             ms[w].max_depth = std::max(ms[w].max_depth, m.max_depth);
             ms[w].levels = std::max(ms[w].levels, m.levels);
         }
-        if (w == 0) signal();
+        signal[w]();
     };
-    std::thread t1(worker, 1);
+    std::vector<std::thread> ts;
+    for (int w = 1; w < W; ++w) ts.emplace_back(worker, w);
     worker(0);
-    t1.join();
-    for (int w = 0; w < 2; ++w)
+    for (auto& t : ts) t.join();
+    for (int w = 0; w < W; ++w)
         if (rcs[w] != QMSORT_OK) return fail(rcs[w], errs[w]);
     if (metrics) {
-        metrics->elapsed_ns = ms[0].elapsed_ns + ms[1].elapsed_ns;
-        metrics->alg_bytes = ms[0].alg_bytes + ms[1].alg_bytes;
-        metrics->kernel_launches = ms[0].kernel_launches + ms[1].kernel_launches;
-        metrics->host_syncs = ms[0].host_syncs + ms[1].host_syncs;
-        metrics->max_depth = std::max(ms[0].max_depth, ms[1].max_depth);
-        metrics->levels = std::max(ms[0].levels, ms[1].levels);
+        for (int w = 0; w < W; ++w) {
+            metrics->elapsed_ns += ms[w].elapsed_ns;
+            metrics->alg_bytes += ms[w].alg_bytes;
+            metrics->kernel_launches += ms[w].kernel_launches;
+            metrics->host_syncs += ms[w].host_syncs;
+            metrics->max_depth = std::max(metrics->max_depth, ms[w].max_depth);
+            metrics->levels = std::max(metrics->levels, ms[w].levels);
+        }
     }
     g_err.clear();
     return QMSORT_OK;
