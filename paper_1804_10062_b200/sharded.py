@@ -499,7 +499,11 @@ def bench_main(args: Any, metric: str, unit: str) -> None:
                            "l2": "input 1 GiB per GPU > L2"},
                 "gpu_launches": launches,
                 "roofline": {"bound": "hbm", "kernel": "whole per-GPU pipeline", "achieved": alg / (ms * 1e6),
-                             "peak": peak, "unit": "GB/s", "frac": alg / (ms * 1e6) / peak, "traffic": None},
+                             "peak": peak, "unit": "GB/s", "frac": alg / (ms * 1e6) / peak, "traffic": None,
+                             # SURVEY.md 8(d) sharded roofline: HBM leg + NVLink leg, serial phases
+                             "nvlink": {"bytes_per_rank": (P - 1) * n * 4 // P, "peak_GBps": 900.0,
+                                        "t_roof_ms": (alg / peak + (P - 1) * n * 4 / P / 900.0) / 1e6,
+                                        "frac_of_step": ((alg / peak + (P - 1) * n * 4 / P / 900.0) / 1e6) / ms}},
                 "e2e": {"value": n * P / (e2e_ms / 1e3) / 1e9, "unit": unit, "ms_per_step": e2e_ms,
                         "h2d_bytes_per_step": n * 4 * P, "d2h_bytes_per_step": n * 4 * P,
                         "api": "sharded.sort_sharded on pinned host shards (H2D + sort + D2H per rank)"},
