@@ -489,7 +489,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                                                             &c->work_count, src, tree[cur], sorted[cur],
                                                             lut[cur], hist));
             QLAUNCH(led, kPhPlan, 0,
-                    colsum_kernel<<<colsum_grid, 512, 0, st>>>(lv[cur].segs, hist, 0u, &c->nsegs));
+                    colsum_kernel<<<colsum_grid, 512, 0, st>>>(lv[cur].segs, hist, c));
             QLAUNCH(led, kPhPlan, 0,
                     plan_fn<<<plan_grid, 512, 0, st>>>(lv[cur].segs, hist, sorted[cur], lv[nxt], p, tasks,
                                                       fills, c, tot));
@@ -825,7 +825,7 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
         QLAUNCH(led, kPhCount, n * sizeof(K),
                 count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
                            st>>>(seg, chunks, nchunks, nullptr, &cnt->work_count, in, tree, sorted, lut, hist));
-        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<64, 512, 0, st>>>(seg, hist, 1u, nullptr));
+        QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<64, 512, 0, st>>>(seg, hist, nullptr));
         QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
     }
     if (!(parts & 2) || n == 0) return QMSORT_OK;

@@ -99,6 +99,7 @@ struct LevelCounters {
     uint32_t overflow;  // capacity exceeded somewhere (host reports an error)
     uint32_t work_count, work_scatter;  // dynamic chunk dispensers of this level's kernels
     uint32_t resplits;  // hybrid: children re-sampled with triple medians (f1)
+    uint32_t max_logk;  // largest log2 K among this level's segments
     unsigned long long nkeys;      // keys in this level's segments (pass ledger)
     unsigned long long task_keys;  // keys handed to the block sorter
     unsigned long long fill_keys;  // keys written by equal-bucket fills
@@ -157,6 +158,7 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
     const uint32_t hwords = (nch + 1) * (2u << logk);
     const uint32_t s = atomicAdd(&nb.cnt->nsegs, 1u);
+    atomicMax(&nb.cnt->max_logk, logk);
     const uint32_t sp = atomicAdd(&nb.cnt->nsplit, 1u << logk);
     const uint32_t c0 = atomicAdd(&nb.cnt->nchunks, nch);
     const uint32_t hb = atomicAdd(&nb.cnt->nhist, hwords);
@@ -506,13 +508,14 @@ __global__ void __launch_bounds__(T, 4) count_kernel(const SegDesc* __restrict__
 // K3a: per (segment, bin): exclusive prefix over the segment's chunks (in
 // place) and the bin total (entry nchunks).  One warp per bin.
 // ---------------------------------------------------------------------------
-// One warp per (segment, bin) pair, flattened over the level's segments (the
-// segment count is read on the device; null nsegs_dev = the host's nsegs).
+// One warp per (segment, bin) pair, flattened over the level's segments with
+// the level's largest bin count (segment count and largest K read on the
+// device; null cnt = one segment of up to 1024 bins).
 __global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__ segs,
-                                                     uint32_t* __restrict__ hist, uint32_t nsegs,
-                                                     const uint32_t* __restrict__ nsegs_dev) {
-    constexpr uint32_t NBMAX = 1024;  // 2 << LOG_KMAX for every key type
-    const uint32_t ns = nsegs_dev ? *nsegs_dev : nsegs;
+                                                     uint32_t* __restrict__ hist,
+                                                     const LevelCounters* __restrict__ cnt) {
+    const uint32_t ns = cnt ? cnt->nsegs : 1u;
+    const uint32_t NBMAX = cnt ? (2u << cnt->max_logk) : 1024u;  // bins incl. equality bins
     const int lane = threadIdx.x & 31;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t idx = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -819,7 +822,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
 }
 
 template <class K, int T, int U, int LOG_KMAX, bool PEER = false>
-__global__ void __launch_bounds__(T, 3) scatter_kernel(const SegDesc* __restrict__ segs,
+__global__ void __launch_bounds__(T, sizeof(K) >= 8 ? 2 : 3) scatter_kernel(const SegDesc* __restrict__ segs,
                                                     const ChunkDesc* __restrict__ chunks,
                                                     uint32_t nchunks, const uint32_t* __restrict__ nchunks_dev,
                                                     uint32_t* __restrict__ work,
