@@ -365,7 +365,7 @@ static int estimate_levels(uint64_t n, const PlanParams& p) {
     int lv = 0;
     uint64_t len = n;
     while (len > p.cap && lv < 16) {
-        const uint32_t k = choose_logk(len, p.target, p.log_kmax, p.slack);
+        const uint32_t k = choose_logk(len, p.target, p.log_kmax, p.cap);
         len = (len + (1ull << k) - 1) >> k;
         ++lv;
     }
@@ -418,7 +418,6 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     p.pivot = (uint32_t)std::max(0, cfg.pivot);
     const double dl = std::min(1.0, std::max(1.0 / 65536.0, cfg.delta > 0 ? cfg.delta : 1.0 / 16.0));
     p.delta_q16 = (uint32_t)(dl * 65536.0);
-    p.slack = (p.cap / p.target >= 4) ? 1u : 0u;
 
     LevelBufs lv[2];
     K* tree[2];

@@ -122,7 +122,6 @@ struct PlanParams {
     int dst_is_a;           // this level's scatter writes the caller's buffer
     uint32_t pivot;         // PivotStrategy (sort.hpp:19): 2 mom_of_thirds, 3 hybrid
     uint32_t delta_q16;     // SortConfig::delta in 1/65536 (hybrid skew band)
-    uint32_t slack;         // 1 if the last level may leave buckets of 2x target
 };
 
 __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
@@ -131,16 +130,20 @@ __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
     return r;
 }
 
-// Number of buckets for a segment of len keys: spread the remaining
-// log2(len/target) bits evenly over the fewest levels of at most 2^log_kmax.
-// When the block sorter's cap is 4x the target or more, the last level may
-// leave buckets of up to twice the target (one "slack" bit), which saves a
-// whole partition level for segments just above K_max * target.
+// Number of buckets for a segment of len keys.  A segment whose buckets would
+// average at most 3/4 of the block sorter's cap with the largest K is split
+// once (K = len / target rounded up to a power of two, at most K_max): the
+// last level then never leaves a sliver for a further level.  Larger segments
+// spread log2(len / target) bits evenly over the fewest levels of <= K_max,
+// where the last level may leave buckets of up to twice the target when the
+// cap allows it (one "slack" bit).
 __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, uint32_t log_kmax,
-                                                uint32_t slack = 0) {
+                                                uint32_t cap) {
     const uint64_t ratio = (len + target - 1) / target;
     uint32_t r = ceil_log2_u64(ratio);
     if (r < 1) r = 1;
+    if (len <= ((uint64_t)cap * 3 / 4) << log_kmax) return r < log_kmax ? r : log_kmax;
+    const uint32_t slack = cap / target >= 4 ? 1u : 0u;
     const uint32_t rs = r > slack ? r - slack : 1;
     const uint32_t levels = (rs + log_kmax - 1) / log_kmax;
     uint32_t k = (r + levels - 1) / levels;
@@ -154,7 +157,7 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
 __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len, uint64_t lo,
                                     uint64_t hi, const PlanParams& p, uint32_t sampler,
                                     bool write_chunks = true) {
-    const uint32_t logk = choose_logk(len, p.target, p.log_kmax, p.slack);
+    const uint32_t logk = choose_logk(len, p.target, p.log_kmax, p.cap);
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
     const uint32_t hwords = (nch + 1) * (2u << logk);
     const uint32_t s = atomicAdd(&nb.cnt->nsegs, 1u);
