@@ -83,7 +83,7 @@ struct Tune<uint32_t> {
     static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};  // block sort classes
     static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     static constexpr int ST = 512, SI = 16;  // sampler
-    static constexpr int XT = 256, XI = 16;  // scatter tile
+    static constexpr int XT = 512, XI = 16;  // scatter tile
     static constexpr int CT = 256, CU = 16;  // count
     static constexpr int MT = 512, MI = 16;  // merge pass
 };

@@ -825,7 +825,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
 }
 
 template <class K, int T, int U, int LOG_KMAX, bool PEER = false>
-__global__ void __launch_bounds__(T, sizeof(K) >= 8 ? 2 : 3) scatter_kernel(const SegDesc* __restrict__ segs,
+__global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >= 8 ? 2 : 3)) scatter_kernel(const SegDesc* __restrict__ segs,
                                                     const ChunkDesc* __restrict__ chunks,
                                                     uint32_t nchunks, const uint32_t* __restrict__ nchunks_dev,
                                                     uint32_t* __restrict__ work,
