@@ -209,6 +209,11 @@ struct BlockSorter {
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
 
+    // Lanes merged by the register-shuffle rounds before the shared-memory
+    // merge-path rounds take over (measured: all 32 for 4-byte keys; 8 for
+    // 8- and 32-byte keys, whose shuffles move 2 or 8 words per key).
+    static constexpr int kWarpLanes = sizeof(K) >= 8 ? 8 : 32;
+
     // Keys rounded up to whole threads: threads at or beyond mp / ITEMS own
     // no keys and only take part in the barriers.
     __device__ __forceinline__ static int padded(int m) { return (m + ITEMS - 1) / ITEMS * ITEMS; }
@@ -255,10 +260,10 @@ struct BlockSorter {
         if (warp_active) {
             register_sort<K, ITEMS>(k);
 #pragma unroll 1
-            for (int lr = 1; lr < 32 && lr * ITEMS < mp; lr <<= 1) warp_merge_round<K, ITEMS>(k, lr);
+            for (int lr = 1; lr < kWarpLanes && lr * ITEMS < mp; lr <<= 1) warp_merge_round<K, ITEMS>(k, lr);
         }
 #pragma unroll 1
-        for (int run = kWarpKeys; run < mp; run <<= 1) {
+        for (int run = kWarpLanes * ITEMS; run < mp; run <<= 1) {
             if (owner) store_blocked(k, s);
             __syncthreads();
             if (owner) {
