@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqmsort_gpu.so")
+LIB_PATH = os.environ.get("QMSORT_GPU_LIB") or os.path.join(_HERE, "libqmsort_gpu.so")
 
 QMSORT_OK = 0
 QMSORT_EINVAL = 1

@@ -212,7 +212,15 @@ struct BlockSorter {
     // Lanes merged by the register-shuffle rounds before the shared-memory
     // merge-path rounds take over (measured: all 32 for 4-byte keys; 8 for
     // 8- and 32-byte keys, whose shuffles move 2 or 8 words per key).
-    static constexpr int kWarpLanes = sizeof(K) >= 8 ? 8 : 32;
+#ifndef QMS_WARP_LANES_4B
+#define QMS_WARP_LANES_4B 32
+#endif
+#ifndef QMS_WINDOW_4B
+#define QMS_WINDOW_4B 0
+#endif
+    static constexpr int kWarpLanes = sizeof(K) >= 8 ? 8 : QMS_WARP_LANES_4B;
+    // merge-path rounds: bitonic window merge (no serial chain) or serial merge
+    static constexpr bool kWindow = sizeof(K) > 8 || (sizeof(K) == 4 && QMS_WINDOW_4B);
 
     // Keys rounded up to whole threads: threads at or beyond mp / ITEMS own
     // no keys and only take part in the barriers.
@@ -273,7 +281,7 @@ struct BlockSorter {
                 const int alen = min(run, mp - a0);
                 const int blen = max(0, min(run, mp - b0));
                 const int a = merge_path_smem<K>(s, a0, alen, b0, blen, diag);
-                if constexpr (sizeof(K) > 8) {  // records: the wide serial merge is select-heavy
+                if constexpr (kWindow) {  // records: the wide serial merge is select-heavy
                     const int a_end = merge_path_smem<K>(s, a0, alen, b0, blen, diag + ITEMS);
                     bitonic_merge_window<K, ITEMS>(s, a0 + a, a_end - a, b0 + diag - a, k);
                 } else {

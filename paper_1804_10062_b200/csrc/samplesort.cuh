@@ -786,9 +786,10 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         }
         if (lane == 31) sm.warp_sums[wid] = x;
         __syncthreads();
-        uint32_t excl = x - local;
-#pragma unroll
-        for (int w = 0; w < T / 32; ++w) excl += (w < (int)wid) ? sm.warp_sums[w] : 0u;
+        // earlier warps' totals: one load per lane and a warp reduction
+        // (not T/32 broadcast loads per thread)
+        const uint32_t ws = lane < wid ? sm.warp_sums[lane] : 0u;
+        uint32_t excl = x - local + __reduce_add_sync(0xffffffffu, ws);
         uint32_t z[BPT];
 #pragma unroll
         for (int i = 0; i < BPT; ++i) {
