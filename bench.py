@@ -331,8 +331,8 @@ def e2e(q, torch, n, pristine, cfg, args) -> dict:
     """Same metric through the host-array API: every step sorts its own pinned
     host copy of the input and H2D + sort + D2H of every step lie inside the
     timed region.  The steps go through qmsort_gpu_sort_host_batch (a stream of
-    independent sort requests): its two workers overlap one step's D2H with the
-    next step's H2D on the two PCIe copy engines.  The single-call latency of
+    independent sort requests): a ring of three device arenas keeps both PCIe
+    copy engines busy (step i+1 in, step i sorting, step i-1 out).  The single-call latency of
     qmsort_gpu_sort_host is reported alongside (sync_ms_per_step)."""
     host_src = pristine.cpu()
     steps = max(2, min(args.steps, 6))
@@ -342,7 +342,7 @@ def e2e(q, torch, n, pristine, cfg, args) -> dict:
     warm = [torch.empty(n, dtype=torch.uint32, pin_memory=True) for _ in range(2)]
     for w in warm:
         w.copy_(host_src)
-    q.sort_batch(warm, cfg)  # warms both workers' device arenas
+    q.sort_batch(warm, cfg)  # allocates the batch arenas
     t = time.perf_counter()
     q.sort_batch(bufs, cfg)
     ms = (time.perf_counter() - t) / steps * 1e3

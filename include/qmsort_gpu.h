@@ -124,9 +124,10 @@ int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsor
 
 /* A stream of independent host arrays (e.g. the trials of a harness, or
  * request batches of a service): the same contract as qmsort_gpu_sort_host for
- * every h_arrays[i] of ns[i] elements, pipelined over two workers with their
- * own device arenas so that one array's device-to-host copy overlaps the next
- * array's host-to-device copy.  Pinned host memory gives the overlap.  metrics
+ * every h_arrays[i] of ns[i] elements, pipelined through a ring of three
+ * device arenas: array i+1 is copied in while array i sorts and array i-1 is
+ * copied back, so both PCIe directions stay busy.  Pinned host memory gives
+ * the overlap.  metrics
  * (optional) holds the sums (elapsed_ns: device sort time of all arrays). */
 int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const size_t* ns,
                                size_t count, const qmsort_gpu_config* cfg,

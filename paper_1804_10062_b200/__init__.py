@@ -259,9 +259,9 @@ def sort(data: Any, cfg: SortConfig | None = None, less: Any = "less", *, worksp
 def sort_batch(arrays: list, cfg: SortConfig | None = None, less: Any = "less", *,
                dtype: int | None = None) -> Metrics:
     """Sort a list of independent host arrays (numpy / CPU tensors, ideally
-    pinned) in place through ``qmsort_gpu_sort_host_batch``: one array's
-    device-to-host copy overlaps the next one's host-to-device copy.  Returns
-    summed Metrics."""
+    pinned) in place through ``qmsort_gpu_sort_host_batch``: a ring of three
+    device arenas overlaps array i+1's host-to-device copy, array i's sort and
+    array i-1's device-to-host copy.  Returns summed Metrics."""
     lib = _lib.load()
     c = (cfg or SortConfig()).to_c()
     m = _lib.GpuMetrics()

@@ -20,11 +20,8 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
-#include <functional>
-#include <future>
 #include <mutex>
 #include <string>
-#include <thread>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -1112,15 +1109,37 @@ struct HostArena {
         if (st) cudaStreamDestroy(st);
     }
 };
-constexpr int kBatchWorkers = 2;
-// The batch entry point's workers use process-wide arenas instead
-// (one per worker, one batch at a time), so worker threads can be short-lived
-// without allocating and freeing device memory on every call.
+// Process-wide state of the batch entry point (one batch at a time, under
+// g_batch_mu): a ring of device arenas with their compute streams, one stream
+// per copy direction and the events that order them.
+constexpr int kBatchArenas = 3;
 static std::mutex g_batch_mu;
-static int host_arena(size_t need, unsigned char** base, cudaStream_t* st, int slot = -1) {
+struct BatchPipe {
+    HostArena ar[kBatchArenas];
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t h2d_done[kBatchArenas] = {}, sort_done[kBatchArenas] = {}, d2h_done[kBatchArenas] = {};
+    int init(size_t need) {
+        if (!h2d) QCK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+        if (!d2h) QCK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        for (int a = 0; a < kBatchArenas; ++a) {
+            if (!ar[a].st) QCK(cudaStreamCreateWithFlags(&ar[a].st, cudaStreamNonBlocking));
+            if (ar[a].bytes < need) {
+                if (ar[a].buf) QCK(cudaFree(ar[a].buf));
+                ar[a].buf = nullptr;
+                ar[a].bytes = 0;
+                QCK(cudaMalloc(&ar[a].buf, need));
+                ar[a].bytes = need;
+            }
+            for (cudaEvent_t* e : {&h2d_done[a], &sort_done[a], &d2h_done[a]})
+                if (!*e) QCK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+        return QMSORT_OK;
+    }
+};
+static BatchPipe g_batch_pipe;
+static int host_arena(size_t need, unsigned char** base, cudaStream_t* st) {
     static thread_local HostArena tl;
-    static HostArena batch[kBatchWorkers];
-    HostArena& ar = slot < 0 ? tl : batch[slot];
+    HostArena& ar = tl;
     if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
     if (ar.bytes < need) {
         if (ar.buf) QCK(cudaFree(ar.buf));
@@ -1135,10 +1154,8 @@ static int host_arena(size_t need, unsigned char** base, cudaStream_t* st, int s
 }
 
 // Host-array sort through the calling thread's arena: H2D, sort, D2H.
-// after_h2d (optional) runs once the input has landed on the device.
 static int sort_host_one(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
-                         qmsort_gpu_metrics* metrics, const std::function<void()>* after_h2d,
-                         int slot = -1) {
+                         qmsort_gpu_metrics* metrics) {
     QTRY(validate(dtype, cmp, n, h_data));
     if (n <= 1) {
         if (metrics) std::memset(metrics, 0, sizeof(*metrics));
@@ -1148,12 +1165,8 @@ static int sort_host_one(int dtype, int cmp, void* h_data, size_t n, const qmsor
     const size_t need = data_bytes + ws_bytes_for(dtype, n);
     unsigned char* base = nullptr;
     cudaStream_t st = nullptr;
-    QTRY(host_arena(need, &base, &st, slot));
+    QTRY(host_arena(need, &base, &st));
     QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, st));
-    if (after_h2d) {
-        QCK(cudaStreamSynchronize(st));
-        (*after_h2d)();
-    }
     int rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, need - data_bytes, metrics, st);
     if (rc != QMSORT_OK) return rc;
     QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, st));
@@ -1221,7 +1234,7 @@ int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu
 
 int qmsort_gpu_sort_host(int dtype, int cmp, void* h_data, size_t n, const qmsort_gpu_config* cfg,
                          qmsort_gpu_metrics* metrics) {
-    return sort_host_one(dtype, cmp, h_data, n, cfg, metrics, nullptr);
+    return sort_host_one(dtype, cmp, h_data, n, cfg, metrics);
 }
 
 int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const size_t* ns,
@@ -1231,68 +1244,64 @@ int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const 
         return fail(QMSORT_EINVAL, "null array list");
     for (size_t i = 0; i < count; ++i) QTRY(validate(dtype, cmp, ns[i], h_arrays[i]));
     if (metrics) std::memset(metrics, 0, sizeof(*metrics));
-    if (count == 0) return QMSORT_OK;
+    std::vector<size_t> todo;  // arrays with something to sort
+    size_t need = 0;
+    for (size_t i = 0; i < count; ++i) {
+        if (ns[i] <= 1) continue;
+        todo.push_back(i);
+        need = std::max(need, align_up(ns[i] * dtype_size(dtype), 256) + ws_bytes_for(dtype, ns[i]));
+    }
+    if (todo.empty()) return QMSORT_OK;
     std::lock_guard<std::mutex> batch_lock(g_batch_mu);
-    // kBatchWorkers workers (own stream + device arena each) take arrays round
-    // robin.  Worker w starts once worker w-1's first H2D has landed, so the
-    // host-to-device engine streams one array after another while earlier
-    // arrays sort and come back on the device-to-host engine.
-    constexpr int W = kBatchWorkers;
-    std::promise<void> started[W];
-    std::shared_future<void> ready[W];
-    std::atomic<bool> signalled[W];
-    std::function<void()> signal[W];
-    for (int w = 0; w < W; ++w) {
-        ready[w] = started[w].get_future().share();
-        signalled[w] = false;
-        signal[w] = [&, w]() {
-            if (!signalled[w].exchange(true)) started[w].set_value();
-        };
-    }
-    int rcs[W];
-    std::string errs[W];
-    qmsort_gpu_metrics ms[W];
-    std::memset(ms, 0, sizeof(ms));
-    auto worker = [&](int w) {
-        rcs[w] = QMSORT_OK;
-        if (w > 0) ready[w - 1].wait();
-        bool first = true;
-        for (size_t i = (size_t)w; i < count; i += W) {
-            qmsort_gpu_metrics m;
-            const int rc = sort_host_one(dtype, cmp, h_arrays[i], ns[i], cfg, &m,
-                                         first ? &signal[w] : nullptr, w);
-            if (first) signal[w]();  // also on failure or n <= 1
-            first = false;
-            if (rc != QMSORT_OK) {
-                rcs[w] = rc;
-                errs[w] = g_err;
-                break;
-            }
-            ms[w].elapsed_ns += m.elapsed_ns;
-            ms[w].alg_bytes += m.alg_bytes;
-            ms[w].kernel_launches += m.kernel_launches;
-            ms[w].host_syncs += m.host_syncs;
-            ms[w].max_depth = std::max(ms[w].max_depth, m.max_depth);
-            ms[w].levels = std::max(ms[w].levels, m.levels);
-        }
-        signal[w]();
+    // One host thread, three device arenas in a ring, one stream per copy
+    // direction: the host-to-device engine streams array j+1 while array j
+    // sorts (its compute stream waits on an event) and array j-1 returns on
+    // the device-to-host engine.  Array j+1 reuses the arena of array j-2 once
+    // that array's copy back has completed (an event, not a host wait).  The
+    // host blocks only inside each sort (its control read) and at the end.
+    constexpr int A = kBatchArenas;
+    BatchPipe& bp = g_batch_pipe;
+    QTRY(bp.init(need));
+    const size_t m = todo.size();
+    auto bytes_of = [&](size_t j) { return ns[todo[j]] * dtype_size(dtype); };
+    auto h2d = [&](size_t j) -> int {
+        const int a = (int)(j % A);
+        if (j >= (size_t)A) QCK(cudaStreamWaitEvent(bp.h2d, bp.d2h_done[a], 0));
+        QCK(cudaMemcpyAsync(bp.ar[a].buf, h_arrays[todo[j]], bytes_of(j), cudaMemcpyHostToDevice, bp.h2d));
+        QCK(cudaEventRecord(bp.h2d_done[a], bp.h2d));
+        return QMSORT_OK;
     };
-    std::vector<std::thread> ts;
-    for (int w = 1; w < W; ++w) ts.emplace_back(worker, w);
-    worker(0);
-    for (auto& t : ts) t.join();
-    for (int w = 0; w < W; ++w)
-        if (rcs[w] != QMSORT_OK) return fail(rcs[w], errs[w]);
-    if (metrics) {
-        for (int w = 0; w < W; ++w) {
-            metrics->elapsed_ns += ms[w].elapsed_ns;
-            metrics->alg_bytes += ms[w].alg_bytes;
-            metrics->kernel_launches += ms[w].kernel_launches;
-            metrics->host_syncs += ms[w].host_syncs;
-            metrics->max_depth = std::max(metrics->max_depth, ms[w].max_depth);
-            metrics->levels = std::max(metrics->levels, ms[w].levels);
+    int rc = h2d(0);
+    for (size_t j = 0; j < m && rc == QMSORT_OK; ++j) {
+        if (j + 1 < m && (rc = h2d(j + 1)) != QMSORT_OK) break;
+        const int a = (int)(j % A);
+        const size_t n = ns[todo[j]];
+        unsigned char* base = static_cast<unsigned char*>(bp.ar[a].buf);
+        const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
+        QCK(cudaStreamWaitEvent(bp.ar[a].st, bp.h2d_done[a], 0));
+        qmsort_gpu_metrics mj;
+        rc = sort_device(dtype, cmp, base, n, cfg, base + data_bytes, bp.ar[a].bytes - data_bytes, &mj,
+                         bp.ar[a].st);
+        if (rc != QMSORT_OK) break;
+        QCK(cudaEventRecord(bp.sort_done[a], bp.ar[a].st));
+        QCK(cudaStreamWaitEvent(bp.d2h, bp.sort_done[a], 0));
+        QCK(cudaMemcpyAsync(h_arrays[todo[j]], base, bytes_of(j), cudaMemcpyDeviceToHost, bp.d2h));
+        QCK(cudaEventRecord(bp.d2h_done[a], bp.d2h));
+        if (metrics) {
+            metrics->elapsed_ns += mj.elapsed_ns;
+            metrics->alg_bytes += mj.alg_bytes;
+            metrics->kernel_launches += mj.kernel_launches;
+            metrics->host_syncs += mj.host_syncs;
+            metrics->max_depth = std::max(metrics->max_depth, mj.max_depth);
+            metrics->levels = std::max(metrics->levels, mj.levels);
         }
     }
+    // drain both copy streams whatever happened (no copy may outlive the call)
+    const cudaError_t e1 = cudaStreamSynchronize(bp.h2d);
+    const cudaError_t e2 = cudaStreamSynchronize(bp.d2h);
+    if (rc != QMSORT_OK) return rc;
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+        return fail(QMSORT_ECUDA, std::string("batch copies: ") + cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
     g_err.clear();
     return QMSORT_OK;
 }
