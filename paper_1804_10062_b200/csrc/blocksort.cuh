@@ -205,7 +205,13 @@ struct BlockSorter {
     static constexpr int kItems = ITEMS;
     static constexpr int kCap = T * ITEMS;
     static constexpr int kSmemElems = SmemPad<K>::elems(kCap);
-    static constexpr size_t kSmemBytes = sizeof(K) * kSmemElems;
+    // records (Rec32) first try the prefix path: the tile unpadded plus a
+    // padded array of 64-bit (prefix | index) keys
+    static constexpr bool kPrefixPath = std::is_same<K, Rec32>::value && kCap <= 4096;
+    static constexpr size_t kPrefixSmemBytes =
+        kPrefixPath ? (size_t)kCap * sizeof(K) + sizeof(uint64_t) * SmemPad<uint64_t>::elems(kCap) : 0;
+    static constexpr size_t kSmemBytes =
+        sizeof(K) * kSmemElems > kPrefixSmemBytes ? sizeof(K) * kSmemElems : kPrefixSmemBytes;
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
 
@@ -294,8 +300,79 @@ struct BlockSorter {
         __syncthreads();
     }
 
+    // Records: sort 64-bit keys (p & ~0xFFF) | i instead of the records, where
+    // p is the top 64 bits of the (w0 - min w0, w1) pair over the tile -- a
+    // monotone map of the lexicographic order -- and i the record's index in
+    // the tile.  If no two keys share their top 52 bits the key order is the
+    // record order, and one gather from shared memory writes the sorted tile;
+    // otherwise (ties in the prefix) returns false with nothing written and
+    // the caller sorts the records themselves.  The uint64 sorter's compare-
+    // and-swaps are a few instructions where a record's is ~30.
+    __device__ static bool sort_tile_prefix(const K* src, K* dst, int m, K* s) {
+        using B64 = BlockSorter<uint64_t, T, ITEMS>;
+        using P8 = SmemPad<uint64_t>;
+        __shared__ unsigned long long red_lo[T / 32], red_hi[T / 32];
+        K* rec = s;
+        uint64_t* s64 = reinterpret_cast<uint64_t*>(s + kCap);
+        const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+        uint64_t w0[ITEMS], w1[ITEMS];
+        unsigned long long lo = ~0ull, hi = 0;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const int i = j * T + tid;
+            w0[j] = w1[j] = 0;
+            if (i < m) {
+                const K r = src[i];
+                rec[i] = r;
+                w0[j] = r.w[0];
+                w1[j] = r.w[1];
+                lo = min(lo, (unsigned long long)r.w[0]);
+                hi = max(hi, (unsigned long long)r.w[0]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            red_lo[wid] = lo;
+            red_hi[wid] = hi;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < T / 32; ++w) {
+            lo = min(lo, red_lo[w]);
+            hi = max(hi, red_hi[w]);
+        }
+        const uint64_t span = hi - lo;
+        const int sh = span ? __clzll((long long)span) : 64;  // w1 bits in the prefix
+        const int mw = B64::warp_padded(m);
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            const int i = j * T + tid;
+            const uint64_t d = w0[j] - lo;
+            const uint64_t p = sh == 64 ? w1[j] : sh == 0 ? d : (d << sh) | (w1[j] >> (64 - sh));
+            if (i < mw) s64[P8::idx(i)] = i < m ? (p & ~0xFFFull) | (uint64_t)i : ~0ull;
+        }
+        __syncthreads();
+        uint64_t k[ITEMS];
+        if (tid * ITEMS < mw) B64::load_blocked(k, s64);
+        __syncthreads();
+        B64::sort(k, s64, m);
+        int tie = 0;
+        for (int i = tid; i + 1 < m; i += T)
+            tie |= ((s64[P8::idx(i)] ^ s64[P8::idx(i + 1)]) >> 12) == 0 ? 1 : 0;
+        if (__syncthreads_or(tie)) return false;
+        for (int i = tid; i < m; i += T) dst[i] = rec[s64[P8::idx(i)] & 0xFFFull];
+        return true;
+    }
+
     // Whole tile: global src (m keys) -> sorted -> global dst.  src may alias dst.
     __device__ __forceinline__ static void sort_tile(const K* src, K* dst, int m, K* s) {
+        if constexpr (kPrefixPath) {
+            if (m > 1 && sort_tile_prefix(src, dst, m, s)) return;
+        }
         load_striped(src, m, s);
         __syncthreads();
         K k[ITEMS];

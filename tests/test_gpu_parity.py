@@ -186,3 +186,32 @@ def test_host_batch_pipeline(oracle, dt):
     q.sort_batch(pins, less="greater")
     for p, a in zip(pins, arrays[2:5]):
         np.testing.assert_array_equal(p.numpy(), oracle.sort(dt, a, greater=True))
+
+
+@pytest.mark.parametrize("case", ["w1_const", "w1_low_bits", "w0_wide", "w0_span2", "mixed"])
+@pytest.mark.parametrize("n", [3000, 200000])
+def test_rec32_prefix_ties(oracle, case, n):
+    """Record block sort: the (prefix | index) fast path must hand every tile
+    whose 52-bit prefixes tie to the full-record sorter -- records equal in
+    w0/w1 (or in w1's top bits) that differ only in later words, a w0 range
+    wider than 64 bits of prefix, two w0 values per tile, and a mix."""
+    rng = np.random.default_rng(n + len(case))
+    r = rng.integers(0, 2**63, size=(n, 4), dtype=np.uint64)
+    if case == "w1_const":
+        r[:, 0] = rng.integers(0, 3, size=n, dtype=np.uint64)
+        r[:, 1] = np.uint64(0xDEADBEEF)
+    elif case == "w1_low_bits":
+        r[:, 0] >>= np.uint64(60)
+        r[:, 1] = (r[:, 1] >> np.uint64(52) << np.uint64(52)) | rng.integers(0, 4096, size=n, dtype=np.uint64)
+        r[:, 1] &= np.uint64(0xFFF00000000FFFFF)
+    elif case == "w0_wide":
+        r[:, 0] = r[:, 0] * np.uint64(2) + np.uint64(1)
+    elif case == "w0_span2":
+        r[:, 0] = rng.integers(7, 9, size=n, dtype=np.uint64)
+    else:
+        r[:, 0] >>= np.uint64(58)
+        r[: n // 2, 1] = np.uint64(5)
+    got, _ = gpu_sort(r)
+    np.testing.assert_array_equal(got, oracle.sort(DT_REC32, r))
+    got, _ = gpu_sort(r, less="greater")
+    np.testing.assert_array_equal(got, oracle.sort(DT_REC32, r, greater=True))
