@@ -7,6 +7,9 @@
 // bucket that fits one CTA is sorted entirely on chip:
 //   1. each thread sorts ITEMS keys in registers with Batcher's odd-even merge
 //      network (compile-time unrolled, no local memory);
+//      uint32 tiles whose keys span fewer than 2^16 - 1 values take this and
+//      the warp rounds with two 16-bit keys per register (key - min, U16x2:
+//      VIMNMX.U16x2 compare-and-swaps, one shuffle per two keys);
 //   2. log2(T) merge-path rounds in shared memory double the run length; each
 //      thread locates its output diagonal by binary search (merge path) and
 //      merges ITEMS outputs serially -- the same "take run1 on ties" rule as
@@ -135,6 +138,35 @@ __device__ __forceinline__ K select_minmax(const K& a, const K& b, bool lower) {
     return (b_less == lower) ? b : a;
 }
 
+// Two 16-bit keys in one register: the halves are two independent sequences
+// that every network step below treats alike (SIMD within a register).  A
+// compare-and-swap is one VIMNMX.U16x2 plus the two-IMAD maximum (the halves'
+// a + b - min cannot carry: each half's result is that half's maximum), a
+// shuffle moves two keys.  Used by the block sorter for tiles whose keys span
+// at most 2^16 values (keys stored as key - min).
+struct U16x2 {
+    uint32_t v;
+};
+template <>
+struct KeyTraits<U16x2> {
+    __device__ __forceinline__ static void cas_alt(U16x2& a, U16x2& b) {
+        const uint32_t lo = __vminu2(a.v, b.v);
+        const uint32_t t = lo * c_neg1 + a.v;
+        b.v = t * c_one + b.v;
+        a.v = lo;
+    }
+    __device__ __forceinline__ static U16x2 shfl_xor(U16x2 a, int m) {
+        return U16x2{__shfl_xor_sync(0xffffffffu, a.v, m)};
+    }
+};
+// Both halves' min and max, then one LOP3 picks per lane (a branch-free
+// select; `lower ? vmin : vmax` compiles to predicated moves).
+__device__ __forceinline__ U16x2 select_minmax(const U16x2& a, const U16x2& b, bool lower) {
+    const uint32_t msk = 0u - (uint32_t)lower;
+    const uint32_t mn = __vminu2(a.v, b.v), mx = __vmaxu2(a.v, b.v);
+    return U16x2{(mn & msk) | (mx & ~msk)};
+}
+
 // One warp-level merge round: every pair of ascending runs of `lr` lanes x
 // ITEMS keys (lane-blocked) becomes one ascending run of 2*lr lanes.  Bitonic
 // merge in its all-ascending form: a flip stage pairs position p with its
@@ -218,15 +250,11 @@ struct BlockSorter {
     // Lanes merged by the register-shuffle rounds before the shared-memory
     // merge-path rounds take over (measured: all 32 for 4-byte keys; 8 for
     // 8- and 32-byte keys, whose shuffles move 2 or 8 words per key).
-#ifndef QMS_WARP_LANES_4B
-#define QMS_WARP_LANES_4B 32
-#endif
-#ifndef QMS_WINDOW_4B
-#define QMS_WINDOW_4B 0
-#endif
-    static constexpr int kWarpLanes = sizeof(K) >= 8 ? 8 : QMS_WARP_LANES_4B;
-    // merge-path rounds: bitonic window merge (no serial chain) or serial merge
-    static constexpr bool kWindow = sizeof(K) > 8 || (sizeof(K) == 4 && QMS_WINDOW_4B);
+    static constexpr int kWarpLanes = sizeof(K) >= 8 ? 8 : 32;
+    // merge-path rounds: bitonic window merge (no serial chain) for records,
+    // serial merge otherwise (measured: the window merge is not faster for
+    // 4-byte keys)
+    static constexpr bool kWindow = sizeof(K) > 8;
 
     // Keys rounded up to whole threads: threads at or beyond mp / ITEMS own
     // no keys and only take part in the barriers.
@@ -267,8 +295,6 @@ struct BlockSorter {
     // be called by all T threads; s must not be in use.
     __device__ __forceinline__ static void sort(K (&k)[ITEMS], K* s, int m) {
         const int mp = padded(m);
-        const int out = threadIdx.x * ITEMS;
-        const bool owner = out < mp;
         // warps holding any key (their other lanes hold maximum-key padding)
         const bool warp_active = (int)(threadIdx.x & ~31u) * ITEMS < mp;
         if (warp_active) {
@@ -276,9 +302,20 @@ struct BlockSorter {
 #pragma unroll 1
             for (int lr = 1; lr < kWarpLanes && lr * ITEMS < mp; lr <<= 1) warp_merge_round<K, ITEMS>(k, lr);
         }
+        merge_rounds(k, s, m, kWarpLanes * ITEMS, false);
+    }
+
+    // Merge-path rounds in shared memory from sorted runs of run0 keys up to
+    // the whole tile; the result is left in s.  in_smem: the runs are already
+    // in s (padded indexing) rather than in the threads' registers.
+    __device__ __forceinline__ static void merge_rounds(K (&k)[ITEMS], K* s, int m, int run0, bool in_smem) {
+        const int mp = padded(m);
+        const int out = threadIdx.x * ITEMS;
+        const bool owner = out < mp;
 #pragma unroll 1
-        for (int run = kWarpLanes * ITEMS; run < mp; run <<= 1) {
-            if (owner) store_blocked(k, s);
+        for (int run = run0; run < mp; run <<= 1) {
+            if (owner && !in_smem) store_blocked(k, s);
+            in_smem = false;
             __syncthreads();
             if (owner) {
                 const int pair = out & ~(2 * run - 1);
@@ -296,7 +333,7 @@ struct BlockSorter {
             }
             __syncthreads();
         }
-        if (owner) store_blocked(k, s);
+        if (owner && !in_smem) store_blocked(k, s);
         __syncthreads();
     }
 
@@ -368,12 +405,110 @@ struct BlockSorter {
         return true;
     }
 
+    // uint32 tiles whose keys span < 2^16 - 1 values: the key - min values are
+    // sorted two per register (U16x2) through the register network and the
+    // warp rounds -- about half the instructions per key -- then unpacked into
+    // shared memory for the merge-path rounds.  Warp w's 1024 keys: register
+    // j of lane l holds positions w*1024 + l*16 + j (low half) and the same
+    // + 512 (high half).  Each half is sorted as a 512-key warp run, then one
+    // cross-half round (flip stage: low position p against high position
+    // 511 - p, then the half-cleaners of both halves) leaves the low halves
+    // holding the warp's 512 smallest keys in order and the high halves the
+    // rest: a sorted run of 1024, as the unpacked warp stage produces.
+    static constexpr bool kPackedPath = std::is_same<K, uint32_t>::value && ITEMS == 32;
+    static constexpr int kPI = ITEMS / 2;  // packed registers per lane
+    __device__ __forceinline__ static void cross_half_round(U16x2 (&pk)[kPI]) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int j = 0; j < kPI / 2; ++j) {
+            const int jj = kPI - 1 - j;
+            const uint32_t y0 = __shfl_xor_sync(0xffffffffu, pk[jj].v, 31);
+            const uint32_t y1 = __shfl_xor_sync(0xffffffffu, pk[j].v, 31);
+            const uint32_t s0 = __byte_perm(y0, 0, 0x1032), s1 = __byte_perm(y1, 0, 0x1032);  // swap halves
+            pk[j].v = (__vminu2(pk[j].v, s0) & 0xFFFFu) | (__vmaxu2(pk[j].v, s0) & 0xFFFF0000u);
+            pk[jj].v = (__vminu2(pk[jj].v, s1) & 0xFFFFu) | (__vmaxu2(pk[jj].v, s1) & 0xFFFF0000u);
+        }
+#pragma unroll
+        for (int sd = 16; sd >= 1; sd >>= 1) {
+            const bool lower = (lane & sd) == 0;
+#pragma unroll
+            for (int j = 0; j < kPI; ++j) pk[j] = select_minmax(pk[j], KeyTraits<U16x2>::shfl_xor(pk[j], sd), lower);
+        }
+#pragma unroll
+        for (int sd = kPI / 2; sd >= 1; sd >>= 1) {
+#pragma unroll
+            for (int j = 0; j < kPI; ++j)
+                if ((j & sd) == 0) net_cas<U16x2>(pk[j], pk[j + sd], j + sd);
+        }
+    }
+    __device__ __forceinline__ static void sort_tile_packed(K* s, int m, uint32_t lo) {
+        const int tid = threadIdx.x;
+        const int base = (int)(tid & ~31u) * ITEMS + (tid & 31) * kPI;
+        if ((int)(tid & ~31u) * ITEMS < m) {  // warps holding keys
+            U16x2 pk[kPI];
+#pragma unroll
+            for (int j = 0; j < kPI; ++j) {
+                const int p0 = base + j, p1 = p0 + 32 * kPI;
+                const uint32_t k0 = p0 < m ? s[P::idx(p0)] - lo : 0xFFFFu;
+                const uint32_t k1 = p1 < m ? s[P::idx(p1)] - lo : 0xFFFFu;
+                pk[j].v = k0 | (k1 << 16);
+            }
+            register_sort<U16x2, kPI>(pk);
+#pragma unroll 1
+            for (int lr = 1; lr < 32; lr <<= 1) warp_merge_round<U16x2, kPI>(pk, lr);
+            cross_half_round(pk);
+            // each warp reads and writes only its own 1024 positions
+#pragma unroll
+            for (int j = 0; j < kPI; ++j) {
+                const int p0 = base + j;
+                const uint32_t v0 = pk[j].v & 0xFFFFu, v1 = pk[j].v >> 16;
+                s[P::idx(p0)] = v0 == 0xFFFFu ? KT::max_key() : v0 + lo;  // 0xFFFF: padding only
+                s[P::idx(p0 + 32 * kPI)] = v1 == 0xFFFFu ? KT::max_key() : v1 + lo;
+            }
+        }
+        K k[ITEMS];
+        merge_rounds(k, s, m, 32 * ITEMS, true);
+    }
+
     // Whole tile: global src (m keys) -> sorted -> global dst.  src may alias dst.
     __device__ __forceinline__ static void sort_tile(const K* src, K* dst, int m, K* s) {
         if constexpr (kPrefixPath) {
             if (m > 1 && sort_tile_prefix(src, dst, m, s)) return;
         }
-        load_striped(src, m, s);
+        if constexpr (kPackedPath) {
+            // striped load with the tile's key range
+            __shared__ uint32_t red_lo[T / 32], red_hi[T / 32];
+            const int mw = warp_padded(m);
+            uint32_t lo = 0xFFFFFFFFu, hi = 0;
+#pragma unroll 4
+            for (int i = threadIdx.x; i < mw; i += T) {
+                const K x = i < m ? src[i] : KT::max_key();
+                s[P::idx(i)] = x;
+                if (i < m) {
+                    lo = min(lo, x);
+                    hi = max(hi, x);
+                }
+            }
+            lo = __reduce_min_sync(0xffffffffu, lo);
+            hi = __reduce_max_sync(0xffffffffu, hi);
+            if ((threadIdx.x & 31) == 0) {
+                red_lo[threadIdx.x >> 5] = lo;
+                red_hi[threadIdx.x >> 5] = hi;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int w = 0; w < T / 32; ++w) {
+                lo = min(lo, red_lo[w]);
+                hi = max(hi, red_hi[w]);
+            }
+            if (m > 1 && hi - lo < 0xFFFFu) {  // 0xFFFF is reserved for padding
+                sort_tile_packed(s, m, lo);
+                store_striped(dst, m, s);
+                return;
+            }
+        } else {
+            load_striped(src, m, s);
+        }
         __syncthreads();
         K k[ITEMS];
         if ((int)threadIdx.x * ITEMS < warp_padded(m)) load_blocked(k, s);

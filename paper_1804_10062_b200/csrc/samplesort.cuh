@@ -917,7 +917,9 @@ __global__ void fill_kernel(const FillTask* __restrict__ fills, const uint32_t* 
 // Block-sort every task of one size class into A (from A or B, at the same
 // offsets): one CTA per task (launched with the sort's task count).
 template <class K, int T, int ITEMS>
-__global__ void __launch_bounds__(T) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
+// 4-byte keys: registers budgeted for 1024 / T resident CTAs (64 per
+// thread), which the packed 16-bit path otherwise exceeds.
+__global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1024 / T : 1) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
                                                             const K* B) {
     using BS = BlockSorter<K, T, ITEMS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];

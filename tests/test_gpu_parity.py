@@ -215,3 +215,21 @@ def test_rec32_prefix_ties(oracle, case, n):
     np.testing.assert_array_equal(got, oracle.sort(DT_REC32, r))
     got, _ = gpu_sort(r, less="greater")
     np.testing.assert_array_equal(got, oracle.sort(DT_REC32, r, greater=True))
+
+
+@pytest.mark.parametrize("base", [0, 12345, (1 << 32) - 65535, (1 << 32) - 70000, (1 << 32) - 1 - 65534])
+@pytest.mark.parametrize("span", [1, 2, 1000, 65533, 65534, 65535, 65536])
+@pytest.mark.parametrize("n", [2, 1000, 1024, 1025, 2048, 3000, 4096, 9000, 16384, 300000])
+def test_u32_packed_spans(oracle, base, span, n):
+    """uint32 block sort: tiles whose keys span < 2^16 - 1 values are sorted
+    two keys per register -- spans at and around the limit, keys touching 0
+    and 2^32 - 1 (the padding must stay above every real key), both orders."""
+    rng = np.random.default_rng(n * 7 + span)
+    hi = min((1 << 32) - 1, base + span - 1)
+    a = rng.integers(base, hi + 1, size=n, dtype=np.uint64).astype(np.uint32)
+    if n > 2:
+        a[0], a[1] = base, hi  # the full span is present
+    got, _ = gpu_sort(a)
+    np.testing.assert_array_equal(got, np.sort(a))
+    got, _ = gpu_sort(a, less="greater")
+    np.testing.assert_array_equal(got, np.sort(a)[::-1])
