@@ -291,7 +291,8 @@ static WsLayout make_layout(size_t n) {
     L.chunk_elems = ch;
     L.seg_cap = (uint32_t)(n / cap + 2);
     L.chunk_cap = (uint32_t)(L.seg_cap + n / ch + 2);
-    L.split_cap = (uint32_t)(2 * n / target + 2 * (uint64_t)L.seg_cap + 2 * (1u << TU::LOGKMAX) + 64);
+    const uint64_t last_target = target * kLastNum / kLastDen;  // choose_logk's last level
+    L.split_cap = (uint32_t)(2 * n / last_target + 2 * (uint64_t)L.seg_cap + 2 * (1u << TU::LOGKMAX) + 64);
     L.task_cap = 4 * L.split_cap + 64;  // per class, all levels of one sort
     L.fill_cap = L.split_cap;
     L.hist_cap = (uint32_t)(2ull * (1u << TU::LOGKMAX) * (n / ch + 2) + 2ull * L.split_cap);

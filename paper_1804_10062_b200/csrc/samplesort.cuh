@@ -130,9 +130,13 @@ __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
     return r;
 }
 
+// Last-level bucket target = 3/4 of the level target: smaller final buckets
+// keep most uint32 tiles inside the packed 16-bit block sort's span
+// (measured: 1716 vs 1817 us block sort on C2, scatter +40 us).
+constexpr uint32_t kLastNum = 3, kLastDen = 4;
 // Number of buckets for a segment of len keys.  A segment whose buckets would
 // average at most 3/4 of the block sorter's cap with the largest K is split
-// once (K = len / target rounded up to a power of two, at most K_max): the
+// once (K = len / (3/4 target) rounded up to a power of two, at most K_max): the
 // last level then never leaves a sliver for a further level.  Larger segments
 // spread log2(len / target) bits evenly over the fewest levels of <= K_max,
 // where the last level may leave buckets of up to twice the target when the
@@ -142,7 +146,12 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
     const uint64_t ratio = (len + target - 1) / target;
     uint32_t r = ceil_log2_u64(ratio);
     if (r < 1) r = 1;
-    if (len <= ((uint64_t)cap * 3 / 4) << log_kmax) return r < log_kmax ? r : log_kmax;
+    if (len <= ((uint64_t)cap * 3 / 4) << log_kmax) {
+        const uint64_t tl = (uint64_t)target * kLastNum / kLastDen;  // last-level bucket target
+        uint32_t rl = ceil_log2_u64((len + tl - 1) / tl);
+        if (rl < 1) rl = 1;
+        return rl < log_kmax ? rl : log_kmax;
+    }
     const uint32_t slack = cap / target >= 4 ? 1u : 0u;
     const uint32_t rs = r > slack ? r - slack : 1;
     const uint32_t levels = (rs + log_kmax - 1) / log_kmax;
