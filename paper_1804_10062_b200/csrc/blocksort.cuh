@@ -295,6 +295,8 @@ struct BlockSorter {
     // be called by all T threads; s must not be in use.
     __device__ __forceinline__ static void sort(K (&k)[ITEMS], K* s, int m) {
         const int mp = padded(m);
+        const int out = threadIdx.x * ITEMS;
+        const bool owner = out < mp;
         // warps holding any key (their other lanes hold maximum-key padding)
         const bool warp_active = (int)(threadIdx.x & ~31u) * ITEMS < mp;
         if (warp_active) {
@@ -302,7 +304,32 @@ struct BlockSorter {
 #pragma unroll 1
             for (int lr = 1; lr < kWarpLanes && lr * ITEMS < mp; lr <<= 1) warp_merge_round<K, ITEMS>(k, lr);
         }
-        merge_rounds(k, s, m, kWarpLanes * ITEMS, false);
+#pragma unroll 1
+        for (int run = kWarpLanes * ITEMS; run < mp; run <<= 1) {
+            if (owner) store_blocked(k, s);
+            __syncthreads();
+            if (owner) merge_step(k, s, mp, out, run);
+            __syncthreads();
+        }
+        if (owner) store_blocked(k, s);
+        __syncthreads();
+    }
+
+    // One merge-path round for the thread whose outputs start at `out`: runs of
+    // `run` keys in s (padded indexing) pairwise into k.
+    __device__ __forceinline__ static void merge_step(K (&k)[ITEMS], const K* s, int mp, int out, int run) {
+        const int pair = out & ~(2 * run - 1);
+        const int diag = out - pair;
+        const int a0 = pair, b0 = pair + run;
+        const int alen = min(run, mp - a0);
+        const int blen = max(0, min(run, mp - b0));
+        const int a = merge_path_smem<K>(s, a0, alen, b0, blen, diag);
+        if constexpr (kWindow) {  // records: the wide serial merge is select-heavy
+            const int a_end = merge_path_smem<K>(s, a0, alen, b0, blen, diag + ITEMS);
+            bitonic_merge_window<K, ITEMS>(s, a0 + a, a_end - a, b0 + diag - a, k);
+        } else {
+            serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + alen, b0 + diag - a, b0 + blen, k);
+        }
     }
 
     // Merge-path rounds in shared memory from sorted runs of run0 keys up to
@@ -317,20 +344,7 @@ struct BlockSorter {
             if (owner && !in_smem) store_blocked(k, s);
             in_smem = false;
             __syncthreads();
-            if (owner) {
-                const int pair = out & ~(2 * run - 1);
-                const int diag = out - pair;
-                const int a0 = pair, b0 = pair + run;
-                const int alen = min(run, mp - a0);
-                const int blen = max(0, min(run, mp - b0));
-                const int a = merge_path_smem<K>(s, a0, alen, b0, blen, diag);
-                if constexpr (kWindow) {  // records: the wide serial merge is select-heavy
-                    const int a_end = merge_path_smem<K>(s, a0, alen, b0, blen, diag + ITEMS);
-                    bitonic_merge_window<K, ITEMS>(s, a0 + a, a_end - a, b0 + diag - a, k);
-                } else {
-                    serial_merge_smem<K, ITEMS>(s, a0 + a, a0 + alen, b0 + diag - a, b0 + blen, k);
-                }
-            }
+            if (owner) merge_step(k, s, mp, out, run);
             __syncthreads();
         }
         if (owner && !in_smem) store_blocked(k, s);

@@ -116,6 +116,7 @@ struct PlanParams {
     uint64_t chunk_elems;   // chunk granularity (multiple of the tile)
     uint32_t cap;           // largest bucket the block sorter takes
     uint32_t target;        // desired bucket size when choosing K
+    uint32_t last_target;   // ... at the last level (Tune<K>::last_target)
     uint32_t log_kmax;      // largest K = 1 << log_kmax
     uint32_t class_cap[kNumClasses];
     uint32_t task_cap, fill_cap;
@@ -130,25 +131,20 @@ __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
     return r;
 }
 
-// Last-level bucket target = 3/4 of the level target: smaller final buckets
-// keep most uint32 tiles inside the packed 16-bit block sort's span
-// (measured: 1716 vs 1817 us block sort on C2, scatter +40 us).
-constexpr uint32_t kLastNum = 3, kLastDen = 4;
 // Number of buckets for a segment of len keys.  A segment whose buckets would
 // average at most 3/4 of the block sorter's cap with the largest K is split
-// once (K = len / (3/4 target) rounded up to a power of two, at most K_max): the
+// once (K = len / last_target rounded up to a power of two, at most K_max): the
 // last level then never leaves a sliver for a further level.  Larger segments
 // spread log2(len / target) bits evenly over the fewest levels of <= K_max,
 // where the last level may leave buckets of up to twice the target when the
 // cap allows it (one "slack" bit).
-__host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, uint32_t log_kmax,
-                                                uint32_t cap) {
+__host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, uint32_t last_target,
+                                                uint32_t log_kmax, uint32_t cap) {
     const uint64_t ratio = (len + target - 1) / target;
     uint32_t r = ceil_log2_u64(ratio);
     if (r < 1) r = 1;
     if (len <= ((uint64_t)cap * 3 / 4) << log_kmax) {
-        const uint64_t tl = (uint64_t)target * kLastNum / kLastDen;  // last-level bucket target
-        uint32_t rl = ceil_log2_u64((len + tl - 1) / tl);
+        uint32_t rl = ceil_log2_u64((len + last_target - 1) / last_target);
         if (rl < 1) rl = 1;
         return rl < log_kmax ? rl : log_kmax;
     }
@@ -166,7 +162,7 @@ __host__ __device__ inline uint32_t choose_logk(uint64_t len, uint32_t target, u
 __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t len, uint64_t lo,
                                     uint64_t hi, const PlanParams& p, uint32_t sampler,
                                     bool write_chunks = true) {
-    const uint32_t logk = choose_logk(len, p.target, p.log_kmax, p.cap);
+    const uint32_t logk = choose_logk(len, p.target, p.last_target, p.log_kmax, p.cap);
     const uint32_t nch = (uint32_t)((len + p.chunk_elems - 1) / p.chunk_elems);
     const uint32_t hwords = (nch + 1) * (2u << logk);
     const uint32_t s = atomicAdd(&nb.cnt->nsegs, 1u);
@@ -927,8 +923,10 @@ __global__ void fill_kernel(const FillTask* __restrict__ fills, const uint32_t* 
 // offsets): one CTA per task (launched with the sort's task count).
 template <class K, int T, int ITEMS>
 // 4-byte keys: registers budgeted for 1024 / T resident CTAs (64 per
-// thread), which the packed 16-bit path otherwise exceeds.
-__global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1024 / T : 1) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
+// thread), which the packed 16-bit path otherwise exceeds.  Other keys: the
+// compiler's choice (0) -- an explicit 1 lets it take ~50% more registers
+// (measured: u64 and record block sorts 30% slower).
+__global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1024 / T : 0) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
                                                             const K* B) {
     using BS = BlockSorter<K, T, ITEMS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
