@@ -55,6 +55,16 @@ __global__ void transform64_kernel(uint64_t* p, uint64_t words, int mode, int in
     }
 }
 
+// The same maps as an Xf (common.cuh) over a range of core keys: the
+// stand-alone passes the fused samplesort path does not need (direct block
+// sort of a small n, merge sort, merge fallback ranges).
+template <class K>
+__global__ void xf_kernel(K* p, uint64_t n, Xf xf, int inverse) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = inverse ? xf_inv(p[i], xf) : xf_fwd(p[i], xf);
+}
+
 // ---------------------------------------------------------------------------
 // K9: counter-based SplitMix64 generators, bit-identical to the host recipes
 // (reference rng.hpp:10-23).  Element j of SplitMix64(seed) is

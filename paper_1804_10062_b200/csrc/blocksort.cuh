@@ -283,9 +283,10 @@ struct BlockSorter {
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) k[i] = s[P::idx(base + i)];
     }
-    __device__ __forceinline__ static void store_striped(K* __restrict__ dst, int m, const K* s) {
+    __device__ __forceinline__ static void store_striped(K* __restrict__ dst, int m, const K* s,
+                                                         const Xf& xf = Xf{0, 0}) {
 #pragma unroll 4
-        for (int i = threadIdx.x; i < m; i += T) dst[i] = s[P::idx(i)];
+        for (int i = threadIdx.x; i < m; i += T) dst[i] = xf_inv(s[P::idx(i)], xf);
     }
 
     // Sort the first m keys held in registers (blocked arrangement; the last
@@ -359,7 +360,7 @@ struct BlockSorter {
     // otherwise (ties in the prefix) returns false with nothing written and
     // the caller sorts the records themselves.  The uint64 sorter's compare-
     // and-swaps are a few instructions where a record's is ~30.
-    __device__ static bool sort_tile_prefix(const K* src, K* dst, int m, K* s) {
+    __device__ static bool sort_tile_prefix(const K* src, K* dst, int m, K* s, const Xf& xf) {
         using B64 = BlockSorter<uint64_t, T, ITEMS>;
         using P8 = SmemPad<uint64_t>;
         __shared__ unsigned long long red_lo[T / 32], red_hi[T / 32];
@@ -415,7 +416,7 @@ struct BlockSorter {
         for (int i = tid; i + 1 < m; i += T)
             tie |= ((s64[P8::idx(i)] ^ s64[P8::idx(i + 1)]) >> 12) == 0 ? 1 : 0;
         if (__syncthreads_or(tie)) return false;
-        for (int i = tid; i < m; i += T) dst[i] = rec[s64[P8::idx(i)] & 0xFFFull];
+        for (int i = tid; i < m; i += T) dst[i] = xf_inv(rec[s64[P8::idx(i)] & 0xFFFull], xf);
         return true;
     }
 
@@ -485,9 +486,11 @@ struct BlockSorter {
     }
 
     // Whole tile: global src (m keys) -> sorted -> global dst.  src may alias dst.
-    __device__ __forceinline__ static void sort_tile(const K* src, K* dst, int m, K* s) {
+    // xf: the inverse order-preserving transform is applied on the way out.
+    __device__ __forceinline__ static void sort_tile(const K* src, K* dst, int m, K* s,
+                                                     const Xf& xf = Xf{0, 0}) {
         if constexpr (kPrefixPath) {
-            if (m > 1 && sort_tile_prefix(src, dst, m, s)) return;
+            if (m > 1 && sort_tile_prefix(src, dst, m, s, xf)) return;
         }
         if constexpr (kPackedPath) {
             // striped load with the tile's key range
@@ -517,7 +520,7 @@ struct BlockSorter {
             }
             if (m > 1 && hi - lo < 0xFFFFu) {  // 0xFFFF is reserved for padding
                 sort_tile_packed(s, m, lo);
-                store_striped(dst, m, s);
+                store_striped(dst, m, s, xf);
                 return;
             }
         } else {
@@ -528,7 +531,7 @@ struct BlockSorter {
         if ((int)threadIdx.x * ITEMS < warp_padded(m)) load_blocked(k, s);
         __syncthreads();
         sort(k, s, m);
-        store_striped(dst, m, s);
+        store_striped(dst, m, s, xf);
     }
 };
 

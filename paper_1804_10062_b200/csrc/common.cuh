@@ -166,6 +166,33 @@ struct SmemPad {
     static constexpr int elems(int n) { return n + n / kPer + 64; }
 };
 
+// Order-preserving transform fused into the sort's first reads and last
+// writes (aux_kernels.cuh has the standalone passes):
+//   f(x) = x ^ b ^ (sext(x) & a),   f^-1(u) = u ^ b ^ (sext(u ^ b) & a)
+// where sext(x) is all ones when x's top bit is set and a never has the top
+// bit (so the top bit of f(x) is top(x) ^ top(b)).  a = b = 0: identity.
+// int32/int64: b = sign bit (less) or its complement (greater), a = 0;
+// unsigned greater: b = ~0; float64: a = 0x7FF..F, b = sign bit (less) or
+// 0x7FF..F (greater); records: every word ^ b.
+struct Xf {
+    uint64_t a, b;
+};
+__device__ __forceinline__ uint32_t xf_fwd(uint32_t x, const Xf& f) { return x ^ (uint32_t)f.b; }
+__device__ __forceinline__ uint32_t xf_inv(uint32_t u, const Xf& f) { return u ^ (uint32_t)f.b; }
+__device__ __forceinline__ uint64_t xf_fwd(uint64_t x, const Xf& f) {
+    return x ^ f.b ^ ((uint64_t)((int64_t)x >> 63) & f.a);
+}
+__device__ __forceinline__ uint64_t xf_inv(uint64_t u, const Xf& f) {
+    const uint64_t v = u ^ f.b;
+    return v ^ ((uint64_t)((int64_t)v >> 63) & f.a);
+}
+__device__ __forceinline__ Rec32 xf_fwd(Rec32 x, const Xf& f) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x.w[i] ^= f.b;
+    return x;
+}
+__device__ __forceinline__ Rec32 xf_inv(Rec32 u, const Xf& f) { return xf_fwd(u, f); }
+
 // SplitMix64 finaliser (reference rng.hpp:14-19) -- also used as a hash.
 __host__ __device__ __forceinline__ uint64_t sm_mix(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

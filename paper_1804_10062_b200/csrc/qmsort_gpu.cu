@@ -351,14 +351,14 @@ static int blocksort_one(const K* src, K* dst, uint64_t off, uint64_t len, cudaS
 // Block-sort the `count` tasks of size class C into A: one CTA per task.
 template <class K, int C>
 static int launch_class(const SortTask* tasks, uint32_t count, K* A, const K* B, cudaStream_t st,
-                        Ledger& led) {
+                        Ledger& led, Xf xf) {
     using TU = Tune<K>;
     constexpr int T = TU::CLS_T[C];
     using BS = BlockSorter<K, T, TU::BI>;
     if (count == 0) return QMSORT_OK;
     auto fn = blocksort_tasks_kernel<K, T, TU::BI>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
-    QLAUNCH(led, kPhBlocksort, 0, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, A, B));
+    QLAUNCH(led, kPhBlocksort, 0, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, A, B, xf));
     return QMSORT_OK;
 }
 
@@ -377,6 +377,14 @@ static int estimate_levels(uint64_t n, const PlanParams& p) {
 
 // Block-sort tiles + merge-path passes over [off, off+len); the range currently
 // lives in X (A or B); the result lands in A.
+template <class K>
+static int xf_range(K* p, uint64_t n, Xf xf, bool inverse, cudaStream_t st, Ledger& led) {
+    if (n == 0) return QMSORT_OK;
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    QLAUNCH(led, kPhTransform, 2 * n * sizeof(K), xf_kernel<K><<<grid, 256, 0, st>>>(p, n, xf, inverse ? 1 : 0));
+    return QMSORT_OK;
+}
+
 template <class K>
 static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStream_t st,
                            Ledger& led) {
@@ -404,9 +412,12 @@ static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStr
     return QMSORT_OK;
 }
 
+// xf (fused transform): level 0 reads the caller's keys through f, every
+// final write (block sort, fills, merge fallback) goes through f^-1.
 template <class K>
 static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
-                      const WsLayout& L, cudaStream_t st, Ledger& led) {
+                      const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf) {
+    const bool fused = xf.a != 0 || xf.b != 0;
     using TU = Tune<K>;
     constexpr uint32_t cap = class_cap<K>(kNumClasses - 1);
     PlanParams p;
@@ -419,6 +430,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     p.task_cap = L.task_cap;
     p.fill_cap = L.fill_cap;
     p.dst_is_a = 0;
+    p.xf_fix = fused ? 1u : 0u;
     p.pivot = (uint32_t)std::max(0, cfg.pivot);
     const double dl = std::min(1.0, std::max(1.0 / 65536.0, cfg.delta > 0 ? cfg.delta : 1.0 / 16.0));
     p.delta_q16 = (uint32_t)(dl * 65536.0);
@@ -455,7 +467,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
 
     using BSS = BlockSorter<K, TU::ST, TU::SI>;
     auto sample_fn = sample_kernel<K, TU::ST, TU::SI>;
+    auto sample_xf_fn = sample_kernel<K, TU::ST, TU::SI, true>;
     QCK(allow_smem((const void*)sample_fn, BSS::kSmemBytes));
+    QCK(allow_smem((const void*)sample_xf_fn, BSS::kSmemBytes));
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
     QCK(allow_smem((const void*)scatter_fn, sizeof(SM)));
@@ -484,13 +498,14 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             LevelCounters* c = &cnts[level];
             p.dst_is_a = (dst == A) ? 1 : 0;
             const uint64_t seed = cfg.seed ^ (0x5851F42D4C957F2Dull * (uint64_t)(level + 1));
+            const Xf lxf = level == 0 ? xf : Xf{0, 0};  // only level 0 reads the caller's keys
             QLAUNCH(led, kPhSample, 0,
-                    sample_fn<<<sample_grid, TU::ST, BSS::kSmemBytes, st>>>(
-                        lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u));
+                    (level == 0 && fused ? sample_xf_fn : sample_fn)<<<sample_grid, TU::ST, BSS::kSmemBytes, st>>>(
+                        lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u, lxf));
             QLAUNCH(led, kPhCount, 0,
                     count_fn<<<count_grid, TU::CT, 0, st>>>(lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks,
                                                             &c->work_count, src, tree[cur], sorted[cur],
-                                                            lut[cur], hist));
+                                                            lut[cur], hist, lxf));
             QLAUNCH(led, kPhPlan, 0,
                     colsum_kernel<<<colsum_grid, 512, 0, st>>>(lv[cur].segs, hist, c));
             QLAUNCH(led, kPhPlan, 0,
@@ -499,7 +514,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             QLAUNCH(led, kPhScatter, 0,
                     scatter_fn<<<scatter_grid, TU::XT, sizeof(SM), st>>>(
                         lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks, &c->work_scatter, src, dst,
-                        tree[cur], sorted[cur], lut[cur], hist, PeerArgs{}));
+                        tree[cur], sorted[cur], lut[cur], hist, PeerArgs{}, lxf));
             std::swap(src, dst);
         }
         // one control read per batch
@@ -517,7 +532,10 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                                 cudaMemcpyDeviceToHost, st));
             QCK(spin_sync(st));
             ++led.syncs;
-            for (const SegDesc& d : h) QTRY(mergesort_range<K>(src, A, B, d.off, d.len, st, led));
+            for (const SegDesc& d : h) {
+                QTRY(mergesort_range<K>(src, A, B, d.off, d.len, st, led));
+                if (fused) QTRY(xf_range<K>(A + d.off, d.len, xf, true, st, led));
+            }
             break;
         }
         batch = 1;  // more levels than a balanced split needs: continue one at a time
@@ -527,12 +545,12 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     const uint32_t* nt = hc[kCntSlots - 1].ntasks;
     for (int c = 0; c < kNumClasses; ++c)
         if (nt[c] > L.task_cap) return fail(QMSORT_EINTERNAL, "block-sort task list capacity exceeded");
-    QTRY((launch_class<K, 0>(tasks + 0 * (size_t)L.task_cap, nt[0], A, B, st, led)));
-    QTRY((launch_class<K, 1>(tasks + 1 * (size_t)L.task_cap, nt[1], A, B, st, led)));
-    QTRY((launch_class<K, 2>(tasks + 2 * (size_t)L.task_cap, nt[2], A, B, st, led)));
-    QTRY((launch_class<K, 3>(tasks + 3 * (size_t)L.task_cap, nt[3], A, B, st, led)));
+    QTRY((launch_class<K, 0>(tasks + 0 * (size_t)L.task_cap, nt[0], A, B, st, led, xf)));
+    QTRY((launch_class<K, 1>(tasks + 1 * (size_t)L.task_cap, nt[1], A, B, st, led, xf)));
+    QTRY((launch_class<K, 2>(tasks + 2 * (size_t)L.task_cap, nt[2], A, B, st, led, xf)));
+    QTRY((launch_class<K, 3>(tasks + 3 * (size_t)L.task_cap, nt[3], A, B, st, led, xf)));
     if (hc[kCntSlots - 1].nfill)
-        QLAUNCH(led, kPhFill, 0, fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, L.fill_cap, A));
+        QLAUNCH(led, kPhFill, 0, fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, L.fill_cap, A, xf));
     // pass ledger from the device counters (count 1, scatter 2, block sort 2, fill 1)
     const uint64_t w = sizeof(K);
     for (int l = 0; l < level; ++l) {
@@ -552,16 +570,21 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     return QMSORT_OK;
 }
 
+// xf: the caller's keys are f^-1(core keys); the samplesort path fuses f and
+// f^-1 into its first reads and last writes, the others run them as passes.
 template <class K>
 static int sort_core(K* A, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
-                     const WsLayout& L, cudaStream_t st, Ledger& led) {
-    using TU = Tune<K>;
+                     const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf = Xf{0, 0}) {
     constexpr uint64_t cap = class_cap<K>(kNumClasses - 1);
     if (n <= 1) return QMSORT_OK;
+    const bool fused = xf.a != 0 || xf.b != 0;
     K* B = reinterpret_cast<K*>(ws + L.b_off);
-    if (n <= cap) return blocksort_one<K>(A, A, 0, n, st, led);
-    if (cfg.algorithm == 1) return mergesort_range<K>(A, A, B, 0, n, st, led);
-    return samplesort<K>(A, B, n, cfg, ws, L, st, led);
+    if (n > cap && cfg.algorithm != 1) return samplesort<K>(A, B, n, cfg, ws, L, st, led, xf);
+    if (fused) QTRY(xf_range<K>(A, n, xf, false, st, led));
+    if (n <= cap) QTRY(blocksort_one<K>(A, A, 0, n, st, led));
+    else QTRY(mergesort_range<K>(A, A, B, 0, n, st, led));
+    if (fused) QTRY(xf_range<K>(A, n, xf, true, st, led));
+    return QMSORT_OK;
 }
 
 static int core_dtype(int dt) {
@@ -589,6 +612,21 @@ static size_t ws_bytes_for(int dt, size_t n) {
         case QMSORT_DT_REC32: return make_layout<Rec32>(n).total;
     }
     return 0;
+}
+
+// The comparator's transform as an Xf (common.cuh; the same maps as
+// transform32/64_kernel).
+static Xf make_xf(int dt, int cmp) {
+    constexpr uint64_t S = 0x8000000000000000ull, M = 0x7FFFFFFFFFFFFFFFull;
+    switch (dt) {
+        case QMSORT_DT_I32: return Xf{0, cmp ? 0x7FFFFFFFull : 0x80000000ull};
+        case QMSORT_DT_U32: return Xf{0, cmp ? 0xFFFFFFFFull : 0};
+        case QMSORT_DT_U64: return Xf{0, cmp ? ~0ull : 0};
+        case QMSORT_DT_F64: return Xf{M, cmp ? M : S};
+        case QMSORT_DT_I64: return Xf{0, cmp ? M : S};
+        case QMSORT_DT_REC32: return Xf{0, cmp ? ~0ull : 0};
+    }
+    return Xf{0, 0};
 }
 
 // Launch the forward / inverse order-preserving transform.
@@ -664,22 +702,22 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     QCK(cudaEventCreate(&e0));
     QCK(cudaEventCreate(&e1));
     QCK(cudaEventRecord(e0, st));
-    int rc = run_transform(dt, cmp, d, n, 0, st, led);
-    if (rc == QMSORT_OK) {
-        unsigned char* w = static_cast<unsigned char*>(ws);
-        switch (core_dtype(dt)) {
-            case QMSORT_DT_U32:
-                rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w, make_layout<uint32_t>(n), st, led);
-                break;
-            case QMSORT_DT_U64:
-                rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w, make_layout<uint64_t>(n), st, led);
-                break;
-            case QMSORT_DT_REC32:
-                rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n), st, led);
-                break;
-        }
+    // the comparator's order-preserving transform runs inside the sort
+    // (fused into its first reads and last writes), not as extra passes
+    const Xf xf = make_xf(dt, cmp);
+    int rc = QMSORT_OK;
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    switch (core_dtype(dt)) {
+        case QMSORT_DT_U32:
+            rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w, make_layout<uint32_t>(n), st, led, xf);
+            break;
+        case QMSORT_DT_U64:
+            rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w, make_layout<uint64_t>(n), st, led, xf);
+            break;
+        case QMSORT_DT_REC32:
+            rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n), st, led, xf);
+            break;
     }
-    if (rc == QMSORT_OK) rc = run_transform(dt, cmp, d, n, 1, st, led);
     cudaEventRecord(e1, st);
     cudaError_t se = spin_event(e1);
     float ms = 0.f;
@@ -827,7 +865,8 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
         auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
         QLAUNCH(led, kPhCount, n * sizeof(K),
                 count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
-                           st>>>(seg, chunks, nchunks, nullptr, &cnt->work_count, in, tree, sorted, lut, hist));
+                           st>>>(seg, chunks, nchunks, nullptr, &cnt->work_count, in, tree, sorted, lut, hist,
+                                 Xf{0, 0}));
         QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<64, 512, 0, st>>>(seg, hist, nullptr));
         QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
     }
@@ -839,7 +878,7 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
         QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
                 fn<<<std::min(nchunks, resident_grid((const void*)fn, TU::XT, sizeof(SM))), TU::XT,
                      sizeof(SM), st>>>(seg, chunks, nchunks, nullptr, &cnt->work_scatter, in, out, tree,
-                                       sorted, lut, hist, *peers));
+                                       sorted, lut, hist, *peers, Xf{0, 0}));
         return QMSORT_OK;
     }
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
@@ -847,7 +886,7 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
             scatter_fn<<<std::min(nchunks, resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM))),
                          TU::XT, sizeof(SM), st>>>(seg, chunks, nchunks, nullptr, &cnt->work_scatter, in,
-                                                   out, tree, sorted, lut, hist, PeerArgs{}));
+                                                   out, tree, sorted, lut, hist, PeerArgs{}, Xf{0, 0}));
     return QMSORT_OK;
 }
 

@@ -117,6 +117,7 @@ struct PlanParams {
     uint32_t cap;           // largest bucket the block sorter takes
     uint32_t target;        // desired bucket size when choosing K
     uint32_t last_target;   // ... at the last level (Tune<K>::last_target)
+    uint32_t xf_fix;        // fused transform: singletons / equal buckets in A still get a writer
     uint32_t log_kmax;      // largest K = 1 << log_kmax
     uint32_t class_cap[kNumClasses];
     uint32_t task_cap, fill_cap;
@@ -318,11 +319,11 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
 // ---------------------------------------------------------------------------
 // K1: per-segment sample + splitter selection.  One CTA per segment.
 // ---------------------------------------------------------------------------
-template <class K, int T, int ITEMS>
+template <class K, int T, int ITEMS, bool XF>
 __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, const K* __restrict__ src,
                                                K* tree_store, K* sorted_store,
                                                uint32_t* lut_store, uint64_t seed,
-                                               uint32_t oversample) {
+                                               uint32_t oversample, const Xf& xf) {
     using BS = BlockSorter<K, T, ITEMS>;
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
@@ -348,6 +349,11 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
             const uint64_t p0 = ((uint64_t)idx * d.len) / (uint64_t)S;
             const K* t = src + d.off + min(p0, d.len - 3);
             K a = t[0], b = t[1], c = t[2];
+            if (XF) {
+                a = xf_fwd(a, xf);
+                b = xf_fwd(b, xf);
+                c = xf_fwd(c, xf);
+            }
             KT::cas(a, b);  // a <= b
             KT::cas(b, c);  // c = max; b = median candidate
             KT::cas(a, b);  // b = median of three
@@ -355,6 +361,7 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
         } else {
             const uint64_t h = sm_mix(seed + (d.off + 1) * kGamma + (uint64_t)(idx + 1) * 0xD1B54A32D192ED03ull);
             k[i] = src[d.off + __umul64hi(h, d.len)];
+            if (XF) k[i] = xf_fwd(k[i], xf);
         }
     }
     BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
@@ -422,15 +429,16 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
 
 // The level's segment count is read on the device (written by the previous
 // level's plan), so a whole sort is enqueued without host round trips.
-template <class K, int T, int ITEMS>
+template <class K, int T, int ITEMS, bool XF = false>  // XF: level 0 of a fused-transform sort
 __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const uint32_t* __restrict__ nsegs,
                                                    const K* __restrict__ src, K* tree_store,
                                                    K* sorted_store, uint32_t* lut_store,
-                                                   uint64_t seed, uint32_t oversample) {
+                                                   uint64_t seed, uint32_t oversample,
+                                                   Xf xf = Xf{0, 0}) {
     const uint32_t ns = *nsegs;
     for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
-        sample_segment<K, T, ITEMS>(seg, segs, src, tree_store, sorted_store, lut_store, seed,
-                                    oversample);
+        sample_segment<K, T, ITEMS, XF>(seg, segs, src, tree_store, sorted_store, lut_store, seed,
+                                        oversample, xf);
         __syncthreads();  // shared memory is reused by the next segment
     }
 }
@@ -438,10 +446,11 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const uint32_t
 // ---------------------------------------------------------------------------
 // K2: per-chunk bucket histogram.
 // ---------------------------------------------------------------------------
-template <class K, int T, int U, int LOG_KMAX>
+template <class K, int T, int U, int LOG_KMAX, bool XF>
 __device__ __forceinline__ void count_chunk(const ClassifierSmem<K, LOG_KMAX>& cls, uint32_t* shist,
                                             const SegDesc& d, const ChunkDesc& c, uint32_t ck,
-                                            const K* __restrict__ src, uint32_t* __restrict__ hist) {
+                                            const K* __restrict__ src, uint32_t* __restrict__ hist,
+                                            const Xf& xf) {
     const uint32_t nb = (1u << d.logk) << d.eq;
     for (uint32_t i = threadIdx.x; i < nb; i += T) shist[i] = 0;
     __syncthreads();
@@ -453,7 +462,7 @@ __device__ __forceinline__ void count_chunk(const ClassifierSmem<K, LOG_KMAX>& c
         K k[U];
         uint32_t bin[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) k[u] = p[base + u * T];
+        for (int u = 0; u < U; ++u) k[u] = XF ? xf_fwd(p[base + u * T], xf) : p[base + u * T];
         classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
 #pragma unroll
         for (int u = 0; u < U; ++u) atomicAdd(&shist[bin[u]], 1u);
@@ -465,7 +474,7 @@ __device__ __forceinline__ void count_chunk(const ClassifierSmem<K, LOG_KMAX>& c
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const uint32_t i = u * T + threadIdx.x;
-            k[u] = i < rem ? p[base + u * T] : KeyTraits<K>::max_key();
+            k[u] = i < rem ? (XF ? xf_fwd(p[base + u * T], xf) : p[base + u * T]) : KeyTraits<K>::max_key();
         }
         classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
 #pragma unroll
@@ -490,7 +499,7 @@ __global__ void __launch_bounds__(T, 4) count_kernel(const SegDesc* __restrict__
                                                   const K* __restrict__ tree_store,
                                                   const K* __restrict__ sorted_store,
                                                   const uint32_t* __restrict__ lut_store,
-                                                  uint32_t* __restrict__ hist) {
+                                                  uint32_t* __restrict__ hist, Xf xf = Xf{0, 0}) {
     constexpr int KMAX = 1 << LOG_KMAX;
     __shared__ ClassifierSmem<K, LOG_KMAX> cls;
     __shared__ uint32_t shist[2 * KMAX];
@@ -508,7 +517,8 @@ __global__ void __launch_bounds__(T, 4) count_kernel(const SegDesc* __restrict__
             load_classifier<K, LOG_KMAX, T>(cls, d, tree_store, sorted_store, lut_store);
             cur_seg = c.seg;
         }
-        count_chunk<K, T, U, LOG_KMAX>(cls, shist, d, c, ck, src, hist);
+        if (xf.a | xf.b) count_chunk<K, T, U, LOG_KMAX, true>(cls, shist, d, c, ck, src, hist, xf);
+        else count_chunk<K, T, U, LOG_KMAX, false>(cls, shist, d, c, ck, src, hist, xf);
     }
 }
 
@@ -598,7 +608,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
         const uint32_t len = tot[b];
         uint32_t sl = 0xFFFFFFFFu;
-        if (len != 0 && !(d.eq && (b & 1)) && len <= p.cap && !(len == 1 && p.dst_is_a)) {
+        if (len != 0 && !(d.eq && (b & 1)) && len <= p.cap && !(len == 1 && p.dst_is_a && !p.xf_fix)) {
             uint32_t cls = 0;
             while (cls < kNumClasses - 1 && len > p.class_cap[cls]) ++cls;
             sl = (cls << 28) | atomicAdd(&cls_count[cls], 1u);
@@ -619,7 +629,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
         if (len == 0) continue;
         const uint64_t off = d.off + start[b];
         if (d.eq && (b & 1)) {  // equal-key bucket: final once it is in the caller's buffer
-            if (!p.dst_is_a) {
+            if (!p.dst_is_a || p.xf_fix) {  // (fused transform: its fill writes f^-1)
                 const uint32_t f = atomicAdd(&sort_cnt->nfill, 1u);
                 if (f < p.fill_cap) {
                     FillTask ft;
@@ -753,11 +763,12 @@ struct PeerSink {
     }
 };
 
-template <class K, int T, int U, int LOG_KMAX, bool FULL, class Sink>
+template <class K, int T, int U, int LOG_KMAX, bool FULL, bool XF, class Sink>
 __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm, const SegDesc& d,
                                              const K* __restrict__ p, uint32_t m,
                                              const Sink& out,
-                                             uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT]) {
+                                             uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT],
+                                             const Xf& xf) {
     using SM = ScatterSmem<K, T, U, LOG_KMAX>;
     constexpr int BPT = SM::BPT;
     const uint32_t tid = threadIdx.x;
@@ -766,8 +777,8 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const uint32_t li = u * T + tid;
-        if (FULL) k[u] = p[li];
-        else k[u] = li < m ? p[li] : KeyTraits<K>::max_key();
+        if (FULL) k[u] = XF ? xf_fwd(p[li], xf) : p[li];
+        else k[u] = li < m ? (XF ? xf_fwd(p[li], xf) : p[li]) : KeyTraits<K>::max_key();
     }
     classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
     // rank within the tile's bucket; pack (bin, rank) into one word
@@ -840,7 +851,7 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
                                                     const K* __restrict__ sorted_store,
                                                     const uint32_t* __restrict__ lut_store,
                                                     const uint32_t* __restrict__ hist,
-                                                    PeerArgs peers = PeerArgs{}) {
+                                                    PeerArgs peers = PeerArgs{}, Xf xf = Xf{0, 0}) {
     using SM = ScatterSmem<K, T, U, LOG_KMAX>;
     constexpr uint32_t TILE = SM::TILE;
     constexpr int BPT = SM::BPT;
@@ -892,13 +903,19 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
         if constexpr (PEER) {
             const PeerSink<K> out{peer_base, peer_start, peers.nb};
             for (; t0 + TILE <= len; t0 += TILE)
-                scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
-            if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+                scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
+            if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
         } else {
             const LocalSink<K> out{dst + d.off};
-            for (; t0 + TILE <= len; t0 += TILE)
-                scatter_tile<K, T, U, LOG_KMAX, true>(sm, d, p + t0, TILE, out, cursor);
-            if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false>(sm, d, p + t0, len - t0, out, cursor);
+            if (xf.a | xf.b) {  // level 0 of a fused-transform sort
+                for (; t0 + TILE <= len; t0 += TILE)
+                    scatter_tile<K, T, U, LOG_KMAX, true, true>(sm, d, p + t0, TILE, out, cursor, xf);
+                if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, true>(sm, d, p + t0, len - t0, out, cursor, xf);
+            } else {
+                for (; t0 + TILE <= len; t0 += TILE)
+                    scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
+                if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
+            }
         }
     }
 }
@@ -907,12 +924,13 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
 // The fill count is read on the device (written by the level's plan).
 template <class K>
 __global__ void fill_kernel(const FillTask* __restrict__ fills, const uint32_t* __restrict__ nfill,
-                            uint32_t fill_cap, K* __restrict__ dst) {
+                            uint32_t fill_cap, K* __restrict__ dst, Xf xf = Xf{0, 0}) {
     const uint32_t nf = min(*nfill, fill_cap);
     for (uint32_t f = 0; f < nf; ++f) {
         const FillTask ft = fills[f];
         K v;
         memcpy(&v, ft.value, sizeof(K));
+        v = xf_inv(v, xf);
         for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ft.len;
              i += (uint64_t)gridDim.x * blockDim.x)
             dst[ft.off + i] = v;
@@ -927,12 +945,12 @@ template <class K, int T, int ITEMS>
 // compiler's choice (0) -- an explicit 1 lets it take ~50% more registers
 // (measured: u64 and record block sorts 30% slower).
 __global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1024 / T : 0) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
-                                                            const K* B) {
+                                                            const K* B, Xf xf = Xf{0, 0}) {
     using BS = BlockSorter<K, T, ITEMS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s = reinterpret_cast<K*>(smem_raw);
     const SortTask t = tasks[blockIdx.x];
-    BS::sort_tile((t.in_a ? A : B) + t.off, A + t.off, (int)t.len, s);
+    BS::sort_tile((t.in_a ? A : B) + t.off, A + t.off, (int)t.len, s, xf);
 }
 
 // Block-sort consecutive tiles of a range (merge-sort front end / fallback).
