@@ -100,6 +100,7 @@ struct LevelCounters {
     uint32_t work_count, work_scatter;  // dynamic chunk dispensers of this level's kernels
     uint32_t resplits;  // hybrid: children re-sampled with triple medians (f1)
     uint32_t max_logk;  // largest log2 K among this level's segments
+    uint32_t max_nchunks;  // most chunks of one of this level's segments
     unsigned long long nkeys;      // keys in this level's segments (pass ledger)
     unsigned long long task_keys;  // keys handed to the block sorter
     unsigned long long fill_keys;  // keys written by equal-bucket fills
@@ -168,6 +169,7 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     const uint32_t hwords = (nch + 1) * (2u << logk);
     const uint32_t s = atomicAdd(&nb.cnt->nsegs, 1u);
     atomicMax(&nb.cnt->max_logk, logk);
+    atomicMax(&nb.cnt->max_nchunks, nch);
     const uint32_t sp = atomicAdd(&nb.cnt->nsplit, 1u << logk);
     const uint32_t c0 = atomicAdd(&nb.cnt->nchunks, nch);
     const uint32_t hb = atomicAdd(&nb.cnt->nhist, hwords);
@@ -534,6 +536,30 @@ __global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__
                                                      const LevelCounters* __restrict__ cnt) {
     const uint32_t ns = cnt ? cnt->nsegs : 1u;
     const uint32_t NBMAX = cnt ? (2u << cnt->max_logk) : 1024u;  // bins incl. equality bins
+    if (cnt && cnt->max_nchunks <= 16) {
+        // segments of a few chunks (the lower levels): one thread per
+        // (segment, bin) walks its column serially -- a warp per column
+        // would leave most lanes idle
+        const uint64_t nt = (uint64_t)gridDim.x * blockDim.x;
+        for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (uint64_t)ns * NBMAX;
+             idx += nt) {
+            const SegDesc d = segs[idx / NBMAX];
+            const uint32_t b = (uint32_t)(idx % NBMAX);
+            if (b >= ((1u << d.logk) << d.eq)) continue;
+            uint32_t* col = hist + d.hist_base + b * (d.nchunks + 1);
+            uint32_t v[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) v[c] = c < (int)d.nchunks ? col[c] : 0u;
+            uint32_t carry = 0;
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                if (c < (int)d.nchunks) col[c] = carry;
+                carry += v[c];
+            }
+            col[d.nchunks] = carry;
+        }
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t idx = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
