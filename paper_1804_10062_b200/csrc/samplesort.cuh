@@ -236,8 +236,24 @@ struct ClassifierSmem {
     static constexpr int KMAX = 1 << LOG_KMAX;
     K sorted[KMAX];                                           // unique splitters
     K tree[KeyTraits<K>::kLut ? 1 : KMAX];                    // rec32: Eytzinger tree
+    uint64_t ptree[KeyTraits<K>::kLut ? 1 : KMAX];            // rec32: the tree's 64-bit prefixes
     uint32_t lut[KeyTraits<K>::kLut ? (1 << kLutMaxBits) : 1];  // integers: j_lo | (j_hi-j_lo) << 16
 };
+
+// Records: a 64-bit prefix that is monotone (non-decreasing) in the
+// lexicographic order -- the top 64 bits of (w0 - base, w1), clamped to
+// [0, 2^64) for w0 outside [base, base + 2^(64-psh)).  base and psh come from
+// the segment's sample (SegDesc lo / shift); any values keep the prefix
+// monotone, they only decide how often two prefixes tie.  p(a) < p(b) implies
+// a < b, so a tree step needs the full record compare only on equal prefixes.
+__device__ __forceinline__ uint64_t rec_prefix(const Rec32& r, uint64_t base, uint32_t psh) {
+    if (r.w[0] < base) return 0;
+    const uint64_t d0 = r.w[0] - base;
+    if (psh == 0) return d0;
+    if (psh >= 64) return d0 ? ~0ull : r.w[1];
+    if (d0 >> (64 - psh)) return ~0ull;
+    return (d0 << psh) | (r.w[1] >> (64 - psh));
+}
 
 template <class K, int LOG_KMAX, int T>
 __device__ __forceinline__ void load_classifier(ClassifierSmem<K, LOG_KMAX>& c, const SegDesc& d,
@@ -251,7 +267,11 @@ __device__ __forceinline__ void load_classifier(ClassifierSmem<K, LOG_KMAX>& c, 
         const uint32_t* src = lut_store + (size_t)d.sp * kLutPerSplitter;
         for (uint32_t i = threadIdx.x; i < nc; i += T) c.lut[i] = src[i];
     } else {
-        for (uint32_t i = threadIdx.x; i < K_; i += T) c.tree[i] = tree_store[d.sp + i];
+        for (uint32_t i = threadIdx.x; i < K_; i += T) {
+            const K t = tree_store[d.sp + i];
+            c.tree[i] = t;
+            if constexpr (std::is_same<K, Rec32>::value) c.ptree[i] = rec_prefix(t, d.lo, d.shift);
+        }
     }
 }
 
@@ -296,12 +316,23 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
             }
         }
     } else {
+        // Eytzinger walk on the splitters' prefixes; the full record compare
+        // only where a key's prefix equals the node's
         uint32_t t[U];
+        uint64_t pk[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) t[u] = 1;
+        for (int u = 0; u < U; ++u) {
+            t[u] = 1;
+            pk[u] = rec_prefix(key[u], d.lo, d.shift);
+        }
         for (uint32_t l = 0; l < d.logk; ++l) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) t[u] = 2 * t[u] + (KT::lt(c.tree[t[u]], key[u]) ? 1u : 0u);
+            for (int u = 0; u < U; ++u) {
+                const uint64_t np = c.ptree[t[u]];
+                bool right = pk[u] > np;
+                if (pk[u] == np) right = KT::lt(c.tree[t[u]], key[u]);
+                t[u] = 2 * t[u] + (right ? 1u : 0u);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) j[u] = t[u] - (1u << d.logk);
@@ -367,6 +398,13 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
         }
     }
     BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
+    uint64_t pbase = 0;
+    uint32_t psh = 0;
+    if constexpr (std::is_same<K, Rec32>::value) {  // prefix window of the sampled w0 range
+        const uint64_t w0a = s[P::idx(0)].w[0], w0b = s[P::idx(S - 1)].w[0];
+        pbase = w0a;
+        psh = w0b > w0a ? (uint32_t)__clzll((long long)(w0b - w0a)) : 64u;
+    }
 
     // candidate splitter j (0 <= j < K-1): sample quantile (j+1)/K
     for (uint32_t j = threadIdx.x; j < K_ - 1; j += T) {
@@ -426,6 +464,10 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
     if (threadIdx.x == 0) {
         segs[seg].m = m;
         segs[seg].eq = (m < K_ - 1) ? 1u : 0u;
+        if constexpr (std::is_same<K, Rec32>::value) {
+            segs[seg].lo = pbase;
+            segs[seg].shift = psh;
+        }
     }
 }
 
