@@ -761,8 +761,13 @@ struct ScatterSmem {
     static constexpr int TILE = T * U;
     // a staged key travels with its segment-relative destination, so the
     // write-out reads one record per key and needs no per-bucket lookup
-    struct alignas(sizeof(K) >= 8 ? 16 : 8) Rec {
-        K key;
+    // 8- and 32-byte keys stage only their index in the tile: the write-out
+    // re-reads the key from the tile just loaded (L1/L2), which moves 8
+    // instead of 16 / 48 bytes per key through shared memory twice (measured:
+    // C5 scatter 3.78 -> 2.87 ms, C4a 2.80 -> 2.56 ms, C3 unchanged).
+    static constexpr bool kStageIndex = sizeof(K) >= 8;
+    struct alignas(sizeof(K) >= 8 && !kStageIndex ? 16 : 8) Rec {
+        typename std::conditional<kStageIndex, uint32_t, K>::type key;  // key, or its tile index
         uint32_t dest;
     };
     ClassifierSmem<K, LOG_KMAX> cls;
@@ -892,7 +897,8 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
             const uint2 sg = sm.sd[bin[u] >> 16];
             const uint32_t pos = sg.x + (bin[u] & 0xFFFFu);
             typename SM::Rec r;
-            r.key = k[u];
+            if constexpr (SM::kStageIndex) r.key = u * T + tid;
+            else r.key = k[u];
             r.dest = sg.y + pos;
             stage[pos] = r;
         }
@@ -903,7 +909,8 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         const uint32_t i = u * T + tid;
         if (FULL || i < m) {
             const typename SM::Rec r = stage[i];
-            out.store(r.dest, r.key);
+            if constexpr (SM::kStageIndex) out.store(r.dest, XF ? xf_fwd(p[r.key], xf) : p[r.key]);
+            else out.store(r.dest, r.key);
         }
     }
     __syncthreads();
