@@ -1015,11 +1015,12 @@ __global__ void fill_kernel(const FillTask* __restrict__ fills, const uint32_t* 
 // Block-sort every task of one size class into A (from A or B, at the same
 // offsets): one CTA per task (launched with the sort's task count).
 template <class K, int T, int ITEMS>
-// 4-byte keys: registers budgeted for 1024 / T resident CTAs (64 per
-// thread), which the packed 16-bit path otherwise exceeds.  Other keys: the
+// 4-byte keys: registers budgeted for 1536 / T resident CTAs (40 per
+// thread, a few spills): occupancy beats registers here (measured on C2:
+// 64 regs 1735 us, 48-51 regs 1684 us, 40 regs 1673 us).  Other keys: the
 // compiler's choice (0) -- an explicit 1 lets it take ~50% more registers
 // (measured: u64 and record block sorts 30% slower).
-__global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1024 / T : 0) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
+__global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1536 / T : 0) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
                                                             const K* B, Xf xf = Xf{0, 0}) {
     using BS = BlockSorter<K, T, ITEMS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
