@@ -872,18 +872,34 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
     }
     classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
     // rank within the tile's bucket; pack (bin, rank) into one word
-    if (((1u << d.logk) << d.eq) <= 64) {  // few bins: warp-aggregated ranks (uniform per segment)
+    if (((1u << d.logk) << d.eq) <= 64) {
+        // Few bins (the sharded exchange's P buckets, small segments): no
+        // staging.  Warp-aggregated ranks give the lanes of one bin
+        // consecutive slots after the bin's cursor, so every key is stored
+        // straight from its register and each bin's lanes write one
+        // contiguous run.
+        uint32_t* base = reinterpret_cast<uint32_t*>(sm.sd);  // bin -> destination of its next key
+#pragma unroll
+        for (int i = 0; i < BPT; ++i) base[tid * BPT + i] = cursor[i];
+        __syncthreads();
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const bool v = FULL || u * T + tid < m;
             const uint32_t r = warp_agg_inc(sm.hist, bin[u], v);
-            if (v) bin[u] = (bin[u] << 16) | r;
+            if (v) out.store(base[bin[u]] + r, k[u]);
         }
-    } else {
+        __syncthreads();
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            if (FULL || u * T + tid < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
+        for (int i = 0; i < BPT; ++i) {
+            cursor[i] += sm.hist[tid * BPT + i];
+            sm.hist[tid * BPT + i] = 0;
         }
+        __syncthreads();
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (FULL || u * T + tid < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
     }
     __syncthreads();
     {  // block exclusive scan over all NB bins, BPT per thread
