@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -49,12 +50,27 @@ static int fail(int code, const std::string& msg) {
         if (e_ != cudaSuccess)                                                               \
             return fail(QMSORT_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
     } while (0)
+// QMSORT_DEBUG_SYNC=1: synchronise after every launch and name the failing
+// one (source line) -- a debugging aid, off by default.
+static bool debug_sync() {
+    static const bool on = [] {
+        const char* e = std::getenv("QMSORT_DEBUG_SYNC");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 #define QCK_LAUNCH(led)                                                                      \
     do {                                                                                     \
         ++(led).launches;                                                                    \
         cudaError_t e_ = cudaGetLastError();                                                 \
+        if (e_ == cudaSuccess && debug_sync()) {                                             \
+            e_ = cudaDeviceSynchronize();                                                    \
+            std::fprintf(stderr, "qmsort debug: launch %d at qmsort_gpu.cu:%d %s\n",         \
+                         (led).launches, __LINE__, cudaGetErrorString(e_));                  \
+        }                                                                                    \
         if (e_ != cudaSuccess)                                                               \
-            return fail(QMSORT_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+            return fail(QMSORT_ECUDA, std::string("kernel launch (qmsort_gpu.cu:") +         \
+                                          std::to_string(__LINE__) + "): " + cudaGetErrorString(e_)); \
     } while (0)
 #define QLAUNCH(led, ph, bytes, ...) \
     do {                             \
@@ -779,6 +795,7 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
                 }
                 r[w] = lo;
             }
+            if (r[1] < r[0]) r[1] = r[0];  // a cell past key_max: empty range (see sample_segment)
             lut[c] = r[0] | ((r[1] - r[0]) << 16);
         }
     } else {

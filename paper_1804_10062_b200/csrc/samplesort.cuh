@@ -467,6 +467,11 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
                 if (w == 0) jl = lo2;
                 else jh = lo2;
             }
+            // cells past hi (cmin > cmax after the clamp) hold no real key, but
+            // the padding keys of a partial tile land in the last one: keep
+            // the range empty rather than negative (a negative count read as
+            // 0xFFFF sent the wide-cell search far outside the splitters)
+            if (jh < jl) jh = jl;
             lut[c] = jl | ((jh - jl) << 16);
         }
     } else {

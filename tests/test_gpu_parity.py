@@ -233,3 +233,19 @@ def test_u32_packed_spans(oracle, base, span, n):
     np.testing.assert_array_equal(got, np.sort(a))
     got, _ = gpu_sort(a, less="greater")
     np.testing.assert_array_equal(got, np.sort(a)[::-1])
+
+
+@pytest.mark.parametrize("dt", [DT_U64, DT_I64, DT_U32])
+@pytest.mark.parametrize("n", [5482783, 3000001])
+def test_skewed_window(oracle, dt, n):
+    """90 % of the keys in a window of 100 values, the rest spread wide: the
+    lower levels get segments whose key range is a single value or two, and
+    the padding keys of a partial tile fall into LUT cells past the range
+    (once read as a negative splitter count -- an out-of-bounds search)."""
+    rng = np.random.default_rng(n)
+    raw = rng.integers(0, 2**62, size=n, dtype=np.uint64)
+    m = rng.random(n) < 0.9
+    raw[m] = rng.integers(1000, 1100, size=int(m.sum()), dtype=np.uint64)
+    a = raw.astype(np.uint32) if dt == DT_U32 else (raw.view(np.int64) if dt == DT_I64 else raw)
+    got, _ = gpu_sort(a)
+    np.testing.assert_array_equal(got, oracle.sort(dt, a))

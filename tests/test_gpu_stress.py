@@ -1,0 +1,71 @@
+"""Randomised GPU stress (seeded, reproducible): dtype x comparator x preset x
+size x value distribution drawn at random, each sort checked byte-for-byte
+against the CPU oracle -- the reference's own fuzz (test_sort.cpp:59-77,
+acceptance.cpp:86-114) at sizes that exercise one and two partition levels,
+the packed 16-bit and record-prefix block sorts, the fused transform and the
+few-bin scatter."""
+import numpy as np
+import pytest
+
+import paper_1804_10062_b200 as q
+from oracle_lib import DT_F64, DT_I32, DT_I64, DT_REC32, DT_U32, DT_U64
+from test_gpu_parity import gpu_sort
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+PRESETS = [q.qms, q.qmqs, q.momqms, q.hqms]
+
+
+def _draw(rng, dt, n):
+    kind = rng.integers(0, 6)
+    w = (n, 4) if dt == DT_REC32 else (n,)
+    if kind == 0:  # full range
+        raw = rng.integers(0, 2**63, size=w, dtype=np.uint64) * 2 + rng.integers(0, 2, size=w, dtype=np.uint64)
+    elif kind == 1:  # narrow range (packed block sort territory)
+        raw = rng.integers(0, int(rng.integers(2, 1 << 20)), size=w, dtype=np.uint64) + np.uint64(rng.integers(0, 1 << 40))
+    elif kind == 2:  # few distinct
+        vals = rng.integers(0, 2**63, size=int(rng.integers(1, 40)), dtype=np.uint64)
+        raw = vals[rng.integers(0, len(vals), size=w)]
+    elif kind == 3:  # sorted runs
+        raw = np.sort(rng.integers(0, 2**40, size=w, dtype=np.uint64), axis=0)
+        if rng.integers(0, 2):
+            raw = raw[::-1].copy()
+    elif kind == 4:  # skew: most keys in a small window
+        raw = rng.integers(0, 2**62, size=w, dtype=np.uint64)
+        m = rng.random(w) < 0.9
+        raw[m] = rng.integers(1000, 1100, size=int(m.sum()), dtype=np.uint64)
+    else:  # organ pipe
+        i = np.arange(n, dtype=np.uint64)
+        raw = np.minimum(i + 1, np.uint64(n) - i)
+        if dt == DT_REC32:
+            raw = np.repeat(raw[:, None], 4, axis=1)
+    if dt == DT_I32:
+        return (raw & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.int32)
+    if dt == DT_U32:
+        return (raw & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    if dt == DT_U64:
+        return raw.astype(np.uint64)
+    if dt == DT_I64:
+        return raw.astype(np.uint64).view(np.int64)
+    if dt == DT_F64:
+        x = ((raw >> np.uint64(11)).astype(np.int64) - (1 << 51)).astype(np.float64) * 3.0e-5
+        x[x == 0] = 0.0
+        return x
+    r = raw.astype(np.uint64).copy()
+    if kind == 0:
+        r[:, 0] >>= np.uint64(52)
+    return r
+
+
+@pytest.mark.parametrize("case", range(120))
+def test_random_sorts(oracle, case):
+    rng = np.random.default_rng(1000 + case)
+    dt = [DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32, DT_I64][int(rng.integers(0, 6))]
+    cap = 1 << 21 if dt == DT_REC32 else 1 << 23
+    n = int(min(cap, 2 ** rng.uniform(0, 23)))
+    a = _draw(rng, dt, n)
+    greater = bool(rng.integers(0, 2))
+    preset = PRESETS[int(rng.integers(0, 4))]()
+    got, _ = gpu_sort(a, preset, "greater" if greater else "less")
+    np.testing.assert_array_equal(got, oracle.sort(dt, a, greater=greater))
