@@ -4,6 +4,8 @@ against the CPU oracle -- the reference's own fuzz (test_sort.cpp:59-77,
 acceptance.cpp:86-114) at sizes that exercise one and two partition levels,
 the packed 16-bit and record-prefix block sorts, the fused transform and the
 few-bin scatter."""
+import os
+
 import numpy as np
 import pytest
 
@@ -58,9 +60,14 @@ def _draw(rng, dt, n):
     return r
 
 
-@pytest.mark.parametrize("case", range(120))
+# QMSORT_STRESS_CASES / QMSORT_STRESS_SEED widen the sweep for one-off runs
+_CASES = int(os.environ.get("QMSORT_STRESS_CASES", "120"))
+_SEED = int(os.environ.get("QMSORT_STRESS_SEED", "1000"))
+
+
+@pytest.mark.parametrize("case", range(_CASES))
 def test_random_sorts(oracle, case):
-    rng = np.random.default_rng(1000 + case)
+    rng = np.random.default_rng(_SEED + case)
     dt = [DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32, DT_I64][int(rng.integers(0, 6))]
     cap = 1 << 21 if dt == DT_REC32 else 1 << 23
     n = int(min(cap, 2 ** rng.uniform(0, 23)))
