@@ -76,3 +76,59 @@ def test_random_sorts(oracle, case):
     preset = PRESETS[int(rng.integers(0, 4))]()
     got, _ = gpu_sort(a, preset, "greater" if greater else "less")
     np.testing.assert_array_equal(got, oracle.sort(dt, a, greater=greater))
+
+
+@pytest.mark.parametrize("case", range(max(1, _CASES // 3)))
+def test_random_elements(oracle, case):
+    """Key + payload elements (f3): random element size, key type/offset,
+    distribution and comparator; keys must equal the oracle's key sequence and
+    the arrangement the stable one."""
+    rng = np.random.default_rng(_SEED + 7919 + case)
+    key_dt = [DT_I32, DT_U32, DT_U64, DT_F64, DT_I64][int(rng.integers(0, 5))]
+    kw = 4 if key_dt in (DT_I32, DT_U32) else 8
+    eb = int(rng.choice([kw, 8, 16, 24, 32, 48, 64]))
+    eb = max(eb, kw)
+    key_off = int(rng.integers(0, (eb - kw) // kw + 1)) * kw
+    n = int(min(1 << 20, 2 ** rng.uniform(0, 20)))
+    k = _draw(rng, key_dt, n)
+    raw = rng.integers(0, 256, size=(n, eb), dtype=np.uint8)
+    raw[:, key_off:key_off + kw] = np.ascontiguousarray(k).view(np.uint8).reshape(n, kw)
+    less = "greater" if rng.integers(0, 2) else "less"
+    t = torch.from_numpy(raw.copy()).cuda()
+    q.sort_elements(t, key_dt, q.qms(), less, key_offset=key_off)
+    got = t.cpu().numpy()
+    np_dt = {DT_I32: np.int32, DT_U32: np.uint32, DT_U64: np.uint64, DT_F64: np.float64, DT_I64: np.int64}[key_dt]
+    keys = got[:, key_off:key_off + kw].copy().view(np_dt).reshape(-1)
+    np.testing.assert_array_equal(keys, oracle.sort(key_dt, k, greater=(less == "greater")))
+    if less == "greater":
+        _, inv = np.unique(k, return_inverse=True)
+        order = np.argsort(-inv, kind="stable")
+    else:
+        order = np.argsort(k, kind="stable")
+    np.testing.assert_array_equal(got, raw[order])
+
+
+@pytest.mark.parametrize("case", range(max(1, _CASES // 3)))
+def test_random_select_nth(oracle, case):
+    """select_nth (f4): random dtype, size, distribution, rank and comparator;
+    the k-th element equals the oracle's sorted[k-1] and the range is
+    partitioned around it."""
+    rng = np.random.default_rng(_SEED + 104729 + case)
+    dt = [DT_I32, DT_U32, DT_U64, DT_F64, DT_I64][int(rng.integers(0, 5))]
+    n = int(min(1 << 21, 2 ** rng.uniform(0, 21))) or 1
+    a = _draw(rng, dt, n)
+    greater = bool(rng.integers(0, 2))
+    k = int(rng.integers(1, n + 1))
+    t = torch.from_numpy(a.copy()).cuda()
+    p = q.select_nth(t, k, "greater" if greater else "less")
+    b = t.cpu().numpy()
+    s = oracle.sort(dt, a, greater=greater)
+    assert p == k - 1
+    np.testing.assert_array_equal(b[p:p + 1].view(np.uint8), s[k - 1:k].view(np.uint8))
+    np.testing.assert_array_equal(np.sort(b.view(np.uint8).reshape(n, -1).view(f"V{b.itemsize}").reshape(n)),
+                                  np.sort(a.view(np.uint8).reshape(n, -1).view(f"V{a.itemsize}").reshape(n)))
+    left, right = b[:p], b[p + 1:]
+    if greater:
+        assert (left.size == 0 or not (left < b[p]).any()) and (right.size == 0 or not (right > b[p]).any())
+    else:
+        assert (left.size == 0 or not (left > b[p]).any()) and (right.size == 0 or not (right < b[p]).any())
