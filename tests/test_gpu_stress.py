@@ -132,3 +132,25 @@ def test_random_select_nth(oracle, case):
         assert (left.size == 0 or not (left < b[p]).any()) and (right.size == 0 or not (right > b[p]).any())
     else:
         assert (left.size == 0 or not (left > b[p]).any()) and (right.size == 0 or not (right < b[p]).any())
+
+
+@pytest.mark.parametrize("case", range(max(1, _CASES // 6)))
+def test_random_sharded_fused(oracle, case):
+    """The distributed samplesort with the exchange fused into the scatter
+    (peer stores), P ranks emulated on one GPU: random P, dtype, ragged shard
+    sizes, distribution and comparator; the concatenated slices equal the
+    oracle's sort of the whole array."""
+    from paper_1804_10062_b200 import sharded
+    rng = np.random.default_rng(_SEED + 15485863 + case)
+    dt = [DT_I32, DT_U32, DT_U64, DT_F64, DT_REC32, DT_I64][int(rng.integers(0, 6))]
+    P = int(rng.integers(1, 9))
+    n = int(min(1 << 21, 2 ** rng.uniform(4, 21)))
+    a = _draw(rng, dt, n)
+    cuts = np.sort(rng.integers(0, n + 1, size=P - 1))
+    bounds = [0, *cuts.tolist(), n]
+    shards = [torch.from_numpy(np.ascontiguousarray(a[bounds[i]:bounds[i + 1]])).cuda() for i in range(P)]
+    greater = bool(rng.integers(0, 2))
+    out = sharded.sort_sharded_emulated_fused(shards, "greater" if greater else "less", dtype=dt)
+    torch.cuda.synchronize()
+    got = np.concatenate([o.cpu().numpy() for o in out])
+    np.testing.assert_array_equal(got, oracle.sort(dt, a, greater=greater))
