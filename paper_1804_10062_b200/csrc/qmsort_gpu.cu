@@ -93,7 +93,9 @@ template <>
 struct Tune<uint32_t> {
     static constexpr int LOGKMAX = 9;
     static constexpr int BI = 32;                                 // block sort keys / thread
-    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};  // block sort classes
+    // block sort classes (96: tiles just over 2048 keys keep all three warps
+    // busy; trailing repeats are never chosen -- kNumClasses is the widest list)
+    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512};
     static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     // last level: 3/4 of the target, so most tiles stay inside the packed
     // 16-bit block sort's span (measured: block sort 1817 -> 1716 us on C2)
@@ -107,7 +109,7 @@ template <>
 struct Tune<uint64_t> {
     static constexpr int LOGKMAX = 9;
     static constexpr int BI = 16;
-    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};
+    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 192, 256, 384, 512};  // measured: C3 block sort -7 %
     static constexpr int TARGET_DIV = 4;
     static constexpr int LAST_NUM = 1, LAST_DEN = 1;
     static constexpr int ST = 512, SI = 16;
@@ -119,7 +121,7 @@ template <>
 struct Tune<Rec32> {
     static constexpr int LOGKMAX = 8;
     static constexpr int BI = 8;
-    static constexpr int CLS_T[kNumClasses] = {64, 128, 256, 512};
+    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512};
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 1;
     static constexpr int ST = 512, SI = 8;
@@ -353,15 +355,21 @@ static int launch_tiles(const K* src, K* dst, uint64_t off, uint64_t len, cudaSt
     return QMSORT_OK;
 }
 
+template <class K, int C>
+static int blocksort_one_from(const K* src, K* dst, uint64_t off, uint64_t len, cudaStream_t st,
+                              Ledger& led) {
+    if constexpr (C + 1 < kNumClasses) {
+        if (len > class_cap<K>(C)) return blocksort_one_from<K, C + 1>(src, dst, off, len, st, led);
+    }
+    return launch_tiles<K, Tune<K>::CLS_T[C], Tune<K>::BI>(src, dst, off, len, st, led);
+}
+
 // Sort [off, off+len) with len <= the cap: one CTA of the smallest class.
 template <class K>
 static int blocksort_one(const K* src, K* dst, uint64_t off, uint64_t len, cudaStream_t st,
                          Ledger& led) {
     using TU = Tune<K>;
-    if (len <= class_cap<K>(0)) return launch_tiles<K, TU::CLS_T[0], TU::BI>(src, dst, off, len, st, led);
-    if (len <= class_cap<K>(1)) return launch_tiles<K, TU::CLS_T[1], TU::BI>(src, dst, off, len, st, led);
-    if (len <= class_cap<K>(2)) return launch_tiles<K, TU::CLS_T[2], TU::BI>(src, dst, off, len, st, led);
-    return launch_tiles<K, TU::CLS_T[3], TU::BI>(src, dst, off, len, st, led);
+    return blocksort_one_from<K, 0>(src, dst, off, len, st, led);
 }
 
 // Block-sort the `count` tasks of size class C into A: one CTA per task.
@@ -375,6 +383,15 @@ static int launch_class(const SortTask* tasks, uint32_t count, K* A, const K* B,
     auto fn = blocksort_tasks_kernel<K, T, TU::BI>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
     QLAUNCH(led, kPhBlocksort, 0, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, A, B, xf));
+    return QMSORT_OK;
+}
+
+// Every size class's task list, smallest first.
+template <class K, int C>
+static int launch_classes_from(const SortTask* tasks, uint32_t task_cap, const uint32_t* nt, K* A,
+                               const K* B, cudaStream_t st, Ledger& led, Xf xf) {
+    QTRY((launch_class<K, C>(tasks + (size_t)C * task_cap, nt[C], A, B, st, led, xf)));
+    if constexpr (C + 1 < kNumClasses) return launch_classes_from<K, C + 1>(tasks, task_cap, nt, A, B, st, led, xf);
     return QMSORT_OK;
 }
 
@@ -561,10 +578,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     const uint32_t* nt = hc[kCntSlots - 1].ntasks;
     for (int c = 0; c < kNumClasses; ++c)
         if (nt[c] > L.task_cap) return fail(QMSORT_EINTERNAL, "block-sort task list capacity exceeded");
-    QTRY((launch_class<K, 0>(tasks + 0 * (size_t)L.task_cap, nt[0], A, B, st, led, xf)));
-    QTRY((launch_class<K, 1>(tasks + 1 * (size_t)L.task_cap, nt[1], A, B, st, led, xf)));
-    QTRY((launch_class<K, 2>(tasks + 2 * (size_t)L.task_cap, nt[2], A, B, st, led, xf)));
-    QTRY((launch_class<K, 3>(tasks + 3 * (size_t)L.task_cap, nt[3], A, B, st, led, xf)));
+    QTRY((launch_classes_from<K, 0>(tasks, L.task_cap, nt, A, B, st, led, xf)));
     if (hc[kCntSlots - 1].nfill)
         QLAUNCH(led, kPhFill, 0, fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, L.fill_cap, A, xf));
     // pass ledger from the device counters (count 1, scatter 2, block sort 2, fill 1)

@@ -40,7 +40,7 @@
 
 namespace qmsort_b200 {
 
-constexpr int kNumClasses = 4;  // block-sort size classes
+constexpr int kNumClasses = 7;  // block-sort size classes (Tune<K>::CLS_T)
 constexpr int kLutMaxBits = 12;
 constexpr int kLutPerSplitter = 16;  // LUT words reserved per splitter slot
 
