@@ -125,7 +125,7 @@ struct Tune<Rec32> {
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 1;
     static constexpr int ST = 512, SI = 8;
-    static constexpr int XT = 256, XI = 8;
+    static constexpr int XT = 512, XI = 4;  // measured: C5 scatter 2.84 -> 2.73 ms (was 256 x 8)
     static constexpr int CT = 256, CU = 4;
     static constexpr int MT = 512, MI = 8;
 };
