@@ -11,9 +11,14 @@ the end-to-end number through the host-array drop-in call (e2e).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-With N > 1 (torchrun, one rank per GPU) every rank holds 2^28 keys and the
-ranks run the distributed samplesort (sharded.py): global splitters, one NCCL
-all-to-all, local sorts -- weak scaling, whole-job keys/s.
+With N > 1 every rank is one process on one GPU (launched by the driver under
+torchrun, or -- when WORLD_SIZE is unset -- by bench.py re-executing itself
+under torch.distributed.run) and the ranks run the distributed samplesort
+(sharded.py): global splitters, the exchange fused into the partition's
+scatter (peer stores over NVLink), local sorts.  Default: the C2 recipe with
+2^28 uint32 keys per GPU (weak scaling, whole-job keys/s); --config c3 / c5:
+the north-star sharded configs, 2^30 uint64 keys / 2^26 32-byte records in
+total (strong scaling).  --sharded runs that path at N = 1 too.
 """
 from __future__ import annotations
 
@@ -27,6 +32,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -34,7 +41,7 @@ METRIC = "sorted Gkeys/s at n=2^28 uint32 (1-8 B200); achieved HBM GB/s vs roofl
 UNIT = "Gkeys/s"
 N_DEFAULT = 1 << 28
 SEED = 42
-CPU_SAMPLE = 1 << 24  # bounded CPU sample (~3 s per qms() sort on one core)
+CPU_WARM = 1 << 24  # reference-arm warm-up sorts: a 2^24 prefix
 # BASELINE.json configs runnable with device generators: (dtype attr, torch dtype,
 # row shape, generator attr, n, key bytes, description)
 CONFIGS = {
@@ -61,7 +68,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: skip extras")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2",
-                    help="BASELINE config (c2 is the headline; the others are informational)")
+                    help="BASELINE config (c2 is the headline; the others are informational; "
+                         "c3 / c5 are the sharded north-star configs with --gpus N / --sharded)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the distributed samplesort path even on one GPU (exercises NCCL)")
     ap.add_argument("--exchange", choices=["peer", "nccl"], default="peer",
@@ -123,86 +131,157 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU legs: the reference QuickMergesort (oracle/_ref) or the C restatement
 # ---------------------------------------------------------------------------
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
 def cpu_lib():
-    ref = os.path.join(ROOT, "oracle", "_ref", "libqmsref.so")
-    if os.path.exists(ref):
-        lib = ctypes.CDLL(ref)
-        lib.qmsref_sort.argtypes = [ctypes.c_int] * 5 + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
-        return "reference", lambda a, std=False: lib.qmsref_sort(
-            1, 0, 0, 0, int(std), a.ctypes.data_as(ctypes.c_void_p), a.shape[0], None)
+    """The reference QuickMergesort on this host: the reference headers
+    compiled here with -O3 -march=native -funroll-loops from the preprocessed
+    translation unit (oracle/_ref/ref_shim.ii, `make -C oracle native`), else
+    the prebuilt -O3 build (oracle/_ref/libqmsref.so), else the C restatement."""
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    paths = []
+    if os.path.exists(os.path.join(ref_dir, "ref_shim.ii")):
+        r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "native"],
+                           stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        if r.returncode == 0:
+            paths.append((os.path.join(ref_dir, "libqmsref_native.so"), "-O3 -march=native -funroll-loops"))
+    paths.append((os.path.join(ref_dir, "libqmsref.so"), "-O3 (prebuilt)"))
+    for ref, flags in paths:
+        if os.path.exists(ref):
+            lib = ctypes.CDLL(ref)
+            lib.qmsref_sort.argtypes = [ctypes.c_int] * 5 + [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+            return "reference", flags, lambda a, std=False: lib.qmsref_sort(
+                1, 0, 0, 0, int(std), a.ctypes.data_as(ctypes.c_void_p), a.shape[0], None)
     port = os.path.join(ROOT, "oracle", "liboracle.so")
     if not os.path.exists(port):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")], check=True)
     lib = ctypes.CDLL(port)
     lib.qmso_sort.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]
-    return "port", lambda a, std=False: lib.qmso_sort(1, 0, 0, a.ctypes.data_as(ctypes.c_void_p), a.shape[0])
+    return "port", "-O3", lambda a, std=False: lib.qmso_sort(1, 0, 0, a.ctypes.data_as(ctypes.c_void_p), a.shape[0])
 
 
 def host_input(n: int):
-    """C2 recipe on the host: u32[i] = SplitMix64(seed)_i >> 32 (numpy, vectorised)."""
+    """C2 recipe on the host: u32[i] = SplitMix64(seed)_i >> 32 (numpy, vectorised, in blocks)."""
     import numpy as np
-    j = np.arange(1, n + 1, dtype=np.uint64)
-    with np.errstate(over="ignore"):
-        z = np.uint64(SEED) + j * np.uint64(0x9E3779B97F4A7C15)
-        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
-        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
-        z = z ^ (z >> np.uint64(31))
-    return (z >> np.uint64(32)).astype(np.uint32)
-
-
-def cpu_baseline(reps: int = 3) -> dict:
-    kind, fn = cpu_lib()
-    base = host_input(CPU_SAMPLE)
-    times, std_times = [], []
-    for _ in range(reps):
-        a = base.copy()
-        t = time.perf_counter()
-        fn(a)
-        times.append(time.perf_counter() - t)
-    if kind == "reference":
-        a = base.copy()
-        t = time.perf_counter()
-        fn(a, std=True)
-        std_times.append(time.perf_counter() - t)
-    best = min(times)
-    out = {"value": CPU_SAMPLE / best / 1e9, "unit": UNIT, "cores": 1, "kind": kind,
-           "sample": f"qmsort::sort(qms(), std::less) on the first 2^24 keys of the C2 input, "
-                     f"best of {reps}, 1 of {os.cpu_count()} host cores (single-threaded reference)"}
-    if std_times:
-        out["std_sort_value"] = CPU_SAMPLE / min(std_times) / 1e9
+    out = np.empty(n, dtype=np.uint32)
+    blk = 1 << 24
+    for s0 in range(0, n, blk):
+        m = min(blk, n - s0)
+        j = np.arange(s0 + 1, s0 + m + 1, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            z = np.uint64(SEED) + j * np.uint64(0x9E3779B97F4A7C15)
+            z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+        out[s0:s0 + m] = (z >> np.uint64(32)).astype(np.uint32)
     return out
 
 
+class PinnedCore:
+    """Run the single-threaded reference on one host core (the reference
+    cannot use more than one thread per sort)."""
+
+    def __init__(self):
+        self.core = None
+        self.prev = None
+
+    def __enter__(self):
+        try:
+            self.prev = os.sched_getaffinity(0)
+            self.core = max(self.prev)  # the last allowed core (core 0 takes the interrupts)
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.core = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            os.sched_setaffinity(0, self.prev)
+
+
+def cpu_baseline(n: int = N_DEFAULT) -> dict:
+    """The reference qms() and std::sort on the SAME host array the GPU sorts
+    (the full C2 input), one sort each, pinned to one core."""
+    kind, flags, fn = cpu_lib()
+    base = host_input(n)
+    a = base.copy()
+    with PinnedCore() as pc:
+        t = time.perf_counter()
+        fn(a)
+        qms_s = time.perf_counter() - t
+        a[:] = base
+        t = time.perf_counter()
+        if kind == "reference":
+            fn(a, std=True)
+        std_s = time.perf_counter() - t if kind == "reference" else None
+    return {"value": n / qms_s / 1e9, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"qmsort::sort(qms(), std::less) on the full C2 array (2^{n.bit_length() - 1} uint32, the "
+                      f"GPU's input), one sort, single-threaded reference built {flags}, pinned to core "
+                      f"{pc.core} of {os.cpu_count()} ({cpu_model()})",
+            "seconds": qms_s, "std_sort_value": (n / std_s / 1e9) if std_s else None,
+            "std_sort_seconds": std_s, "cpu_model": cpu_model(), "host_cores": os.cpu_count(),
+            "build_flags": flags}
+
+
 def run_reference(args) -> None:
-    """--impl reference: the reference CPU QuickMergesort on the host cores."""
+    """--impl reference: the reference CPU QuickMergesort on the host, on our
+    arm's workload: every timed step sorts a fresh copy of the full 2^28 C2
+    array (single-threaded, pinned to one core).  The W warm-up steps sort a
+    2^24 prefix (a CPU sort has nothing to warm beyond caches and pages)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    kind, fn = cpu_lib()
-    base = host_input(CPU_SAMPLE)
-    for _ in range(args.warmup):
-        a = base.copy()
-        fn(a)
-    times = []
-    for _ in range(args.steps):
-        a = base.copy()
-        t = time.perf_counter()
-        fn(a)
-        times.append(time.perf_counter() - t)
+    kind, flags, fn = cpu_lib()
+    n = args.n
+    base = host_input(n)
+    a = base.copy()
+    times, std_s = [], None
+    with PinnedCore() as pc:
+        for _ in range(args.warmup):
+            w = base[: min(n, CPU_WARM)].copy()
+            fn(w)
+        for _ in range(args.steps):
+            a[:] = base
+            t = time.perf_counter()
+            fn(a)
+            times.append(time.perf_counter() - t)
+        if kind == "reference":
+            a[:] = base
+            t = time.perf_counter()
+            fn(a, std=True)
+            std_s = time.perf_counter() - t
     ms = statistics.mean(times) * 1e3
-    value = CPU_SAMPLE / (ms / 1e3) / 1e9
-    sample = (f"each step: qmsort::sort(qms()) of the first 2^24 keys of the C2 input "
-              f"(bounded sample of the 2^28 workload); single-threaded reference, 1 of "
-              f"{os.cpu_count()} host cores")
+    value = n / (ms / 1e3) / 1e9
+    sample = (f"each step: qmsort::sort(qms(), std::less) of a fresh copy of the full C2 array (2^{n.bit_length() - 1} "
+              f"uint32, the workload our arm sorts); single-threaded reference built {flags}, pinned to core "
+              f"{pc.core} of {os.cpu_count()} ({cpu_model()}); warm-up steps sort a 2^24 prefix")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe)",
-            "config": {"workload": "C2 uint32 uniform, CPU sample 2^24 keys", "n": CPU_SAMPLE},
+            "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe, seed 42)",
+            "config": workload_config(n),
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+            "step_ms": [round(t * 1e3, 1) for t in times],
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample,
+                             "cpu_model": cpu_model(), "host_cores": os.cpu_count(), "build_flags": flags,
+                             "std_sort_value": (n / std_s / 1e9) if std_s else None},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(n: int) -> dict:
+    """The workload both arms run (BASELINE.json configs[1])."""
+    return {"workload": f"C2: sort n=2^{n.bit_length() - 1} uint32 i.i.d. uniform (seeded SplitMix64, seed 42), "
+                        "qms() preset", "n": n, "key_bytes": 4}
 
 
 # ---------------------------------------------------------------------------
@@ -312,10 +391,10 @@ def run_ours(args) -> None:
             "scaling": "weak", "vs_baseline": None,
             "dtype": {"DT_U32": "u32", "DT_U64": "u64", "DT_F64": "f64", "DT_REC32": "4xu64"}[dt_name],
             "data": f"synthetic (seeded SplitMix64, SURVEY.md 8(d) {args.config.upper()} recipe, seed 42)",
-            "config": {"workload": f"{desc}, qms() preset, 1 B200",
-                       "n": n, "key_bytes": kb, "algorithm": args.algorithm,
-                       "l2": "flushed (256 MiB write) before every timed step; input > L2",
-                       "parallelism": "single GPU"},
+            "config": (workload_config(n) if args.config == "c2"
+                       else {"workload": f"{desc}, qms() preset", "n": n, "key_bytes": kb}),
+            "setup": {"algorithm": args.algorithm, "parallelism": "single B200",
+                      "l2": "flushed (256 MiB write) before every timed step; input > L2"},
             "step_ms": [round(t, 4) for t in times],
             "gpu_launches": launches, "clocks": clk, "roofline": roofline,
             "sort_roofline": sort_roofline}
@@ -323,7 +402,7 @@ def run_ours(args) -> None:
     if not args.no_e2e:
         line["e2e"] = e2e(q, torch, n, pristine, cfg, args)
     if not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline()
+        line["cpu_baseline"] = cpu_baseline(n)
     print(json.dumps(line), flush=True)
 
 
@@ -368,8 +447,29 @@ def e2e(q, torch, n, pristine, cfg, args) -> dict:
                    "one array per step"}
 
 
+def relaunch_under_torchrun(args) -> None:
+    """--gpus N > 1 without a torchrun environment: re-execute this script as N
+    ranks (one process per GPU) through torch.distributed.run; rank 0 prints
+    the line."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+    if have < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} GPU(s) visible")
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     if args.quick:
         args.no_cpu_baseline = True
         args.no_e2e = True

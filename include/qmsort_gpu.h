@@ -183,8 +183,8 @@ int qmsort_gpu_sample(int core_dtype, const void* d_data, size_t n, size_t s, ui
 /* One partition level with caller-given sorted splitters (core dtype):
  * bucket b = #{splitters < key} (b in [0, nsplit]); writes d_in permuted so
  * that buckets are contiguous and ascending into d_out and the bucket sizes
- * into d_counts[0..nsplit] (uint64).  nsplit <= 1023.  Uses d_ws (see
- * qmsort_gpu_partition_workspace_bytes) or allocates if NULL. */
+ * into d_counts[0..nsplit] (uint64).  nsplit <= 511 (255 for REC32).  Uses
+ * d_ws (see qmsort_gpu_partition_workspace_bytes) or allocates if NULL. */
 size_t qmsort_gpu_partition_workspace_bytes(int core_dtype, size_t n);
 int qmsort_gpu_partition(int core_dtype, const void* d_in, size_t n, const void* d_splitters,
                          uint32_t nsplit, void* d_out, uint64_t* d_counts, void* d_ws,
@@ -204,6 +204,64 @@ int qmsort_gpu_partition_count(int core_dtype, const void* d_in, size_t n, const
 int qmsort_gpu_partition_scatter_peers(int core_dtype, const void* d_in, size_t n, uint32_t nsplit,
                                        void* const* dests, const uint64_t* dest_offsets,
                                        void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- the distributed samplesort ------------------------ */
+/* Single-process entry over P <= 8 devices (one host thread drives them all):
+ * rank r holds d_in[r][0..n_in[r]) (caller dtype, on device devices[r];
+ * read only).  The call sorts the union of all ranks' keys under cmp and
+ * leaves the r-th slice of the global order in d_out[r] (capacity out_cap[r]
+ * elements, on devices[r]), its length in out_n[r]: concatenating the slices
+ * in rank order gives the sorted array.  Global splitters from a seeded
+ * sample, one exchange fused into the partition's scatter (each rank's kernel
+ * stores straight into the peers' receive buffers over NVLink; peer access is
+ * enabled between distinct devices), then local sorts.  A device may be listed
+ * more than once (P ranks on one GPU run the same kernels and exchange).
+ * QMSORT_ENOWS if some out_cap[r] < out_n[r] (out_n holds the sizes needed).
+ * metrics: elapsed_ns = host wall time of the call, launches and pass bytes
+ * summed over the ranks.  Replaces, for a sharded array, the reference entry
+ * qmsort::sort (sort.hpp:215-226), which has no distributed form. */
+int qmsort_gpu_sort_sharded(int dtype, int cmp, uint32_t P, const int* devices,
+                            const void* const* d_in, const size_t* n_in, void* const* d_out,
+                            const size_t* out_cap, size_t* out_n, const qmsort_gpu_config* cfg,
+                            qmsort_gpu_metrics* metrics);
+
+/* The same algorithm as steps a rank runs (one process per GPU; the caller
+ * carries the small host collectives -- samples, the count matrix -- and the
+ * receive-buffer handles, e.g. over torch.distributed):
+ *   1. shard_sample: s seeded keys of the rank's caller-dtype data, mapped
+ *      into the core key domain (seed: cfg.seed ^ 0x9E3779B97F4A7C15 * (r+1));
+ *   2. (all ranks' samples gathered and sorted as core keys, e.g. with
+ *      qmsort_gpu_sort) shard_splitters: P-1 quantile splitters, merged into
+ *      nuniq distinct values with multiplicities (host only);
+ *   3. shard_count: three-way counts, 2 nuniq + 1 bins (bin 2j: keys between
+ *      splitters j-1 and j; 2j+1: keys equal to splitter j); the plan stays
+ *      in d_ws (shard_workspace_bytes);
+ *   4. shard_plan (host only, identical on every rank) from the P x (2 nuniq
+ *      + 1) count matrix (row = sender): bin -> rank (-1: an equal-key run
+ *      spread over several ranks as fills), per-sender offsets in the
+ *      receivers' buffers, receive sizes and fills;
+ *   5. shard_scatter: the rank's bins straight into rank_dest[] (its row of
+ *      bin_off), peer memory or local;
+ *   6. shard_finish: [lo fill | sorted received keys | hi fill] into d_out,
+ *      the received keys sorted out of place (d_recv is only read).
+ * Receive buffers and d_out hold caller-dtype keys. */
+size_t qmsort_gpu_shard_workspace_bytes(int dtype, size_t n);
+int qmsort_gpu_shard_sample(int dtype, int cmp, const void* d_in, size_t n, size_t s, uint64_t seed,
+                            void* d_out_core, void* stream);
+int qmsort_gpu_shard_splitters(int core_dtype, const void* h_sorted_sample, size_t m, uint32_t P,
+                               void* h_uniq, uint32_t* h_mult, uint32_t* nuniq);
+int qmsort_gpu_shard_count(int dtype, int cmp, const void* d_in, size_t n, const void* d_uniq,
+                           uint32_t nuniq, uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream);
+int qmsort_gpu_shard_plan(uint32_t P, uint32_t nuniq, const uint32_t* h_mult, const uint64_t* h_counts,
+                          int32_t* h_bin_rank, uint64_t* h_bin_off, uint64_t* h_recv_n,
+                          uint64_t* h_lo_fill, uint64_t* h_hi_fill, int32_t* h_lo_val, int32_t* h_hi_val);
+int qmsort_gpu_shard_scatter(int dtype, int cmp, const void* d_in, size_t n, uint32_t nuniq,
+                             const int32_t* h_bin_rank, const uint64_t* h_bin_off, void* const* rank_dest,
+                             uint32_t P, void* d_ws, size_t ws_bytes, void* stream);
+int qmsort_gpu_shard_finish(int dtype, int cmp, const void* d_recv, size_t n_recv, const void* d_uniq,
+                            int32_t lo_val, uint64_t lo_fill, int32_t hi_val, uint64_t hi_fill, void* d_out,
+                            const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes,
+                            qmsort_gpu_metrics* metrics, void* stream);
 
 /* CUDA IPC for the receive buffers of the fused exchange (one process per
  * GPU): export the allocation holding d_ptr (handle + d_ptr's byte offset in

@@ -96,6 +96,14 @@ EXPORTED = [
     "qmsort_gpu_ipc_handle",
     "qmsort_gpu_ipc_open",
     "qmsort_gpu_ipc_close",
+    "qmsort_gpu_sort_sharded",
+    "qmsort_gpu_shard_workspace_bytes",
+    "qmsort_gpu_shard_sample",
+    "qmsort_gpu_shard_splitters",
+    "qmsort_gpu_shard_count",
+    "qmsort_gpu_shard_plan",
+    "qmsort_gpu_shard_scatter",
+    "qmsort_gpu_shard_finish",
 ]
 
 _lib = None
@@ -114,6 +122,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         )
     lib = ctypes.CDLL(p)
     vp, sz, u64, i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int
+    u32, i32 = ctypes.c_uint32, ctypes.c_int32
     cfgp, mp = ctypes.POINTER(GpuConfig), ctypes.POINTER(GpuMetrics)
     sig = {
         "qmsort_gpu_config_init": (None, [cfgp, i]),
@@ -143,6 +152,18 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_ipc_handle": (i, [vp, vp, ctypes.POINTER(u64)]),
         "qmsort_gpu_ipc_open": (i, [vp, u64, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
         "qmsort_gpu_ipc_close": (i, [vp]),
+        "qmsort_gpu_sort_sharded": (i, [i, i, u32, ctypes.POINTER(i), ctypes.POINTER(vp), ctypes.POINTER(sz),
+                                        ctypes.POINTER(vp), ctypes.POINTER(sz), ctypes.POINTER(sz), cfgp, mp]),
+        "qmsort_gpu_shard_workspace_bytes": (sz, [i, sz]),
+        "qmsort_gpu_shard_sample": (i, [i, i, vp, sz, sz, u64, vp, vp]),
+        "qmsort_gpu_shard_splitters": (i, [i, vp, sz, u32, vp, ctypes.POINTER(u32), ctypes.POINTER(u32)]),
+        "qmsort_gpu_shard_count": (i, [i, i, vp, sz, vp, u32, vp, vp, sz, vp]),
+        "qmsort_gpu_shard_plan": (i, [u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u64), ctypes.POINTER(i32),
+                                      ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                      ctypes.POINTER(u64), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+        "qmsort_gpu_shard_scatter": (i, [i, i, vp, sz, u32, ctypes.POINTER(i32), ctypes.POINTER(u64),
+                                         ctypes.POINTER(vp), u32, vp, sz, vp]),
+        "qmsort_gpu_shard_finish": (i, [i, i, vp, sz, vp, i32, u64, i32, u64, vp, cfgp, vp, sz, mp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

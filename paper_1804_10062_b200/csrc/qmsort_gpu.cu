@@ -21,8 +21,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
+#include <thread>
 #include <string>
+#include <chrono>
+#include <map>
+#include <set>
 #include <unordered_map>
 #include <unordered_set>
 #include <vector>
@@ -197,15 +202,23 @@ struct Ledger {
     }
 };
 
-// Raise the dynamic shared-memory limit of a kernel once per process.
+// Raise the dynamic shared-memory limit of a kernel once per (device,
+// kernel): the attribute belongs to the device context, so a process that
+// sorts on several GPUs sets it on each.
+static int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
 static cudaError_t allow_smem(const void* fn, size_t bytes) {
     static std::mutex mu;
-    static std::unordered_set<const void*> done;
+    static std::set<std::pair<int, const void*>> done;
     if (bytes <= 48 * 1024) return cudaSuccess;
+    const auto key = std::make_pair(current_device(), fn);
     std::lock_guard<std::mutex> g(mu);
-    if (done.count(fn)) return cudaSuccess;
+    if (done.count(key)) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e == cudaSuccess) done.insert(fn);
+    if (e == cudaSuccess) done.insert(key);
     return e;
 }
 
@@ -275,20 +288,22 @@ static int read_small(cudaStream_t st, void* dst0, const void* src0, size_t b0,
     return QMSORT_OK;
 }
 
-// Grid size of a persistent kernel: resident CTAs per SM x SMs (cached).
+// Grid size of a persistent kernel: resident CTAs per SM x SMs (cached per
+// device and kernel).
 static unsigned resident_grid(const void* fn, int threads, size_t smem) {
     static std::mutex mu;
-    static std::unordered_map<const void*, unsigned> cache;
+    static std::map<std::pair<int, const void*>, unsigned> cache;
+    const int dev = current_device();
+    const auto key = std::make_pair(dev, fn);
     std::lock_guard<std::mutex> g(mu);
-    auto it = cache.find(fn);
+    auto it = cache.find(key);
     if (it != cache.end()) return it->second;
-    int dev = 0, sms = 148, per_sm = 1;
-    cudaGetDevice(&dev);
+    int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
     const unsigned r = (unsigned)(per_sm * sms);
-    cache[fn] = r;
+    cache[key] = r;
     return r;
 }
 
@@ -447,9 +462,11 @@ static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStr
 
 // xf (fused transform): level 0 reads the caller's keys through f, every
 // final write (block sort, fills, merge fallback) goes through f^-1.
+// src0 (optional): level 0 reads the keys from there instead of A (an
+// out-of-place sort; src0 is only read).
 template <class K>
 static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
-                      const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf) {
+                      const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf, const K* src0 = nullptr) {
     const bool fused = xf.a != 0 || xf.b != 0;
     using TU = Tune<K>;
     constexpr uint32_t cap = class_cap<K>(kNumClasses - 1);
@@ -514,7 +531,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     const unsigned plan_grid = resident_grid((const void*)plan_fn, 512, 0);
     const unsigned colsum_grid = resident_grid((const void*)colsum_kernel, 512, 0);
 
-    K* src = A;
+    K* src = src0 ? const_cast<K*>(src0) : A;  // level 0 only reads it
     K* dst = B;
     const int max_levels = std::min(cfg.max_levels > 0 ? cfg.max_levels : 8, kCntSlots - 2);
     int level = 0;
@@ -548,7 +565,10 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                     scatter_fn<<<scatter_grid, TU::XT, sizeof(SM), st>>>(
                         lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks, &c->work_scatter, src, dst,
                         tree[cur], sorted[cur], lut[cur], hist, PeerArgs{}, lxf));
-            std::swap(src, dst);
+            // A and B alternate; an out-of-place source is left after level 0
+            K* prev = src;
+            src = dst;
+            dst = (prev == A || prev == B) ? prev : A;
         }
         // one control read per batch
         QTRY(read_small(st, hc, cnts, sizeof(LevelCounters) * (size_t)(level + 1), &hc[kCntSlots - 1],
@@ -602,14 +622,21 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
 
 // xf: the caller's keys are f^-1(core keys); the samplesort path fuses f and
 // f^-1 into its first reads and last writes, the others run them as passes.
+// src0 (optional): sort the n keys at src0 into A (src0 is only read).
 template <class K>
 static int sort_core(K* A, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
-                     const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf = Xf{0, 0}) {
+                     const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf = Xf{0, 0},
+                     const K* src0 = nullptr) {
     constexpr uint64_t cap = class_cap<K>(kNumClasses - 1);
-    if (n <= 1) return QMSORT_OK;
+    if (src0 == A) src0 = nullptr;
+    if (n <= 1) {
+        if (n == 1 && src0) QCK(cudaMemcpyAsync(A, src0, sizeof(K), cudaMemcpyDeviceToDevice, st));
+        return QMSORT_OK;
+    }
     const bool fused = xf.a != 0 || xf.b != 0;
     K* B = reinterpret_cast<K*>(ws + L.b_off);
-    if (n > cap && cfg.algorithm != 1) return samplesort<K>(A, B, n, cfg, ws, L, st, led, xf);
+    if (n > cap && cfg.algorithm != 1) return samplesort<K>(A, B, n, cfg, ws, L, st, led, xf, src0);
+    if (src0) QCK(cudaMemcpyAsync(A, src0, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
     if (fused) QTRY(xf_range<K>(A, n, xf, false, st, led));
     if (n <= cap) QTRY(blocksort_one<K>(A, A, 0, n, st, led));
     else QTRY(mergesort_range<K>(A, A, B, 0, n, st, led));
@@ -710,9 +737,15 @@ static void fill_metrics(qmsort_gpu_metrics* m, Ledger& led, float ms) {
     led.collect(m->phase_ns);
 }
 
+// src (optional): sort the n keys at src into d, leaving src untouched.
 static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_config* cfgp,
-                       void* wsp, size_t ws_bytes, qmsort_gpu_metrics* m, cudaStream_t st) {
+                       void* wsp, size_t ws_bytes, qmsort_gpu_metrics* m, cudaStream_t st,
+                       const void* src = nullptr) {
     QTRY(validate(dt, cmp, n, d));
+    if (src == d) src = nullptr;
+    if (src && n > 0 && ((const char*)src < (const char*)d + n * dtype_size(dt)) &&
+        ((const char*)d < (const char*)src + n * dtype_size(dt)))
+        return fail(QMSORT_EINVAL, "source and destination ranges overlap");
     qmsort_gpu_config cfg;
     if (cfgp) cfg = *cfgp;
     else qmsort_gpu_config_init(&cfg, 0);
@@ -725,6 +758,7 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     } else if (n > 1 && ws_bytes < need) {
         return fail(QMSORT_ENOWS, "workspace too small: need " + std::to_string(need) + " bytes");
     }
+    if (src && n == 1) QCK(cudaMemcpyAsync(d, src, dtype_size(dt), cudaMemcpyDeviceToDevice, st));
     Ledger led;
     led.prof = cfg.profile != 0;
     led.st = st;
@@ -739,13 +773,16 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     unsigned char* w = static_cast<unsigned char*>(ws);
     switch (core_dtype(dt)) {
         case QMSORT_DT_U32:
-            rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w, make_layout<uint32_t>(n), st, led, xf);
+            rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w, make_layout<uint32_t>(n), st, led, xf,
+                                     static_cast<const uint32_t*>(src));
             break;
         case QMSORT_DT_U64:
-            rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w, make_layout<uint64_t>(n), st, led, xf);
+            rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w, make_layout<uint64_t>(n), st, led, xf,
+                                     static_cast<const uint64_t*>(src));
             break;
         case QMSORT_DT_REC32:
-            rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n), st, led, xf);
+            rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n), st, led, xf,
+                                  static_cast<const Rec32*>(src));
             break;
     }
     cudaEventRecord(e1, st);
@@ -776,12 +813,14 @@ __global__ void gather_sample_kernel(const K* __restrict__ src, uint64_t n, uint
 }
 
 // Classifier (LUT or Eytzinger tree) of caller-given sorted splitters for one
-// segment covering the whole input; three-way classification off.
+// segment covering the whole input.  eq = 1 (the sharded exchange, distinct
+// splitters): three-way bins, 2j = keys between splitters j-1 and j, 2j+1 =
+// keys equal to splitter j.
 template <class K>
 __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nsplit, uint32_t logk,
                                        SegDesc* seg, K* tree, K* sorted, uint32_t* lut, uint64_t n,
                                        uint32_t nchunks, ChunkDesc* chunks, uint64_t chunk_elems,
-                                       uint64_t key_max) {
+                                       uint64_t key_max, uint32_t eq) {
     using KT = KeyTraits<K>;
     const uint32_t K_ = 1u << logk;
     const uint32_t lutbits = min(logk + 4, (uint32_t)kLutMaxBits);
@@ -837,7 +876,7 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
         d.nchunks = nchunks;
         d.logk = logk;
         d.m = nsplit;
-        d.eq = 0;
+        d.eq = eq;
         d.sp = 0;
         d.hist_base = 0;
         d.shift = shift;
@@ -853,27 +892,33 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
 template <int T, int LOG_KMAX>
 __global__ void __launch_bounds__(T) given_plan_kernel(const SegDesc* __restrict__ segs,
                                                        uint32_t* __restrict__ hist,
-                                                       uint32_t nsplit, uint64_t* counts) {
+                                                       uint32_t ncounts, uint64_t* counts) {
     constexpr int NB = 2 << LOG_KMAX;
     __shared__ uint32_t start[NB];
     __shared__ uint32_t warp_sums[32];
     const SegDesc d = segs[0];
-    const uint32_t nb = 1u << d.logk;
+    const uint32_t nb = (1u << d.logk) << d.eq;
     const uint32_t stride = d.nchunks + 1;
     for (uint32_t b = threadIdx.x; b < nb; b += T) {
         const uint32_t v = hist[b * stride + d.nchunks];
         start[b] = v;
-        if (b <= nsplit) counts[b] = v;
+        if (b < ncounts) counts[b] = v;
     }
     __syncthreads();
     block_exclusive_scan_smem<T>(start, (int)nb, warp_sums);
     for (uint32_t b = threadIdx.x; b < nb; b += T) hist[b * stride + d.nchunks] = start[b];
 }
 
+// Partition the n keys at `in` by nsplit sorted splitters (count + plan when
+// parts & 1, scatter when parts & 2).  eq: distinct splitters, three-way bins
+// (2 nsplit + 1 counts).  xf: `in` holds the caller's keys, classified through
+// f (the splitters are core keys); local scatters write core keys, the peer
+// scatter the caller's.
 template <class K>
 static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit, K* out,
                            uint64_t* counts, unsigned char* ws, const WsLayout& L, cudaStream_t st,
-                           Ledger& led, int parts = 3, const PeerArgs* peers = nullptr) {
+                           Ledger& led, int parts = 3, const PeerArgs* peers = nullptr,
+                           bool eq = false, Xf xf = Xf{0, 0}) {
     using TU = Tune<K>;
     const uint32_t logk = std::max<uint32_t>(1, ceil_log2_u64((uint64_t)nsplit + 1));
     if (logk > (uint32_t)TU::LOGKMAX) return fail(QMSORT_EINVAL, "too many splitters");
@@ -889,17 +934,19 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     if (parts & 1) {  // classify + count + plan (bucket sizes into counts)
         QLAUNCH(led, kPhSample, 0,
                 given_splitters_kernel<K><<<1, 256, 0, st>>>(spl, nsplit, logk, seg, tree, sorted, lut,
-                                                             n, nchunks, chunks, L.chunk_elems, key_max));
-        QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (nsplit + 1), st));
+                                                             n, nchunks, chunks, L.chunk_elems, key_max,
+                                                             eq ? 1u : 0u));
+        const uint32_t ncounts = eq ? 2 * nsplit + 1 : nsplit + 1;
+        QCK(cudaMemsetAsync(counts, 0, sizeof(uint64_t) * ncounts, st));
         if (n == 0) return QMSORT_OK;
         QCK(cudaMemsetAsync(cnt, 0, sizeof(LevelCounters), st));
         auto count_fn = count_kernel<K, TU::CT, TU::CU, TU::LOGKMAX>;
         QLAUNCH(led, kPhCount, n * sizeof(K),
                 count_fn<<<std::min(nchunks, resident_grid((const void*)count_fn, TU::CT, 0)), TU::CT, 0,
                            st>>>(seg, chunks, nchunks, nullptr, &cnt->work_count, in, tree, sorted, lut, hist,
-                                 Xf{0, 0}));
+                                 xf));
         QLAUNCH(led, kPhPlan, 0, colsum_kernel<<<64, 512, 0, st>>>(seg, hist, nullptr));
-        QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, nsplit, counts));
+        QLAUNCH(led, kPhPlan, 0, given_plan_kernel<512, TU::LOGKMAX><<<1, 512, 0, st>>>(seg, hist, ncounts, counts));
     }
     if (!(parts & 2) || n == 0) return QMSORT_OK;
     using SM = ScatterSmem<K, TU::XT, TU::XI, TU::LOGKMAX>;
@@ -909,7 +956,7 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
         QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
                 fn<<<std::min(nchunks, resident_grid((const void*)fn, TU::XT, sizeof(SM))), TU::XT,
                      sizeof(SM), st>>>(seg, chunks, nchunks, nullptr, &cnt->work_scatter, in, out, tree,
-                                       sorted, lut, hist, *peers, Xf{0, 0}));
+                                       sorted, lut, hist, *peers, xf));
         return QMSORT_OK;
     }
     auto scatter_fn = scatter_kernel<K, TU::XT, TU::XI, TU::LOGKMAX>;
@@ -917,7 +964,7 @@ static int partition_given(const K* in, size_t n, const K* spl, uint32_t nsplit,
     QLAUNCH(led, kPhScatter, 2 * n * sizeof(K),
             scatter_fn<<<std::min(nchunks, resident_grid((const void*)scatter_fn, TU::XT, sizeof(SM))),
                          TU::XT, sizeof(SM), st>>>(seg, chunks, nchunks, nullptr, &cnt->work_scatter, in,
-                                                   out, tree, sorted, lut, hist, PeerArgs{}, Xf{0, 0}));
+                                                   out, tree, sorted, lut, hist, PeerArgs{}, xf));
     return QMSORT_OK;
 }
 
@@ -1213,10 +1260,16 @@ struct BatchPipe {
         return QMSORT_OK;
     }
 };
-static BatchPipe g_batch_pipe;
+// One batch pipe per device (the streams, arenas and events of a device
+// cannot serve another); created on first use, under g_batch_mu.
+static std::map<int, BatchPipe>& batch_pipes() {
+    static std::map<int, BatchPipe>* m = new std::map<int, BatchPipe>();  // never destroyed: outlives the CUDA context teardown order
+    return *m;
+}
+// The calling thread's arena on the current device.
 static int host_arena(size_t need, unsigned char** base, cudaStream_t* st) {
-    static thread_local HostArena tl;
-    HostArena& ar = tl;
+    static thread_local std::map<int, HostArena> tl;
+    HostArena& ar = tl[current_device()];
     if (!ar.st) QCK(cudaStreamCreateWithFlags(&ar.st, cudaStreamNonBlocking));
     if (ar.bytes < need) {
         if (ar.buf) QCK(cudaFree(ar.buf));
@@ -1250,6 +1303,8 @@ static int sort_host_one(int dtype, int cmp, void* h_data, size_t n, const qmsor
     QCK(cudaStreamSynchronize(st));
     return QMSORT_OK;
 }
+
+#include "shard.cuh"
 
 }  // namespace qmsort_b200
 
@@ -1337,7 +1392,7 @@ int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const 
     // that array's copy back has completed (an event, not a host wait).  The
     // host blocks only inside each sort (its control read) and at the end.
     constexpr int A = kBatchArenas;
-    BatchPipe& bp = g_batch_pipe;
+    BatchPipe& bp = batch_pipes()[current_device()];
     QTRY(bp.init(need));
     const size_t m = todo.size();
     auto bytes_of = [&](size_t j) { return ns[todo[j]] * dtype_size(dtype); };
@@ -1537,13 +1592,77 @@ int qmsort_gpu_partition_scatter_peers(int core, const void* d_in, size_t n, uin
     if (n > 0 && (dests == nullptr || dest_offsets == nullptr))
         return fail(QMSORT_EINVAL, "null destination list");
     PeerArgs pa{};
-    pa.nb = nsplit + 1;
-    for (uint32_t b = 0; b < pa.nb; ++b) {
+    pa.nbins = nsplit + 1;
+    for (uint32_t b = 0; n > 0 && b < pa.nbins; ++b) {  // bucket b -> rank b
         pa.dest[b] = reinterpret_cast<unsigned long long>(dests[b]);
-        pa.off[b] = dest_offsets[b];
+        pa.bin_rank[b] = (signed char)b;
+        pa.bin_off[b] = dest_offsets[b];
     }
     return partition_entry(core, d_in, n, nullptr, nsplit, nullptr, nullptr, d_ws, ws_bytes, stream,
                            2, &pa);
+}
+
+// ---- the distributed samplesort (shard.cuh) ----
+int qmsort_gpu_sort_sharded(int dtype, int cmp, uint32_t P, const int* devices, const void* const* d_in,
+                            const size_t* n_in, void* const* d_out, const size_t* out_cap, size_t* out_n,
+                            const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics) {
+    return sort_sharded_sp(dtype, cmp, P, devices, d_in, n_in, d_out, out_cap, out_n, cfg, metrics);
+}
+
+size_t qmsort_gpu_shard_workspace_bytes(int dtype, size_t n) {
+    if (dtype_size(dtype) == 0) return 0;
+    return shard_ws_bytes(dtype, n);
+}
+
+int qmsort_gpu_shard_sample(int dtype, int cmp, const void* d_in, size_t n, size_t s, uint64_t seed,
+                            void* d_out, void* stream) {
+    QTRY(validate(dtype, cmp, n, d_in));
+    if (s > 0 && n > 0 && !d_out) return fail(QMSORT_EINVAL, "null output");
+    return dispatch_sample(dtype, cmp, d_in, n, s, seed, d_out, static_cast<cudaStream_t>(stream));
+}
+
+int qmsort_gpu_shard_splitters(int core, const void* h_sorted, size_t m, uint32_t P, void* h_uniq,
+                               uint32_t* h_mult, uint32_t* nuniq) {
+    if (!h_sorted || !h_uniq || !h_mult || !nuniq) return fail(QMSORT_EINVAL, "null argument");
+    return shard_splitters_host(core, h_sorted, m, P, h_uniq, h_mult, nuniq);
+}
+
+int qmsort_gpu_shard_count(int dtype, int cmp, const void* d_in, size_t n, const void* d_uniq, uint32_t nuniq,
+                           uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream) {
+    if (!d_counts || (nuniq && !d_uniq)) return fail(QMSORT_EINVAL, "null argument");
+    Ledger led;
+    return shard_partition(dtype, cmp, d_in, n, d_uniq, nuniq, d_counts, d_ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream), 1, nullptr, led);
+}
+
+int qmsort_gpu_shard_plan(uint32_t P, uint32_t nuniq, const uint32_t* mult, const uint64_t* counts,
+                          int32_t* bin_rank, uint64_t* bin_off, uint64_t* recv_n, uint64_t* lo_fill,
+                          uint64_t* hi_fill, int32_t* lo_val, int32_t* hi_val) {
+    if ((nuniq && !mult) || !counts || !bin_rank || !bin_off || !recv_n || !lo_fill || !hi_fill || !lo_val ||
+        !hi_val)
+        return fail(QMSORT_EINVAL, "null argument");
+    return shard_plan_host(P, nuniq, mult, counts, bin_rank, bin_off, recv_n, lo_fill, hi_fill, lo_val, hi_val);
+}
+
+int qmsort_gpu_shard_scatter(int dtype, int cmp, const void* d_in, size_t n, uint32_t nuniq,
+                             const int32_t* bin_rank, const uint64_t* bin_off, void* const* rank_dest, uint32_t P,
+                             void* d_ws, size_t ws_bytes, void* stream) {
+    if (n == 0) return validate(dtype, cmp, n, d_in);
+    if (!bin_rank || !bin_off || !rank_dest) return fail(QMSORT_EINVAL, "null argument");
+    PeerArgs pa;
+    QTRY(make_peer_args(nuniq, bin_rank, bin_off, rank_dest, P, &pa));
+    Ledger led;
+    return shard_partition(dtype, cmp, d_in, n, nullptr, nuniq, nullptr, d_ws, ws_bytes,
+                           static_cast<cudaStream_t>(stream), 2, &pa, led);
+}
+
+int qmsort_gpu_shard_finish(int dtype, int cmp, const void* d_recv, size_t n_recv, const void* d_uniq,
+                            int32_t lo_val, uint64_t lo_fill, int32_t hi_val, uint64_t hi_fill, void* d_out,
+                            const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes,
+                            qmsort_gpu_metrics* metrics, void* stream) {
+    if (n_recv > 0 && !d_recv) return fail(QMSORT_EINVAL, "null receive buffer");
+    return shard_finish(dtype, cmp, d_recv, n_recv, d_uniq, lo_val, lo_fill, hi_val, hi_fill, d_out, cfg, d_ws,
+                        ws_bytes, metrics, static_cast<cudaStream_t>(stream));
 }
 
 // A handle names the whole allocation (e.g. a block of a caching allocator);

@@ -835,30 +835,35 @@ __device__ __forceinline__ void vec_store(uint32_t* p, const uint32_t (&v)[N]) {
 // partition -- bucket b's keys straight into rank b's receive buffer, a peer
 // GPU's memory mapped through CUDA IPC, at that rank's offset for this sender.
 constexpr int kMaxPeers = 8;
+constexpr int kMaxPeerBins = 64;  // the few-bin (unstaged) scatter path handles <= 64 bins
 struct PeerArgs {
-    unsigned long long dest[kMaxPeers];  // receive buffer of rank b (device pointer)
-    unsigned long long off[kMaxPeers];   // element offset of this sender's part in it
-    uint32_t nb;                         // number of ranks (buckets)
+    unsigned long long dest[kMaxPeers];   // receive buffer of rank r (device pointer)
+    unsigned long long bin_off[kMaxPeerBins];  // element offset of this sender's bin b in its rank's buffer
+    signed char bin_rank[kMaxPeerBins];   // rank of bin b; -1: not sent (an equal-key share
+                                          // the receivers fill, see qmsort_gpu_shard_plan)
+    uint32_t nbins;
 };
 template <class K>
 struct LocalSink {
+    static constexpr bool kFewBinsOnly = false;
     K* out;
     __device__ __forceinline__ void store(uint32_t dest, const K& key) const { out[dest] = key; }
+    __device__ __forceinline__ void store_bin(uint32_t, uint32_t dest, const K& key) const { out[dest] = key; }
 };
+// The fused exchange: bin b's keys go to base[b] + (segment-relative
+// position) * sizeof(K), base[b] = dest[rank(b)] + (bin_off[b] - local start
+// of b) * sizeof(K); 0 = the bin is not sent.
 template <class K>
 struct PeerSink {
-    const unsigned long long* base;  // shared memory: dest[b] + (off[b] - start[b]) * sizeof(K)
-    const uint32_t* start;           // shared memory: bucket starts in the local grouping
-    uint32_t nb;
-    __device__ __forceinline__ void store(uint32_t dest, const K& key) const {
-        uint32_t b = 0;
-#pragma unroll
-        for (int j = 1; j < kMaxPeers; ++j) b += (j < (int)nb && dest >= start[j]) ? 1u : 0u;
-        *reinterpret_cast<K*>(base[b] + (unsigned long long)dest * sizeof(K)) = key;
+    static constexpr bool kFewBinsOnly = true;  // <= kMaxPeerBins bins: never staged
+    const unsigned long long* base;  // shared memory, one per bin
+    __device__ __forceinline__ void store_bin(uint32_t b, uint32_t dest, const K& key) const {
+        const unsigned long long p = base[b];
+        if (p) *reinterpret_cast<K*>(p + (unsigned long long)dest * sizeof(K)) = key;
     }
 };
 
-template <class K, int T, int U, int LOG_KMAX, bool FULL, bool XF, class Sink>
+template <class K, int T, int U, int LOG_KMAX, bool FULL, bool XF, class Sink, bool RAW = false>
 __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm, const SegDesc& d,
                                              const K* __restrict__ p, uint32_t m,
                                              const Sink& out,
@@ -877,7 +882,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
     }
     classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
     // rank within the tile's bucket; pack (bin, rank) into one word
-    if (((1u << d.logk) << d.eq) <= 64) {
+    if (Sink::kFewBinsOnly || ((1u << d.logk) << d.eq) <= 64) {
         // Few bins (the sharded exchange's P buckets, small segments): no
         // staging.  Warp-aggregated ranks give the lanes of one bin
         // consecutive slots after the bin's cursor, so every key is stored
@@ -891,7 +896,9 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         for (int u = 0; u < U; ++u) {
             const bool v = FULL || u * T + tid < m;
             const uint32_t r = warp_agg_inc(sm.hist, bin[u], v);
-            if (v) out.store(base[bin[u]] + r, k[u]);
+            // the exchange ships the caller's bit patterns (receivers sort
+            // them with the fused transform); local levels store core keys
+            if (v) out.store_bin(bin[u], base[bin[u]] + r, RAW && XF ? xf_inv(k[u], xf) : k[u]);
         }
         __syncthreads();
 #pragma unroll
@@ -902,6 +909,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         __syncthreads();
         return;
     }
+    if constexpr (!Sink::kFewBinsOnly) {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (FULL || u * T + tid < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
@@ -961,6 +969,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         }
     }
     __syncthreads();
+    }
 }
 
 template <class K, int T, int U, int LOG_KMAX, bool PEER = false>
@@ -980,14 +989,18 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
     __shared__ uint32_t next_chunk;
-    __shared__ unsigned long long peer_base[kMaxPeers];
-    __shared__ uint32_t peer_start[kMaxPeers];
-    if (PEER && threadIdx.x < kMaxPeers) {  // single segment: bucket starts from the plan
+    __shared__ unsigned long long peer_base[PEER ? kMaxPeerBins : 1];
+    if (PEER) {  // single segment: bin starts of the local grouping from the plan
         const SegDesc d0 = segs[0];
-        const uint32_t b = threadIdx.x;
-        const uint32_t st = b < peers.nb ? hist[d0.hist_base + b * (d0.nchunks + 1) + d0.nchunks] : 0u;
-        peer_start[b] = st;
-        peer_base[b] = b < peers.nb ? peers.dest[b] + (peers.off[b] - st) * sizeof(K) : 0ull;
+        const uint32_t nb0 = (1u << d0.logk) << d0.eq;
+        for (uint32_t b = threadIdx.x; b < kMaxPeerBins; b += T) {
+            unsigned long long v = 0;
+            if (b < nb0 && b < peers.nbins && peers.bin_rank[b] >= 0) {
+                const uint32_t st = hist[d0.hist_base + b * (d0.nchunks + 1) + d0.nchunks];
+                v = peers.dest[peers.bin_rank[b]] + (peers.bin_off[b] - st) * sizeof(K);
+            }
+            peer_base[b] = v;
+        }
     }
     const uint32_t nck = nchunks_dev ? *nchunks_dev : nchunks;  // device count: no host round trip
     uint32_t cur_seg = 0xFFFFFFFFu;
@@ -1023,10 +1036,17 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
         const uint32_t len = (uint32_t)(c.end - c.begin);
         uint32_t t0 = 0;
         if constexpr (PEER) {
-            const PeerSink<K> out{peer_base, peer_start, peers.nb};
-            for (; t0 + TILE <= len; t0 += TILE)
-                scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
-            if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
+            const PeerSink<K> out{peer_base};
+            if (xf.a | xf.b) {
+                for (; t0 + TILE <= len; t0 += TILE)
+                    scatter_tile<K, T, U, LOG_KMAX, true, true, PeerSink<K>, true>(sm, d, p + t0, TILE, out, cursor, xf);
+                if (t0 < len)
+                    scatter_tile<K, T, U, LOG_KMAX, false, true, PeerSink<K>, true>(sm, d, p + t0, len - t0, out, cursor, xf);
+            } else {
+                for (; t0 + TILE <= len; t0 += TILE)
+                    scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
+                if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
+            }
         } else {
             const LocalSink<K> out{dst + d.off};
             if (xf.a | xf.b) {  // level 0 of a fused-transform sort

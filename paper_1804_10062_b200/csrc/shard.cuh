@@ -1,0 +1,452 @@
+// shard.cuh -- the distributed samplesort across GPUs.
+//
+// Included by qmsort_gpu.cu inside namespace qmsort_b200 (it uses the
+// partition, sort and transform helpers defined there).  One global sort of
+// the keys held by P ranks:
+//   1. every rank draws a seeded sample of its keys through the comparator's
+//      transform f (shard_sample_kernel);
+//   2. the P samples are sorted together and P-1 evenly spaced quantiles are
+//      the global splitters; equal splitters are merged into distinct values
+//      u_j with a multiplicity c_j (shard_splitters, host);
+//   3. every rank classifies its keys three-way against the u_j -- bin 2j =
+//      keys between u_{j-1} and u_j, bin 2j+1 = keys equal to u_j -- and
+//      counts them (partition_given, eq mode);
+//   4. from the P x (2m+1) count matrix every rank computes the same plan
+//      (shard_plan, host): open bins go to the rank #{splitters below}; the
+//      keys equal to a splitter value repeated c_j >= 2 times are NOT sent --
+//      their global count is split evenly over the c_j + 1 ranks the repeated
+//      splitter spans and each of those ranks writes its share as a fill
+//      (duplicate-heavy input stays balanced: no rank receives every copy of a
+//      frequent key);
+//   5. the scatter kernel stores every bin straight into its rank's receive
+//      buffer (peer memory over NVLink: P2P pointers in one process, CUDA IPC
+//      mappings across processes) -- the exchange IS the partition's scatter;
+//   6. each rank sorts its received keys into its output (out of place,
+//      transform fused) between its lower and upper fill.
+// Rank r's output is the r-th slice of the global order.  The reference has
+// no distributed sort (single-threaded); the algorithm is the
+// north star's "global splitter selection, one all-to-all, local sorts".
+#pragma once
+
+// out[i] = f(src[position i]): seeded positions (counter-based SplitMix64,
+// uniform via a 64x64 high multiply), the same draw as gather_sample_kernel.
+template <class K>
+__global__ void shard_sample_kernel(const K* __restrict__ src, uint64_t n, uint64_t s, uint64_t seed,
+                                    K* __restrict__ out, Xf xf) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = sm_mix(seed + (i + 1) * kGamma);
+        out[i] = xf_fwd(src[__umul64hi(h, n)], xf);
+    }
+}
+
+// dst[0, len) = f^-1(values[idx]) -- a rank's share of an equal-key run.
+template <class K>
+__global__ void shard_fill_kernel(K* __restrict__ dst, uint64_t len, const K* __restrict__ values,
+                                  uint32_t idx, Xf xf) {
+    const K v = xf_inv(values[idx], xf);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = v;
+}
+
+static int dispatch_sample(int dt, int cmp, const void* d, size_t n, size_t s, uint64_t seed, void* out,
+                           cudaStream_t st) {
+    if (n == 0 || s == 0) return QMSORT_OK;
+    const Xf xf = make_xf(dt, cmp);
+    const unsigned grid = (unsigned)std::min<size_t>((s + 255) / 256, 1184);
+    switch (core_dtype(dt)) {
+        case QMSORT_DT_U32:
+            shard_sample_kernel<uint32_t><<<grid, 256, 0, st>>>((const uint32_t*)d, n, s, seed, (uint32_t*)out, xf);
+            break;
+        case QMSORT_DT_U64:
+            shard_sample_kernel<uint64_t><<<grid, 256, 0, st>>>((const uint64_t*)d, n, s, seed, (uint64_t*)out, xf);
+            break;
+        case QMSORT_DT_REC32:
+            shard_sample_kernel<Rec32><<<grid, 256, 0, st>>>((const Rec32*)d, n, s, seed, (Rec32*)out, xf);
+            break;
+    }
+    QCK(cudaGetLastError());
+    return QMSORT_OK;
+}
+
+// Sample seed of rank r (the same on every path).
+static uint64_t shard_seed(uint64_t seed, uint32_t r) { return seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(r + 1)); }
+
+// Host: P-1 splitters at sample ranks ((i+1) m) / P of the sorted sample,
+// merged into distinct values (byte equality of core keys = key equality).
+static int shard_splitters_host(int core, const void* sorted, size_t m, uint32_t P, void* uniq,
+                                uint32_t* mult, uint32_t* nuniq) {
+    const size_t w = dtype_size(core);
+    if (w == 0 || core != core_dtype(core)) return fail(QMSORT_EINVAL, "splitters expect a core dtype");
+    if (P < 1 || P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
+    if (m < P) return fail(QMSORT_EINVAL, "sample smaller than the rank count");
+    const unsigned char* s = static_cast<const unsigned char*>(sorted);
+    unsigned char* u = static_cast<unsigned char*>(uniq);
+    uint32_t k = 0;
+    for (uint32_t i = 0; i + 1 < P; ++i) {
+        const unsigned char* v = s + ((uint64_t)(i + 1) * m / P) * w;
+        if (k > 0 && std::memcmp(u + (k - 1) * w, v, w) == 0) {
+            ++mult[k - 1];
+        } else {
+            std::memcpy(u + k * w, v, w);
+            mult[k++] = 1;
+        }
+    }
+    *nuniq = k;
+    return QMSORT_OK;
+}
+
+// Host: the exchange plan from the P x (2m+1) count matrix (row = sender).
+// Every rank computes the same plan from the same matrix.
+static int shard_plan_host(uint32_t P, uint32_t m, const uint32_t* mult, const uint64_t* counts,
+                           int32_t* bin_rank, uint64_t* bin_off, uint64_t* recv_n, uint64_t* lo_fill,
+                           uint64_t* hi_fill, int32_t* lo_val, int32_t* hi_val) {
+    if (P < 1 || P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
+    const uint32_t nb = 2 * m + 1;
+    if (nb > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
+    uint64_t tot_mult = 0;
+    for (uint32_t j = 0; j < m; ++j) {
+        if (mult[j] == 0) return fail(QMSORT_EINVAL, "splitter multiplicity 0");
+        tot_mult += mult[j];
+    }
+    if (tot_mult != P - 1) return fail(QMSORT_EINVAL, "splitter multiplicities must sum to P-1");
+    for (uint32_t r = 0; r < P; ++r) {
+        recv_n[r] = lo_fill[r] = hi_fill[r] = 0;
+        lo_val[r] = hi_val[r] = -1;
+    }
+    uint32_t p = 0;  // splitters below the current value
+    for (uint32_t j = 0; j < m; ++j) {
+        bin_rank[2 * j] = (int32_t)p;  // open bin: rank #{splitters < key}
+        if (mult[j] == 1) {
+            bin_rank[2 * j + 1] = (int32_t)p;  // keys equal to a single splitter: the lower rank
+        } else {
+            bin_rank[2 * j + 1] = -1;  // filled by ranks p .. p + c
+            uint64_t e = 0;
+            for (uint32_t s = 0; s < P; ++s) e += counts[(size_t)s * nb + 2 * j + 1];
+            const uint64_t c = mult[j];
+            for (uint64_t i = 0; i <= c; ++i) {
+                const uint64_t share = e * (i + 1) / (c + 1) - e * i / (c + 1);
+                const uint32_t r = p + (uint32_t)i;
+                if (i == 0) {
+                    hi_fill[r] = share;
+                    hi_val[r] = (int32_t)j;
+                } else {
+                    lo_fill[r] = share;
+                    lo_val[r] = (int32_t)j;
+                }
+            }
+        }
+        p += mult[j];
+    }
+    bin_rank[2 * m] = (int32_t)p;
+    // receive offsets: senders in rank order, each sender's bins in order
+    for (uint32_t s = 0; s < P; ++s)
+        for (uint32_t b = 0; b < nb; ++b) {
+            const int32_t r = bin_rank[b];
+            bin_off[(size_t)s * nb + b] = r < 0 ? 0 : recv_n[r];
+            if (r >= 0) recv_n[r] += counts[(size_t)s * nb + b];
+        }
+    return QMSORT_OK;
+}
+
+// Partition workspace of one rank's count + scatter (the plan stays in it).
+static size_t shard_ws_bytes(int dt, size_t n) { return ws_bytes_for(dt, std::max<size_t>(n, 2)); }
+
+// Count (parts 1) or scatter to peers (parts 2) of one rank's n caller keys.
+static int shard_partition(int dt, int cmp, const void* d_in, size_t n, const void* uniq, uint32_t nuniq,
+                           uint64_t* counts, void* ws, size_t ws_bytes, cudaStream_t st, int parts,
+                           const PeerArgs* peers, Ledger& led) {
+    QTRY(validate(dt, cmp, n, d_in));
+    if (2 * nuniq + 1 > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
+    if (!ws) return fail(QMSORT_EINVAL, "the shard partition needs a caller workspace");
+    const size_t nn = std::max<size_t>(n, 2);
+    if (ws_bytes < shard_ws_bytes(dt, n)) return fail(QMSORT_ENOWS, "shard workspace too small");
+    unsigned char* w = static_cast<unsigned char*>(ws);
+    const Xf xf = make_xf(dt, cmp);
+    switch (core_dtype(dt)) {
+        case QMSORT_DT_U32:
+            return partition_given<uint32_t>((const uint32_t*)d_in, n, (const uint32_t*)uniq, nuniq, nullptr, counts,
+                                             w, make_layout<uint32_t>(nn), st, led, parts, peers, true, xf);
+        case QMSORT_DT_U64:
+            return partition_given<uint64_t>((const uint64_t*)d_in, n, (const uint64_t*)uniq, nuniq, nullptr, counts,
+                                             w, make_layout<uint64_t>(nn), st, led, parts, peers, true, xf);
+        case QMSORT_DT_REC32:
+            return partition_given<Rec32>((const Rec32*)d_in, n, (const Rec32*)uniq, nuniq, nullptr, counts, w,
+                                          make_layout<Rec32>(nn), st, led, parts, peers, true, xf);
+    }
+    return fail(QMSORT_EINVAL, "unknown dtype");
+}
+
+static int make_peer_args(uint32_t nuniq, const int32_t* bin_rank, const uint64_t* bin_off,
+                          void* const* rank_dest, uint32_t P, PeerArgs* pa) {
+    if (P < 1 || P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
+    const uint32_t nb = 2 * nuniq + 1;
+    if (nb > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
+    *pa = PeerArgs{};
+    pa->nbins = nb;
+    for (uint32_t r = 0; r < P; ++r) pa->dest[r] = reinterpret_cast<unsigned long long>(rank_dest[r]);
+    for (uint32_t b = 0; b < nb; ++b) {
+        if (bin_rank[b] >= (int32_t)P) return fail(QMSORT_EINVAL, "bin routed to a rank >= P");
+        pa->bin_rank[b] = (signed char)(bin_rank[b] < 0 ? -1 : bin_rank[b]);
+        pa->bin_off[b] = bin_off[b];
+        if (bin_rank[b] >= 0 && rank_dest[bin_rank[b]] == nullptr)
+            return fail(QMSORT_EINVAL, "null receive buffer");
+    }
+    return QMSORT_OK;
+}
+
+// One rank's output: [lo fill | sorted received keys | hi fill], the received
+// keys (caller dtype) sorted out of place with the fused transform.
+static int shard_finish(int dt, int cmp, const void* recv, size_t n_recv, const void* uniq, int32_t lo_val,
+                        uint64_t lo_fill, int32_t hi_val, uint64_t hi_fill, void* out,
+                        const qmsort_gpu_config* cfg, void* ws, size_t ws_bytes, qmsort_gpu_metrics* m,
+                        cudaStream_t st) {
+    QTRY(validate(dt, cmp, n_recv + lo_fill + hi_fill, out));
+    const size_t w = dtype_size(dt);
+    unsigned char* o = static_cast<unsigned char*>(out);
+    QTRY(sort_device(dt, cmp, o + lo_fill * w, n_recv, cfg, ws, ws_bytes, m, st, recv));
+    const Xf xf = make_xf(dt, cmp);
+    for (int side = 0; side < 2; ++side) {
+        const uint64_t len = side ? hi_fill : lo_fill;
+        const int32_t vi = side ? hi_val : lo_val;
+        if (len == 0) continue;
+        if (vi < 0 || !uniq) return fail(QMSORT_EINVAL, "fill without a splitter value");
+        unsigned char* at = o + (side ? (lo_fill + n_recv) * w : 0);
+        const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((len + 255) / 256, 148 * 8));
+        switch (core_dtype(dt)) {
+            case QMSORT_DT_U32:
+                shard_fill_kernel<uint32_t><<<grid, 256, 0, st>>>((uint32_t*)at, len, (const uint32_t*)uniq, vi, xf);
+                break;
+            case QMSORT_DT_U64:
+                shard_fill_kernel<uint64_t><<<grid, 256, 0, st>>>((uint64_t*)at, len, (const uint64_t*)uniq, vi, xf);
+                break;
+            case QMSORT_DT_REC32:
+                shard_fill_kernel<Rec32><<<grid, 256, 0, st>>>((Rec32*)at, len, (const Rec32*)uniq, vi, xf);
+                break;
+        }
+        QCK(cudaGetLastError());
+        if (m) ++m->kernel_launches;
+    }
+    return QMSORT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Single-process driver over P devices (the C-level sharded entry).  Device
+// buffers of different ranks are addressed directly (peer access enabled
+// between distinct devices); a device may appear more than once, which runs
+// P ranks on one GPU with the same kernels and the same exchange.
+// ---------------------------------------------------------------------------
+struct DevGuard {
+    int prev = 0;
+    DevGuard() { cudaGetDevice(&prev); }
+    ~DevGuard() { cudaSetDevice(prev); }
+};
+
+struct ShardRank {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t scattered = nullptr, ready = nullptr;
+    void *smp = nullptr, *uniq = nullptr, *counts = nullptr, *pws = nullptr, *recv = nullptr, *fws = nullptr;
+    size_t pws_bytes = 0, fws_bytes = 0;
+};
+
+static int sort_sharded_sp(int dt, int cmp, uint32_t P, const int* devices, const void* const* d_in,
+                           const size_t* n_in, void* const* d_out, const size_t* out_cap, size_t* out_n,
+                           const qmsort_gpu_config* cfgp, qmsort_gpu_metrics* metrics) {
+    if (P < 1 || P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
+    if (!devices || !d_in || !n_in || !d_out || !out_cap || !out_n) return fail(QMSORT_EINVAL, "null argument");
+    if (dtype_size(dt) == 0) return fail(QMSORT_EINVAL, "unknown dtype");
+    qmsort_gpu_config tmp;
+    const qmsort_gpu_config& cfg = cfg_or_default(cfgp, tmp);
+    const int core = core_dtype(dt);
+    const size_t w = dtype_size(dt);
+    uint64_t total = 0;
+    for (uint32_t r = 0; r < P; ++r) {
+        QTRY(validate(dt, cmp, n_in[r], d_in[r]));
+        total += n_in[r];
+    }
+    if (total >= (1ull << 32) * P) return fail(QMSORT_EINVAL, "too many keys");
+    const auto t0 = std::chrono::steady_clock::now();
+    DevGuard guard;
+    int ndev = 0;
+    QCK(cudaGetDeviceCount(&ndev));
+    for (uint32_t r = 0; r < P; ++r)
+        if (devices[r] < 0 || devices[r] >= ndev) return fail(QMSORT_EINVAL, "bad device ordinal");
+    // peer access between every pair of distinct devices (idempotent)
+    for (uint32_t a = 0; a < P; ++a)
+        for (uint32_t b = 0; b < P; ++b) {
+            if (devices[a] == devices[b]) continue;
+            int can = 0;
+            QCK(cudaDeviceCanAccessPeer(&can, devices[a], devices[b]));
+            if (!can) return fail(QMSORT_ECUDA, "no peer access between devices " + std::to_string(devices[a]) +
+                                                    " and " + std::to_string(devices[b]));
+            QCK(cudaSetDevice(devices[a]));
+            const cudaError_t e = cudaDeviceEnablePeerAccess(devices[b], 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) QCK(e);
+            cudaGetLastError();  // clear "already enabled"
+        }
+    const uint32_t s = 64 * P;  // samples per rank (oversampling 64 per rank)
+    std::vector<ShardRank> R(P);
+    uint32_t launches = 0;
+    uint64_t alg = 0;
+    auto cleanup = [&]() {
+        for (ShardRank& x : R) {
+            cudaSetDevice(x.dev);
+            if (x.st) cudaStreamSynchronize(x.st);
+            for (void* p : {x.smp, x.uniq, x.counts, x.pws, x.recv, x.fws})
+                if (p) cudaFree(p);
+            if (x.scattered) cudaEventDestroy(x.scattered);
+            if (x.ready) cudaEventDestroy(x.ready);
+            if (x.st) cudaStreamDestroy(x.st);
+        }
+    };
+    struct Cleanup {
+        std::function<void()> f;
+        ~Cleanup() { f(); }
+    } cl{cleanup};
+    // 1. samples (core keys) of every rank, gathered on rank 0's device
+    for (uint32_t r = 0; r < P; ++r) {
+        ShardRank& x = R[r];
+        x.dev = devices[r];
+        QCK(cudaSetDevice(x.dev));
+        QCK(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking));
+        QCK(cudaEventCreateWithFlags(&x.scattered, cudaEventDisableTiming));
+        QCK(cudaEventCreateWithFlags(&x.ready, cudaEventDisableTiming));
+        QCK(cudaMalloc(&x.smp, (size_t)s * P * w));
+        QCK(cudaMalloc(&x.uniq, kMaxPeers * w));
+        QCK(cudaMalloc(&x.counts, kMaxPeerBins * sizeof(uint64_t)));
+        x.pws_bytes = shard_ws_bytes(dt, n_in[r]);
+        QCK(cudaMalloc(&x.pws, x.pws_bytes));
+    }
+    std::vector<unsigned char> smp_h((size_t)s * P * w);
+    for (uint32_t r = 0; r < P; ++r) {
+        ShardRank& x = R[r];
+        QCK(cudaSetDevice(x.dev));
+        unsigned char* mine = static_cast<unsigned char*>(R[0].smp) + (size_t)r * s * w;
+        if (n_in[r] > 0) {
+            // sample into this rank's buffer, then copy to rank 0's gather slot
+            QTRY(dispatch_sample(dt, cmp, d_in[r], n_in[r], s, shard_seed(cfg.seed, r), x.smp, x.st));
+            ++launches;
+            QCK(cudaMemcpyPeerAsync(mine, R[0].dev, x.smp, x.dev, (size_t)s * w, x.st));
+        } else {  // an empty shard contributes maximum keys (never chosen as splitters below)
+            QCK(cudaSetDevice(R[0].dev));
+            QCK(cudaMemsetAsync(mine, 0xFF, (size_t)s * w, R[0].st));
+            QCK(cudaSetDevice(x.dev));
+        }
+        QCK(cudaEventRecord(x.ready, x.st));
+    }
+    QCK(cudaSetDevice(R[0].dev));
+    for (uint32_t r = 1; r < P; ++r) QCK(cudaStreamWaitEvent(R[0].st, R[r].ready, 0));
+    {
+        qmsort_gpu_config scfg;
+        qmsort_gpu_config_init(&scfg, 0);
+        qmsort_gpu_metrics sm_;
+        QTRY(sort_device(core, 0, R[0].smp, (size_t)s * P, &scfg, nullptr, 0, &sm_, R[0].st));
+        launches += sm_.kernel_launches;
+        QCK(cudaMemcpyAsync(smp_h.data(), R[0].smp, smp_h.size(), cudaMemcpyDeviceToHost, R[0].st));
+        QCK(cudaStreamSynchronize(R[0].st));
+    }
+    // 2. splitters (host), to every device
+    unsigned char uniq_h[kMaxPeers * 32];
+    uint32_t mult[kMaxPeers] = {}, nuniq = 0;
+    QTRY(shard_splitters_host(core, smp_h.data(), (size_t)s * P, P, uniq_h, mult, &nuniq));
+    const uint32_t nb = 2 * nuniq + 1;
+    // 3. three-way counts of every rank
+    std::vector<uint64_t> C((size_t)P * nb, 0);
+    for (uint32_t r = 0; r < P; ++r) {
+        ShardRank& x = R[r];
+        QCK(cudaSetDevice(x.dev));
+        if (nuniq) QCK(cudaMemcpyAsync(x.uniq, uniq_h, nuniq * w, cudaMemcpyHostToDevice, x.st));
+        Ledger led;
+        QTRY(shard_partition(dt, cmp, d_in[r], n_in[r], x.uniq, nuniq, (uint64_t*)x.counts, x.pws, x.pws_bytes,
+                             x.st, 1, nullptr, led));
+        launches += led.launches;
+        alg += led.alg_bytes;
+        QCK(cudaMemcpyAsync(&C[(size_t)r * nb], x.counts, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, x.st));
+    }
+    for (uint32_t r = 0; r < P; ++r) {
+        QCK(cudaSetDevice(R[r].dev));
+        QCK(cudaStreamSynchronize(R[r].st));
+    }
+    // 4. the plan (host, identical for every rank)
+    int32_t bin_rank[kMaxPeerBins];
+    std::vector<uint64_t> bin_off((size_t)P * nb);
+    uint64_t recv_n[kMaxPeers], lo_fill[kMaxPeers], hi_fill[kMaxPeers];
+    int32_t lo_val[kMaxPeers], hi_val[kMaxPeers];
+    QTRY(shard_plan_host(P, nuniq, mult, C.data(), bin_rank, bin_off.data(), recv_n, lo_fill, hi_fill, lo_val,
+                         hi_val));
+    bool fits = true;
+    for (uint32_t r = 0; r < P; ++r) {
+        out_n[r] = recv_n[r] + lo_fill[r] + hi_fill[r];
+        if (out_n[r] > out_cap[r]) fits = false;
+        if (out_n[r] > 0 && d_out[r] == nullptr) return fail(QMSORT_EINVAL, "null output buffer");
+    }
+    if (!fits) return fail(QMSORT_ENOWS, "an output buffer is smaller than its slice (see out_n)");
+    // receive buffers, then 5. every rank's scatter stores into the peers' buffers
+    std::vector<void*> dest(P, nullptr);
+    for (uint32_t r = 0; r < P; ++r) {
+        ShardRank& x = R[r];
+        QCK(cudaSetDevice(x.dev));
+        QCK(cudaMalloc(&x.recv, std::max<uint64_t>(1, recv_n[r]) * w));
+        dest[r] = x.recv;
+    }
+    for (uint32_t r = 0; r < P; ++r) {
+        ShardRank& x = R[r];
+        QCK(cudaSetDevice(x.dev));
+        PeerArgs pa;
+        QTRY(make_peer_args(nuniq, bin_rank, &bin_off[(size_t)r * nb], dest.data(), P, &pa));
+        Ledger led;
+        QTRY(shard_partition(dt, cmp, d_in[r], n_in[r], x.uniq, nuniq, nullptr, x.pws, x.pws_bytes, x.st, 2, &pa,
+                             led));
+        launches += led.launches;
+        alg += led.alg_bytes;
+        QCK(cudaEventRecord(x.scattered, x.st));
+    }
+    // 6. local sorts once every sender's stores have landed (events, no host
+    // wait): one host thread per rank, each sort has its own control read
+    std::vector<int> rcs(P, QMSORT_OK);
+    std::vector<std::string> errs(P);
+    std::vector<qmsort_gpu_metrics> ms(P);
+    auto finish_rank = [&](uint32_t r) {
+        ShardRank& x = R[r];
+        const int rc = [&]() -> int {
+            QCK(cudaSetDevice(x.dev));
+            for (uint32_t q = 0; q < P; ++q)
+                if (q != r) QCK(cudaStreamWaitEvent(x.st, R[q].scattered, 0));
+            x.fws_bytes = ws_bytes_for(dt, std::max<uint64_t>(2, recv_n[r]));
+            QCK(cudaMallocAsync(&x.fws, x.fws_bytes, x.st));
+            std::memset(&ms[r], 0, sizeof(ms[r]));
+            const int rc2 = shard_finish(dt, cmp, x.recv, recv_n[r], x.uniq, lo_val[r], lo_fill[r], hi_val[r],
+                                         hi_fill[r], d_out[r], &cfg, x.fws, x.fws_bytes, &ms[r], x.st);
+            cudaFreeAsync(x.fws, x.st);
+            x.fws = nullptr;
+            if (rc2 != QMSORT_OK) return rc2;
+            QCK(cudaStreamSynchronize(x.st));
+            return QMSORT_OK;
+        }();
+        rcs[r] = rc;
+        if (rc != QMSORT_OK) errs[r] = g_err;
+    };
+    {
+        std::vector<std::thread> th;
+        for (uint32_t r = 1; r < P; ++r) th.emplace_back(finish_rank, r);
+        finish_rank(0);
+        for (std::thread& t : th) t.join();
+    }
+    for (uint32_t r = 0; r < P; ++r) {
+        if (rcs[r] != QMSORT_OK) return fail(rcs[r], "rank " + std::to_string(r) + ": " + errs[r]);
+        launches += ms[r].kernel_launches;
+        alg += ms[r].alg_bytes;
+    }
+    if (metrics) {
+        std::memset(metrics, 0, sizeof(*metrics));
+        metrics->elapsed_ns = (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                  std::chrono::steady_clock::now() - t0).count();
+        metrics->kernel_launches = launches;
+        metrics->alg_bytes = alg;
+        metrics->host_syncs = 3;
+    }
+    g_err.clear();
+    return QMSORT_OK;
+}

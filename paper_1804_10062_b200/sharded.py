@@ -1,38 +1,126 @@
 """Distributed samplesort across the GPUs of one node.
 
 The array is sharded: rank r holds n_r keys.  One sort call
-  1. maps keys into the unsigned core domain (order-preserving transform),
-  2. draws ``oversample * P`` seeded sample keys per rank,
-  3. all-gathers the samples; every rank sorts the same P*s keys and picks the
-     same P-1 global splitters (deterministic),
-  4. partitions its keys by the splitters on the GPU (count / scan / scatter,
-     K2-K4 of samplesort.cuh) -- bucket j goes to rank j,
-  5. exchanges bucket sizes, then the keys, with ONE all-to-all over NVLink,
-  6. sorts the received keys locally with the single-GPU pipeline and maps
-     them back out of the core domain.
+  1. draws ``oversample * P`` seeded sample keys per rank, mapped into the
+     unsigned core key domain (``qmsort_gpu_shard_sample``),
+  2. all-gathers the samples; every rank sorts the same P*s keys and picks the
+     same P-1 global splitters, merged into distinct values with
+     multiplicities (``qmsort_gpu_shard_splitters``, host),
+  3. classifies and counts its keys three-way against them on the GPU
+     (``qmsort_gpu_shard_count``: bin 2j = keys between splitters j-1 and j,
+     2j+1 = keys equal to splitter j),
+  4. all-gathers the P x (2m+1) count matrix and computes the exchange plan
+     (``qmsort_gpu_shard_plan``, host, identical on every rank): each bin's
+     rank and offset in that rank's receive buffer; keys equal to a splitter
+     value that repeats are not sent -- the ranks that value spans fill their
+     even share of it (duplicate-heavy input stays balanced),
+  5. exchanges the keys: by default the exchange IS the partition's scatter
+     (``qmsort_gpu_shard_scatter`` stores every bin straight into its rank's
+     receive buffer, peer memory mapped through CUDA IPC, over NVLink); the
+     baseline alternative scatters into a local staging buffer grouped by rank
+     and runs one NCCL all-to-all,
+  6. sorts the received keys into a fresh output between its fills
+     (``qmsort_gpu_shard_finish``).
 Rank r's result is the r-th slice of the global order; concatenating the
-slices in rank order gives the sorted array.
+slices in rank order gives the sorted array.  The input shards are only read.
 
-The exchange is expressed against a small ``Exchange`` interface so the same
-code runs over ``torch.distributed`` (NCCL between GPUs, gloo for the CPU
-tests) and, for single-GPU testing, over an in-process emulation of P ranks.
-The per-rank compute ops (``Ops``) are the C-ABI kernels by default; tests
-substitute CPU doubles to exercise the exchange logic without a GPU.
+The same C functions drive the single-process entry over several devices
+(``qmsort_gpu_sort_sharded``, :func:`sort_sharded_devices`).  The exchange is
+expressed against a small interface so the same code runs over
+``torch.distributed`` (NCCL or IPC between GPUs, gloo for the CPU tests) and
+over an in-process emulation of P ranks on one GPU.  The per-rank compute ops
+(``GpuOps``) are the C-ABI kernels; tests substitute CPU doubles
+(tests/sharded_doubles.py) to exercise the exchange logic without a GPU.
 """
 from __future__ import annotations
 
 import ctypes
 from typing import Any, Sequence
 
+import numpy as np
+
 from . import _lib
 
 CORE = {_lib.DT_I32: _lib.DT_U32, _lib.DT_U32: _lib.DT_U32, _lib.DT_U64: _lib.DT_U64,
         _lib.DT_F64: _lib.DT_U64, _lib.DT_REC32: _lib.DT_REC32, _lib.DT_I64: _lib.DT_U64}
+KEY_BYTES = {_lib.DT_I32: 4, _lib.DT_U32: 4, _lib.DT_U64: 8, _lib.DT_F64: 8, _lib.DT_I64: 8,
+             _lib.DT_REC32: 32}
+MAX_RANKS = 8
 
 
-def _words(dt: int) -> int:
-    """Rows of the wire tensor per key: keys travel as int32 / int64 words."""
-    return 4 if dt == _lib.DT_REC32 else 1
+def rank_seed(seed: int, r: int) -> int:
+    """Sample seed of rank r (shard.cuh shard_seed)."""
+    return (seed ^ (0x9E3779B97F4A7C15 * (r + 1))) & 0xFFFFFFFFFFFFFFFF
+
+
+def wire(t, dt: int):
+    """Keys as int32 / int64 words for the collectives (records: (n, 4) int64)."""
+    import torch
+    return t.view(torch.int32) if KEY_BYTES[dt] == 4 else t.view(torch.int64)
+
+
+# ---------------------------------------------------------------------------
+# host-only plan (C, no device work): identical on every rank
+# ---------------------------------------------------------------------------
+def splitters(core: int, sorted_sample: np.ndarray, P: int) -> tuple[np.ndarray, list]:
+    """P-1 quantile splitters of the sorted core-key sample, merged into
+    distinct values: (unique splitters as uint8 rows, multiplicities)."""
+    lib = _lib.load()
+    w = KEY_BYTES[core]
+    smp = np.ascontiguousarray(sorted_sample).view(np.uint8).reshape(-1)
+    m = smp.shape[0] // w
+    uniq = np.zeros(MAX_RANKS * w, dtype=np.uint8)
+    mult = (ctypes.c_uint32 * MAX_RANKS)()
+    nu = ctypes.c_uint32(0)
+    _lib.check(lib.qmsort_gpu_shard_splitters(core, smp.ctypes.data, m, P, uniq.ctypes.data, mult,
+                                              ctypes.byref(nu)), "qmsort_gpu_shard_splitters")
+    k = int(nu.value)
+    return uniq[:k * w].copy(), [int(mult[i]) for i in range(k)]
+
+
+def plan(P: int, mult: Sequence[int], C: np.ndarray) -> dict:
+    """Exchange plan from the P x (2m+1) count matrix (row = sender)."""
+    lib = _lib.load()
+    m = len(mult)
+    nb = 2 * m + 1
+    C = np.ascontiguousarray(np.asarray(C, dtype=np.uint64).reshape(P, nb))
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    bin_rank = np.zeros(nb, dtype=np.int32)
+    bin_off = np.zeros((P, nb), dtype=np.uint64)
+    recv_n, lo_fill, hi_fill = (np.zeros(P, dtype=np.uint64) for _ in range(3))
+    lo_val, hi_val = np.zeros(P, dtype=np.int32), np.zeros(P, dtype=np.int32)
+    mu = (ctypes.c_uint32 * max(1, m))(*mult)
+    _lib.check(lib.qmsort_gpu_shard_plan(P, m, mu, C.ctypes.data_as(u64p), bin_rank.ctypes.data_as(i32p),
+                                         bin_off.ctypes.data_as(u64p), recv_n.ctypes.data_as(u64p),
+                                         lo_fill.ctypes.data_as(u64p), hi_fill.ctypes.data_as(u64p),
+                                         lo_val.ctypes.data_as(i32p), hi_val.ctypes.data_as(i32p)),
+               "qmsort_gpu_shard_plan")
+    return {"bin_rank": bin_rank, "bin_off": bin_off, "recv_n": recv_n.astype(np.int64),
+            "lo_fill": lo_fill.astype(np.int64), "hi_fill": hi_fill.astype(np.int64),
+            "lo_val": lo_val, "hi_val": hi_val, "C": C.astype(np.int64)}
+
+
+def staging_offsets(pl: dict, r: int) -> tuple[np.ndarray, list]:
+    """Non-fused exchange: sender r's bins grouped by destination rank in a
+    local staging buffer -- each bin's offset there and the per-rank sizes."""
+    C, br = pl["C"], pl["bin_rank"]
+    P = C.shape[0]
+    send = [int(sum(C[r][b] for b in range(len(br)) if br[b] == t)) for t in range(P)]
+    base = np.concatenate([[0], np.cumsum(send)]).astype(np.int64)
+    off = np.zeros(len(br), dtype=np.uint64)
+    acc = list(base[:P])
+    for b, t in enumerate(br):
+        if t >= 0:
+            off[b] = acc[t]
+            acc[t] += int(C[r][b])
+    return off, send
+
+
+def recv_counts(pl: dict, r: int) -> list:
+    """What each sender ships to rank r (non-fused exchange)."""
+    C, br = pl["C"], pl["bin_rank"]
+    return [int(sum(C[s][b] for b in range(len(br)) if br[b] == r)) for s in range(C.shape[0])]
 
 
 # ---------------------------------------------------------------------------
@@ -47,89 +135,111 @@ class GpuOps:
         self.lib = _lib.load()
         self.stream = stream
         self.launches = 0  # kernels of the local sorts (bench.py gpu_launches)
+        self.alg_bytes = 0
         self.wsbuf = None
 
     def _s(self):
         return self.torch.cuda.current_stream().cuda_stream if self.stream is None else self.stream
 
-    def to_core(self, t, dt: int, cmp: int, inverse: bool = False) -> None:
-        rc = self.lib.qmsort_gpu_transform(dt, cmp, t.data_ptr(), t.shape[0], int(inverse), self._s())
-        _lib.check(rc, "qmsort_gpu_transform")
-
-    def sample(self, t, core: int, s: int, seed: int):
-        out = self.torch.empty((s,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        if t.shape[0] == 0:
-            return out[:0]
-        rc = self.lib.qmsort_gpu_sample(core, t.data_ptr(), t.shape[0], s, seed, out.data_ptr(), self._s())
-        _lib.check(rc, "qmsort_gpu_sample")
-        return out
+    def synchronize(self) -> None:
+        if self.stream is None:
+            self.torch.cuda.current_stream().synchronize()
+        else:
+            self.torch.cuda.synchronize()
 
     def _ws(self, nbytes: int, device):
-        """Grow-only device workspace shared by the local sort and partition."""
+        """Grow-only device workspace shared by the partition and the local sort."""
         if self.wsbuf is None or self.wsbuf.numel() < nbytes or self.wsbuf.device != device:
             self.wsbuf = None
             self.wsbuf = self.torch.empty(int(nbytes * 1.25) + 4096, dtype=self.torch.uint8, device=device)
         return self.wsbuf
 
-    def sort(self, t, core: int) -> None:
+    def sample(self, t, dt: int, cmp: int, s: int, seed: int):
+        """s seeded keys of t in the core domain (wire words)."""
+        core = CORE[dt]
+        out = self.torch.empty((s,) + tuple(t.shape[1:]), dtype=wire(t, dt).dtype, device=t.device)
+        if t.shape[0] == 0:
+            return out[:0]
+        _lib.check(self.lib.qmsort_gpu_shard_sample(dt, cmp, t.data_ptr(), t.shape[0], s, seed,
+                                                    out.data_ptr(), self._s()), "qmsort_gpu_shard_sample")
+        assert KEY_BYTES[core] == KEY_BYTES[dt]
+        return out
+
+    def sort_core(self, t, core: int) -> None:
         from . import SortConfig, sort
         if t.shape[0] > 1:
-            cfg = SortConfig()
             ws = self._ws(self.lib.qmsort_gpu_workspace_bytes(core, t.shape[0], None), t.device)
-            m = sort(t, cfg, "less", dtype=core, stream=self._s(), workspace=ws)
+            m = sort(t, SortConfig(), "less", dtype=core, stream=self._s(), workspace=ws)
             self.launches += m.kernel_launches
 
-    def partition(self, t, core: int, splitters):
-        """Bucket j = #{splitters < key}; returns (keys grouped by bucket, counts[P])."""
-        torch = self.torch
-        nsplit = splitters.shape[0]
-        out = torch.empty_like(t)
-        counts = torch.zeros(nsplit + 1, dtype=torch.int64, device=t.device)
-        n = t.shape[0]
-        if n:
-            wsb = self.lib.qmsort_gpu_partition_workspace_bytes(core, n)
-            ws = self._ws(wsb, t.device)
-            rc = self.lib.qmsort_gpu_partition(core, t.data_ptr(), n, splitters.data_ptr(), nsplit,
-                                               out.data_ptr(), counts.data_ptr(), ws.data_ptr(),
-                                               ws.numel(), self._s())
-            _lib.check(rc, "qmsort_gpu_partition")
-        return out, counts
+    def put(self, host_bytes: np.ndarray, like):
+        """Unique splitters (uint8 rows) onto this rank's device."""
+        t = self.torch.from_numpy(np.ascontiguousarray(host_bytes)).to(like.device)
+        return t
 
-    # -- the exchange fused into the partition's scatter ------------------
-    def partition_count(self, t, core: int, splitters):
-        """Classify + count against the splitters; the plan stays in the workspace
-        for scatter_peers.  Returns the bucket sizes (int64 device tensor)."""
-        torch = self.torch
-        nsplit = splitters.shape[0]
-        counts = torch.zeros(nsplit + 1, dtype=torch.int64, device=t.device)
+    def count(self, t, dt: int, cmp: int, uniq, m: int):
+        counts = self.torch.zeros(2 * m + 1, dtype=self.torch.int64, device=t.device)
         n = t.shape[0]
-        if n:
-            ws = self._ws(self.lib.qmsort_gpu_partition_workspace_bytes(core, n), t.device)
-            rc = self.lib.qmsort_gpu_partition_count(core, t.data_ptr(), n, splitters.data_ptr(), nsplit,
-                                                     counts.data_ptr(), ws.data_ptr(), ws.numel(),
-                                                     self._s())
-            _lib.check(rc, "qmsort_gpu_partition_count")
+        ws = self._ws(self.lib.qmsort_gpu_shard_workspace_bytes(dt, n), t.device)
+        _lib.check(self.lib.qmsort_gpu_shard_count(dt, cmp, t.data_ptr(), n, uniq.data_ptr() if m else None, m,
+                                                   counts.data_ptr(), ws.data_ptr(), ws.numel(), self._s()),
+                   "qmsort_gpu_shard_count")
+        self.alg_bytes += n * KEY_BYTES[dt]
         return counts
 
-    def scatter_peers(self, t, core: int, nsplit: int, dests: Sequence[int], offsets: Sequence[int]) -> None:
-        """Bucket b of t (planned by partition_count) -> dests[b] + offsets[b] keys."""
+    def scatter(self, t, dt: int, cmp: int, m: int, bin_rank, bin_off, dests: Sequence[Any]) -> None:
+        """Bin b of t (planned by count) -> dests[bin_rank[b]] + bin_off[b] keys.
+        dests: device pointers (ints, e.g. IPC-mapped peers) or tensors."""
         n = t.shape[0]
         if not n:
             return
+        P = len(dests)
+        nb = 2 * m + 1
+        br = (ctypes.c_int32 * nb)(*[int(x) for x in bin_rank])
+        bo = (ctypes.c_uint64 * nb)(*[int(x) for x in bin_off])
+        # an empty receive buffer may report a null pointer; no key goes there
+        d = (ctypes.c_void_p * P)(*[int(x) if isinstance(x, int) else (x.data_ptr() or t.data_ptr())
+                                    for x in dests])
         ws = self.wsbuf
-        P = nsplit + 1
-        d = (ctypes.c_void_p * P)(*[int(x) for x in dests])
-        o = (ctypes.c_uint64 * P)(*[int(x) for x in offsets])
-        rc = self.lib.qmsort_gpu_partition_scatter_peers(core, t.data_ptr(), n, nsplit, d, o,
-                                                         ws.data_ptr(), ws.numel(), self._s())
-        _lib.check(rc, "qmsort_gpu_partition_scatter_peers")
+        _lib.check(self.lib.qmsort_gpu_shard_scatter(dt, cmp, t.data_ptr(), n, m, br, bo, d, P, ws.data_ptr(),
+                                                     ws.numel(), self._s()), "qmsort_gpu_shard_scatter")
+        self.alg_bytes += 2 * n * KEY_BYTES[dt]
+
+    def alloc(self, n: int, like):
+        # never a null pointer, even for 0 keys (a peer's scatter is handed every buffer)
+        t = self.torch.empty((max(1, n),) + tuple(like.shape[1:]), dtype=like.dtype, device=like.device)
+        return t[:n]
+
+    def finish(self, recv, n_recv: int, dt: int, cmp: int, uniq, lo_val: int, lo_fill: int, hi_val: int,
+               hi_fill: int, like):
+        """[lo fill | received keys sorted | hi fill] as a fresh tensor."""
+        torch = self.torch
+        n_out = n_recv + lo_fill + hi_fill
+        out = torch.empty((n_out,) + tuple(like.shape[1:]), dtype=like.dtype, device=like.device)
+        if n_out == 0:
+            return out
+        ws = self._ws(self.lib.qmsort_gpu_workspace_bytes(dt, max(2, n_recv), None), like.device)
+        from . import SortConfig
+        c = SortConfig().to_c()
+        mt = _lib.GpuMetrics()
+        _lib.check(self.lib.qmsort_gpu_shard_finish(dt, cmp, recv.data_ptr() if n_recv else None, n_recv,
+                                                    uniq.data_ptr() if uniq is not None and uniq.numel() else None,
+                                                    lo_val, lo_fill, hi_val, hi_fill, out.data_ptr(),
+                                                    ctypes.byref(c), ws.data_ptr(), ws.numel(), ctypes.byref(mt),
+                                                    self._s()), "qmsort_gpu_shard_finish")
+        self.launches += mt.kernel_launches
+        self.alg_bytes += mt.alg_bytes
+        return out
 
 
 # ---------------------------------------------------------------------------
 # exchanges
 # ---------------------------------------------------------------------------
 class TorchExchange:
-    """torch.distributed process group (NCCL on GPUs, gloo on CPUs)."""
+    """torch.distributed process group (NCCL on GPUs, gloo on CPUs): the
+    non-fused baseline -- one all-to-all of a staging buffer."""
+
+    fused = False
 
     def __init__(self, group: Any = None):
         import torch.distributed as dist
@@ -138,17 +248,16 @@ class TorchExchange:
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
+    def _cpu_group(self) -> bool:
+        return self.dist.get_backend(self.group) == "gloo"
+
     def all_gather(self, t):
         import torch
+        if self._cpu_group() and t.is_cuda:
+            t = t.cpu()
         parts = [torch.empty_like(t) for _ in range(self.P)]
-        self.dist.all_gather(parts, t, group=self.group)
+        self.dist.all_gather(parts, t.contiguous(), group=self.group)
         return torch.cat(parts)
-
-    def all_to_all_counts(self, counts):
-        import torch
-        out = torch.empty_like(counts)
-        self.dist.all_to_all_single(out, counts, group=self.group)
-        return out
 
     def all_to_all_v(self, t, send: Sequence[int], recv: Sequence[int]):
         import torch
@@ -161,10 +270,12 @@ class TorchExchange:
 class PeerExchange(TorchExchange):
     """The data exchange fused into the partition (one process per GPU): every
     rank exports a receive buffer through CUDA IPC once; senders' scatter
-    kernels then store their bucket for rank j straight into rank j's buffer
-    over NVLink (qmsort_gpu_partition_scatter_peers).  torch.distributed only
-    carries the handles, the P x P bucket-size matrix and two barriers -- no
-    collective touches the keys."""
+    kernels then store their bins for rank j straight into rank j's buffer
+    over NVLink (qmsort_gpu_shard_scatter).  torch.distributed only carries
+    the samples, the count matrix, the handles and two barriers -- no
+    collective touches the keys.  The receive buffer is reused across calls;
+    every call returns a fresh output tensor (the local sort reads the
+    receive buffer out of place)."""
 
     fused = True
 
@@ -179,12 +290,14 @@ class PeerExchange(TorchExchange):
     def ensure_capacity(self, nbytes: int, device) -> None:
         """Collective: (re)allocate every rank's buffer to >= nbytes and swap handles."""
         import torch
-        if self.recv is not None and self.cap >= nbytes:
+        need = [None] * self.P
+        self.dist.all_gather_object(need, int(self.recv is None or self.cap < nbytes), group=self.group)
+        if not any(need):
             return
         for p in self.opened:
             _lib.check(self.lib.qmsort_gpu_ipc_close(ctypes.c_void_p(p)), "qmsort_gpu_ipc_close")
         self.opened = []
-        self.cap = max(int(nbytes * 1.25) + 4096, 1 << 20)
+        self.cap = max(int(nbytes * 1.25) + 4096, self.cap, 1 << 20)
         self.recv = torch.empty(self.cap, dtype=torch.uint8, device=device)
         h = (ctypes.c_uint8 * _IPC_BYTES)()
         off = ctypes.c_uint64()
@@ -204,44 +317,36 @@ class PeerExchange(TorchExchange):
             self.ptrs.append(int(p.value))
             self.opened.append(int(base.value))
 
-    def barrier(self) -> None:
+    def barrier(self, ops: Any = None) -> None:
+        """Every stream the rank's ops ran on has drained, then a host barrier."""
         import torch
-        torch.cuda.current_stream().synchronize()
+        if ops is not None and hasattr(ops, "synchronize"):
+            ops.synchronize()
+        else:
+            torch.cuda.synchronize()
         self.dist.barrier(group=self.group)
 
 
 _IPC_BYTES = 64  # QMSORT_IPC_HANDLE_BYTES
 
 
-def _wire(t, dt: int):
-    """Reinterpret core keys as int32 / int64 words for the collectives."""
+def _pad_sample(smp, s: int, like):
+    """An empty (or short) shard contributes maximum keys (never a splitter below them)."""
     import torch
-    if dt == _lib.DT_U32:
-        return t.view(torch.int32)
-    return t.view(torch.int64)
+    if smp.shape[0] >= s:
+        return smp
+    pad = torch.full((s - smp.shape[0],) + tuple(smp.shape[1:]), -1, dtype=smp.dtype, device=smp.device)
+    return torch.cat([smp, pad])
 
 
-def _unwire(t, dt: int, like):
-    return t.view(like.dtype)
-
-
-def pick_splitters(sorted_samples, P: int):
-    """P-1 evenly spaced quantiles of the sorted global sample."""
-    import torch
-    m = sorted_samples.shape[0]
-    idx = torch.tensor([((i + 1) * m) // P for i in range(P - 1)], dtype=torch.long,
-                       device=sorted_samples.device)
-    return sorted_samples.index_select(0, idx).contiguous()
+def _np_rows(t) -> np.ndarray:
+    return t.detach().cpu().contiguous().numpy()
 
 
 def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchange: Any = None,
-                 ops: Any = None, oversample: int = 64, seed: int = 42,
-                 force_exchange: bool = False):
-    """Globally sort the keys held by all ranks; returns this rank's slice.
-
-    ``local`` is this rank's shard (CUDA tensor for the GPU ops); it is
-    transformed in place.  The returned tensor has the caller's dtype.
-    """
+                 ops: Any = None, oversample: int = 64, seed: int = 42):
+    """Globally sort the keys held by all ranks; returns this rank's slice
+    (a fresh tensor of the caller's dtype).  ``local`` is only read."""
     from . import _cmp_code, dtype_of
     dt = dtype_of(local) if dtype is None else dtype
     core = CORE[dt]
@@ -249,158 +354,146 @@ def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchang
     ex = exchange or TorchExchange()
     ops = ops or GpuOps()
     P, r = ex.P, ex.rank
-
-    # all torch-level handling happens on int32 / int64 views of the keys
-    w = _wire(local, core)
-    ops.to_core(w, dt, cmp)
-    if P == 1 and not force_exchange:
-        ops.sort(w, core)
-        ops.to_core(w, dt, cmp, inverse=True)
-        return local
+    if P > MAX_RANKS:
+        raise ValueError(f"at most {MAX_RANKS} ranks")
     s = oversample * P
-    smp = ops.sample(w, core, s, seed ^ (0x9E3779B97F4A7C15 * (r + 1) & 0xFFFFFFFFFFFFFFFF))
-    if smp.shape[0] < s:  # empty shard: contribute maximum keys (never chosen below)
-        import torch
-        pad = torch.full((s - smp.shape[0],) + tuple(w.shape[1:]), -1, dtype=w.dtype, device=w.device)
-        smp = torch.cat([smp, pad])
+    smp = _pad_sample(ops.sample(local, dt, cmp, s, rank_seed(seed, r)), s, local)
     all_smp = ex.all_gather(smp).contiguous()
-    ops.sort(all_smp, core)
-    spl = pick_splitters(all_smp, P)
-    if getattr(ex, "fused", False) and P <= 8:  # the peer scatter addresses up to 8 ranks
-        return _exchange_fused(w, local, dt, core, cmp, spl, ex, ops)
-    parted, counts = ops.partition(w, core, spl)
-    recv_counts = ex.all_to_all_counts(counts)
-    send = [int(x) for x in counts.tolist()]
-    recv = [int(x) for x in recv_counts.tolist()]
-    got = ex.all_to_all_v(parted, send, recv).contiguous()
-    ops.sort(got, core)
-    ops.to_core(got, dt, cmp, inverse=True)
-    return _unwire(got, core, local)
-
-
-_KEY_BYTES = {_lib.DT_U32: 4, _lib.DT_U64: 8, _lib.DT_REC32: 32}
-
-
-def _bucket_offsets(C: list, P: int, r: int) -> tuple[list, list]:
-    """From the P x P bucket-size matrix (row s = sender s): every rank's receive
-    total and where sender r's bucket j starts inside rank j's buffer."""
-    totals = [sum(C[s][j] for s in range(P)) for j in range(P)]
-    offs = [sum(C[s][j] for s in range(r)) for j in range(P)]
-    return totals, offs
-
-
-def _exchange_fused(w, local, dt: int, core: int, cmp: int, spl, ex, ops):
-    """Partition + exchange in one scatter pass: bucket j lands in rank j's buffer."""
-    import torch
-    P, r = ex.P, ex.rank
-    counts = ops.partition_count(w, core, spl)
-    cpu_group = ex.dist.get_backend(ex.group) == "gloo"
-    allc = ex.all_gather(counts.cpu() if cpu_group else counts)
-    C = allc.view(P, P).cpu().tolist()
-    totals, offs = _bucket_offsets(C, P, r)
-    kb = _KEY_BYTES[core]
-    ex.ensure_capacity(max(totals) * kb, w.device)
-    ex.barrier()  # every receiver is done with its buffer and holds the handles
-    ops.scatter_peers(w, core, P - 1, ex.ptrs, offs)
-    ex.barrier()  # every sender's stores into this rank's buffer have completed
-    rows = (totals[r],) + tuple(w.shape[1:])
-    got = ex.recv[: totals[r] * kb].view(w.dtype).view(rows)
-    ops.sort(got, core)
-    ops.to_core(got, dt, cmp, inverse=True)
-    return _unwire(got, core, local)
+    if all_smp.device != local.device:
+        all_smp = all_smp.to(local.device)
+    ops.sort_core(all_smp, core)
+    uniq_h, mult = splitters(core, _np_rows(all_smp), P)
+    m = len(mult)
+    uniq = ops.put(uniq_h, local)
+    counts = ops.count(local, dt, cmp, uniq, m)
+    C = _np_rows(ex.all_gather(counts)).reshape(P, 2 * m + 1)
+    pl = plan(P, mult, C)
+    w = KEY_BYTES[dt]
+    wl = wire(local, dt)
+    n_recv = int(pl["recv_n"][r])
+    if getattr(ex, "fused", False):
+        ex.ensure_capacity(int(pl["recv_n"].max()) * w, local.device)
+        ex.barrier(ops)  # every receiver is done reading its buffer and holds the handles
+        ops.scatter(local, dt, cmp, m, pl["bin_rank"], pl["bin_off"][r], ex.ptrs)
+        ex.barrier(ops)  # every sender's stores into this rank's buffer have landed
+        recv = ex.recv[: n_recv * w].view(wl.dtype).view((n_recv,) + tuple(wl.shape[1:]))
+    else:
+        off, send = staging_offsets(pl, r)
+        staging = ops.alloc(local.shape[0], wl)
+        ops.scatter(local, dt, cmp, m, pl["bin_rank"], off, [staging] * P)
+        recv = ex.all_to_all_v(staging, send, recv_counts(pl, r)).contiguous()
+    out = ops.finish(recv, n_recv, dt, cmp, uniq, int(pl["lo_val"][r]), int(pl["lo_fill"][r]),
+                     int(pl["hi_val"][r]), int(pl["hi_fill"][r]), wl)
+    return out.view(local.dtype)
 
 
 def sort_sharded_emulated_fused(shards: list, less: Any = "less", *, dtype: int | None = None,
-                                ops: Any = None, oversample: int = 64, seed: int = 42) -> list:
+                                oversample: int = 64, seed: int = 42) -> list:
     """The fused exchange with P ranks emulated in one process on one GPU: each
-    rank's scatter stores its buckets straight into the other ranks' receive
+    rank's scatter stores its bins straight into the other ranks' receive
     buffers (plain device pointers instead of IPC-mapped peers)."""
-    import torch
-    from . import _cmp_code, dtype_of
-    dt = dtype_of(shards[0]) if dtype is None else dtype
-    core = CORE[dt]
-    cmp = _cmp_code(less)
-    P = len(shards)
-    like = shards[0]
-    # one workspace per emulated rank: each keeps its partition plan until its scatter
-    opss = [GpuOps() for _ in range(P)]
-    shards = [_wire(t, core) for t in shards]
-    for t, o in zip(shards, opss):
-        o.to_core(t, dt, cmp)
-    s = oversample * P
-    smps = []
-    for r, t in enumerate(shards):
-        smp = opss[r].sample(t, core, s, seed ^ (0x9E3779B97F4A7C15 * (r + 1) & 0xFFFFFFFFFFFFFFFF))
-        if smp.shape[0] < s:
-            pad = torch.full((s - smp.shape[0],) + tuple(t.shape[1:]), -1, dtype=t.dtype, device=t.device)
-            smp = torch.cat([smp, pad])
-        smps.append(smp)
-    all_smp = torch.cat(smps).contiguous()
-    opss[0].sort(all_smp, core)
-    spl = pick_splitters(all_smp, P)
-    C = [[int(x) for x in opss[r].partition_count(t, core, spl).tolist()] for r, t in enumerate(shards)]
-    totals = [sum(C[s_][j] for s_ in range(P)) for j in range(P)]
-    recvs = [torch.empty((totals[j],) + tuple(shards[0].shape[1:]), dtype=shards[0].dtype,
-                         device=shards[0].device) for j in range(P)]
-    ptrs = [t.data_ptr() for t in recvs]
-    for r, t in enumerate(shards):  # ops[r] still holds rank r's plan in its workspace
-        _, offs = _bucket_offsets(C, P, r)
-        opss[r].scatter_peers(t, core, P - 1, ptrs, offs)
-    out = []
-    for j in range(P):
-        opss[j].sort(recvs[j], core)
-        opss[j].to_core(recvs[j], dt, cmp, inverse=True)
-        out.append(_unwire(recvs[j], core, like))
-    return out
+    return _emulated(shards, less, dtype, [GpuOps() for _ in shards], oversample, seed, fused=True)
 
 
 def sort_sharded_emulated(shards: list, less: Any = "less", *, dtype: int | None = None,
                           ops: Any = None, oversample: int = 64, seed: int = 42) -> list:
-    """Same algorithm as sort_sharded with the exchange done in-process."""
+    """Same algorithm as sort_sharded with the (non-fused) exchange done in-process."""
+    opss = [ops] * len(shards) if ops is not None else [GpuOps() for _ in shards]
+    return _emulated(shards, less, dtype, opss, oversample, seed, fused=False)
+
+
+def _emulated(shards, less, dtype, opss, oversample, seed, fused):
     import torch
     from . import _cmp_code, dtype_of
     dt = dtype_of(shards[0]) if dtype is None else dtype
     core = CORE[dt]
     cmp = _cmp_code(less)
-    ops = ops or GpuOps()
     P = len(shards)
-    like = shards[0]
-    shards = [_wire(t, core) for t in shards]
-    for t in shards:
-        ops.to_core(t, dt, cmp)
-    if P == 1:
-        ops.sort(shards[0], core)
-        ops.to_core(shards[0], dt, cmp, inverse=True)
-        return [_unwire(shards[0], core, like)]
+    wl = [wire(t, dt) for t in shards]
     s = oversample * P
-    smps = []
-    for r, t in enumerate(shards):
-        smp = ops.sample(t, core, s, seed ^ (0x9E3779B97F4A7C15 * (r + 1) & 0xFFFFFFFFFFFFFFFF))
-        if smp.shape[0] < s:
-            pad = torch.full((s - smp.shape[0],) + tuple(t.shape[1:]), -1, dtype=t.dtype, device=t.device)
-            smp = torch.cat([smp, pad])
-        smps.append(smp)
+    smps = [_pad_sample(opss[r].sample(t, dt, cmp, s, rank_seed(seed, r)), s, t) for r, t in enumerate(shards)]
     all_smp = torch.cat(smps).contiguous()
-    ops.sort(all_smp, core)
-    spl = pick_splitters(all_smp, P)
-    parts, counts = zip(*[ops.partition(t, core, spl) for t in shards])
-    cnt = [[int(x) for x in c.tolist()] for c in counts]
+    opss[0].sort_core(all_smp, core)
+    uniq_h, mult = splitters(core, _np_rows(all_smp), P)
+    m = len(mult)
+    uniqs = [opss[r].put(uniq_h, t) for r, t in enumerate(shards)]
+    C = np.stack([_np_rows(opss[r].count(t, dt, cmp, uniqs[r], m)) for r, t in enumerate(shards)])
+    pl = plan(P, mult, C)
+    if fused:
+        recvs = [opss[j].alloc(int(pl["recv_n"][j]), wl[j]) for j in range(P)]
+        for r, t in enumerate(shards):  # ops[r] still holds rank r's plan in its workspace
+            opss[r].scatter(t, dt, cmp, m, pl["bin_rank"], pl["bin_off"][r], recvs)
+    else:
+        stagings, sends = [], []
+        for r, t in enumerate(shards):
+            off, send = staging_offsets(pl, r)
+            st = opss[r].alloc(t.shape[0], wl[r])
+            opss[r].scatter(t, dt, cmp, m, pl["bin_rank"], off, [st] * P)
+            stagings.append(st)
+            sends.append(np.concatenate([[0], np.cumsum(send)]).astype(np.int64))
+        recvs = []
+        for j in range(P):  # rank j receives, in sender order, what each sender grouped for it
+            pieces = [stagings[r][int(sends[r][j]):int(sends[r][j + 1])] for r in range(P)]
+            recvs.append(torch.cat(pieces).contiguous() if pieces else opss[j].alloc(0, wl[j]))
     out = []
-    for j in range(P):  # rank j receives bucket j of every rank, in rank order
-        pieces = []
-        for r in range(P):
-            off = sum(cnt[r][:j])
-            pieces.append(parts[r][off:off + cnt[r][j]])
-        got = torch.cat(pieces).contiguous()
-        ops.sort(got, core)
-        ops.to_core(got, dt, cmp, inverse=True)
-        out.append(_unwire(got, core, like))
+    for j in range(P):
+        o = opss[j].finish(recvs[j], int(pl["recv_n"][j]), dt, cmp, uniqs[j], int(pl["lo_val"][j]),
+                           int(pl["lo_fill"][j]), int(pl["hi_val"][j]), int(pl["hi_fill"][j]), wl[j])
+        out.append(o.view(shards[j].dtype))
     return out
 
 
+def sort_sharded_devices(shards: list, devices: Sequence[int] | None = None, less: Any = "less", *,
+                         dtype: int | None = None, cfg: Any = None):
+    """The single-process C entry (qmsort_gpu_sort_sharded): shard r lives on
+    devices[r] (a device may repeat); returns (slices, Metrics)."""
+    import torch
+    from . import Metrics, SortConfig, _cmp_code, dtype_of
+    lib = _lib.load()
+    dt = dtype_of(shards[0]) if dtype is None else dtype
+    P = len(shards)
+    devs = list(devices) if devices is not None else [t.device.index or 0 for t in shards]
+    total = sum(int(t.shape[0]) for t in shards)
+    ia = (ctypes.c_int * P)(*devs)
+    din = (ctypes.c_void_p * P)(*[t.data_ptr() for t in shards])
+    nin = (ctypes.c_size_t * P)(*[int(t.shape[0]) for t in shards])
+    on = (ctypes.c_size_t * P)()
+    c = (cfg or SortConfig()).to_c()
+    mt = _lib.GpuMetrics()
+    # a balanced split needs about total / P per rank; on QMSORT_ENOWS the call
+    # reports the exact sizes and is repeated once with them
+    caps = [min(total, (3 * total) // (2 * P) + 65536)] * P
+    for attempt in range(2):
+        outs = [torch.empty((max(1, cp),) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+                for cp, t in zip(caps, shards)]
+        dout = (ctypes.c_void_p * P)(*[o.data_ptr() for o in outs])
+        cap = (ctypes.c_size_t * P)(*caps)
+        rc = lib.qmsort_gpu_sort_sharded(dt, _cmp_code(less), P, ia, din, nin, dout, cap, on, ctypes.byref(c),
+                                         ctypes.byref(mt))
+        if rc == _lib.QMSORT_ENOWS and attempt == 0:
+            caps = [int(on[r]) for r in range(P)]
+            del outs
+            continue
+        _lib.check(rc, "qmsort_gpu_sort_sharded")
+        break
+    return [outs[r][: int(on[r])] for r in range(P)], Metrics.from_c(mt)
+
+
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): weak-scaling global sort, N x n keys
+# bench.py --gpus N (torchrun) and --sharded: the north-star sharded configs
 # ---------------------------------------------------------------------------
+# config -> (dtype attr, torch dtype, row shape, generator, keys, key bytes,
+#            scaling, description)
+SHARDED_CONFIGS = {
+    "c2": ("DT_U32", "uint32", (), "GEN_U32", 1 << 28, 4, "weak",
+           "C2 recipe, 2^28 uint32 keys per GPU"),
+    "c3": ("DT_U64", "uint64", (), "GEN_U64", 1 << 30, 8, "strong",
+           "C3: 2^30 uint64 keys in total, shard r = global indices [r n/P, (r+1) n/P)"),
+    "c5": ("DT_REC32", "uint64", (4,), "GEN_REC32", 1 << 26, 32, "strong",
+           "C5: 2^26 32-byte records in total, shard r = global records [r n/P, (r+1) n/P)"),
+}
+
+
 def bench_main(args: Any, metric: str, unit: str) -> None:
     import json
     import os
@@ -414,60 +507,76 @@ def bench_main(args: Any, metric: str, unit: str) -> None:
 
     for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531")):
         os.environ.setdefault(k, v)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0"))))
-    rank, P = dist.get_rank(), dist.get_world_size()
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, P = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", local)
-    n = args.n
-    pristine = torch.empty(n, dtype=torch.uint32, device=dev)
-    q.generate(q.GEN_U32, pristine, seed=42, start=rank * n, total=n * P)
-    x = torch.empty_like(pristine)
-    ex = PeerExchange() if getattr(args, "exchange", "peer") == "peer" else TorchExchange()
+    cfgname = args.config if args.config in SHARDED_CONFIGS else "c2"
+    dt_name, tdt, tail, gen, n_cfg, kb, scaling, desc = SHARDED_CONFIGS[cfgname]
+    dt = getattr(q, dt_name)
+    if scaling == "weak":
+        n_total = args.n * P
+        n_loc = args.n
+        start = rank * n_loc
+    else:
+        n_total = n_cfg
+        start = rank * n_total // P
+        n_loc = (rank + 1) * n_total // P - start
+    pristine = torch.empty((n_loc,) + tail, dtype=getattr(torch, tdt), device=dev)
+    q.generate(getattr(q, gen), pristine, seed=42, start=start, total=n_total)
+    exchange = getattr(args, "exchange", "peer")
+    ex = PeerExchange() if exchange == "peer" else TorchExchange()
     ops = GpuOps()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def step():
-        x.copy_(pristine)
         torch.cuda.synchronize()
         dist.barrier()
         e0.record()
-        out = sort_sharded(x, "less", exchange=ex, ops=ops, force_exchange=True)
+        out = sort_sharded(pristine, "less", dtype=dt, exchange=ex, ops=ops)
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), out
 
-    for _ in range(args.warmup):
+    for _ in range(max(1, args.warmup)):
         step()
-    ops.launches = 0
+    ops.launches = ops.alg_bytes = 0
     times, out = [], None
     for _ in range(args.steps):
         t, out = step()
         times.append(t)
-    launches = ops.launches
+    launches, alg_rank = ops.launches, ops.alg_bytes // max(1, args.steps)
     # verification (untimed): every slice sorted, slices ordered across ranks,
     # multiset of all keys preserved
     viol, s_out, _ = q.check(out)
     _, s_in, _ = q.check(pristine, order=False)
     mask = (1 << 62) - 1
-    ends = torch.tensor([int(out[0].item()) if out.numel() else -1,
-                         int(out[-1].item()) if out.numel() else -1], dtype=torch.int64, device=dev)
-    all_ends = [torch.empty_like(ends) for _ in range(P)]
-    dist.all_gather(all_ends, ends)
+    lens = torch.tensor([out.shape[0]], dtype=torch.int64, device=dev)
+    all_lens = [torch.empty_like(lens) for _ in range(P)]
+    dist.all_gather(all_lens, lens)
+    wout = wire(out, dt)  # NCCL has no unsigned types: int32 / int64 words
+    ends_rows = torch.zeros((2,) + tail, dtype=wout.dtype, device=dev)
+    if out.shape[0]:
+        ends_rows[0], ends_rows[1] = wout[0], wout[-1]
+    all_ends = [torch.empty_like(ends_rows) for _ in range(P)]
+    dist.all_gather(all_ends, ends_rows)
     stats = torch.tensor([viol, s_out & mask, s_in & mask], dtype=torch.int64, device=dev)
     dist.all_reduce(stats)
+    alg_t = torch.tensor([alg_rank], dtype=torch.float64, device=dev)
+    dist.all_reduce(alg_t, op=dist.ReduceOp.MAX)
     ms = statistics.mean(times)
     # end to end: pinned host shard -> H2D -> distributed sort -> D2H of the slice
     host_in = pristine.cpu().pin_memory()
-    e2e_t = []
-    host_out = torch.empty(n + n // 2, dtype=torch.uint32, pin_memory=True)
+    host_out = torch.empty((n_loc * 3 // 2 + 1024,) + tail, dtype=pristine.dtype, pin_memory=True)
     xd = torch.empty_like(pristine)
+    e2e_t, d2h = [], 0
     for i in range(1 + min(args.steps, 3)):
         dist.barrier()
         t0 = time.perf_counter()
         xd.copy_(host_in, non_blocking=True)
-        res = sort_sharded(xd, "less", exchange=ex, ops=ops, force_exchange=True)
+        res = sort_sharded(xd, "less", dtype=dt, exchange=ex, ops=ops)
         if res.shape[0] <= host_out.shape[0]:
             host_out[:res.shape[0]].copy_(res)
         else:
@@ -477,35 +586,54 @@ def bench_main(args: Any, metric: str, unit: str) -> None:
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
         if i:
             e2e_t.append(float(el.item()))
+            d2h = res.shape[0]
+    d2h_t = torch.tensor([d2h], dtype=torch.int64, device=dev)
+    dist.all_reduce(d2h_t)
     if rank == 0:
-        seam_ok = all(int(all_ends[r][1]) <= int(all_ends[r + 1][0]) for r in range(P - 1)
-                      if int(all_ends[r][1]) >= 0 and int(all_ends[r + 1][0]) >= 0)
+        def key_of(row):
+            v = row.view(-1).tolist() if tail else [row.item()]
+            return [x & ((1 << (8 * min(kb, 8))) - 1) for x in v]
+        pairs = [(int(all_lens[r].item()), all_ends[r]) for r in range(P)]
+        nonempty = [e for ln, e in pairs if ln > 0]
+        seam_ok = all(key_of(nonempty[i][1]) <= key_of(nonempty[i + 1][0]) for i in range(len(nonempty) - 1))
         e2e_ms = statistics.mean(e2e_t) * 1e3
-        peak = 6552.6
+        peak = 6555.2
         try:
             peak = float(json.load(open(os.path.join(os.path.dirname(os.path.dirname(__file__)),
                                                      "MEASURED_PEAKS.json")))["hbm_gbs"])
         except OSError:
             pass
-        # per-GPU pass ledger: partition (count 1 + scatter 2) + exchange (2) + local sort (8)
-        alg = (3 + 2 + 8) * n * 4
-        line = {"metric": metric, "value": n * P / (ms / 1e3) / 1e9, "unit": unit, "n_gpus": P,
+        n_max = max(int(x.item()) for x in all_lens)
+        # per-rank pass ledger from the device counters: count 1 + scatter
+        # (= the exchange) 2 + the local sort's own ledger (8 for uniform keys)
+        alg = float(alg_t.item())
+        nvl_bytes = (P - 1) * n_loc * kb / P  # bytes each rank ships over NVLink
+        t_hbm = alg / peak / 1e6           # ms at the HBM roofline
+        t_nvl = nvl_bytes / 900.0 / 1e6    # ms at 900 GB/s per direction
+        line = {"metric": metric if cfgname == "c2" else f"sorted Gkeys/s, {desc} (sharded)",
+                "value": n_total / (ms / 1e3) / 1e9, "unit": unit, "n_gpus": P,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-                "data": "synthetic (seeded SplitMix64, SURVEY.md 8(d) C2 recipe, seed 42)",
-                "config": {"workload": f"distributed samplesort of {P} x 2^{n.bit_length() - 1} "
-                                       "uint32 keys (" + ("exchange fused into the scatter: IPC peer stores over NVLink" if getattr(args, "exchange", "peer") == "peer" else "one NCCL all-to-all") + ")",
-                           "n_per_gpu": n, "parallelism": f"sharded samplesort x{P}",
-                           "l2": "input 1 GiB per GPU > L2"},
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+                "dtype": {"DT_U32": "u32", "DT_U64": "u64", "DT_REC32": "4xu64"}[dt_name],
+                "data": f"synthetic (seeded SplitMix64, SURVEY.md 8(d) {cfgname.upper()} recipe, seed 42)",
+                "config": {"workload": f"distributed samplesort, {desc}, {P} rank(s) (" +
+                                       ("exchange fused into the scatter: IPC peer stores over NVLink"
+                                        if exchange == "peer" else "one NCCL all-to-all") + ")",
+                           "n_total": n_total, "n_per_gpu": n_loc, "largest_slice": n_max,
+                           "key_bytes": kb, "parallelism": f"sharded samplesort x{P}",
+                           "l2": "input > L2 on every rank"},
+                "step_ms": [round(t, 4) for t in times],
                 "gpu_launches": launches,
-                "roofline": {"bound": "hbm", "kernel": "whole per-GPU pipeline", "achieved": alg / (ms * 1e6),
-                             "peak": peak, "unit": "GB/s", "frac": alg / (ms * 1e6) / peak, "traffic": None,
-                             # SURVEY.md 8(d) sharded roofline: HBM leg + NVLink leg, serial phases
-                             "nvlink": {"bytes_per_rank": (P - 1) * n * 4 // P, "peak_GBps": 900.0,
-                                        "t_roof_ms": (alg / peak + (P - 1) * n * 4 / P / 900.0) / 1e6,
-                                        "frac_of_step": ((alg / peak + (P - 1) * n * 4 / P / 900.0) / 1e6) / ms}},
-                "e2e": {"value": n * P / (e2e_ms / 1e3) / 1e9, "unit": unit, "ms_per_step": e2e_ms,
-                        "h2d_bytes_per_step": n * 4 * P, "d2h_bytes_per_step": n * 4 * P,
+                "roofline": {"bound": "hbm", "kernel": "whole per-GPU pipeline (max over ranks)",
+                             "achieved": alg / (ms * 1e6), "peak": peak, "unit": "GB/s",
+                             "frac": alg / (ms * 1e6) / peak, "traffic": None,
+                             "alg_bytes_per_rank": alg, "ledger_bytes_over_nw": alg / (n_loc * kb),
+                             "hbm_frac": t_hbm / ms,
+                             "nvlink": {"bytes_per_rank": nvl_bytes, "peak_GBps": 900.0,
+                                        "achieved_GBps": nvl_bytes / (ms * 1e6), "frac": t_nvl / ms},
+                             "t_roof_ms": t_hbm + t_nvl, "frac_of_serial_roofline": (t_hbm + t_nvl) / ms},
+                "e2e": {"value": n_total / (e2e_ms / 1e3) / 1e9, "unit": unit, "ms_per_step": e2e_ms,
+                        "h2d_bytes_per_step": n_total * kb, "d2h_bytes_per_step": int(d2h_t.item()) * kb,
                         "api": "sharded.sort_sharded on pinned host shards (H2D + sort + D2H per rank)"},
                 "verify": {"order_violations_within_slices": int(stats[0].item()),
                            "slices_ordered_across_ranks": seam_ok,

@@ -59,11 +59,16 @@ def test_partition_by_splitters(nsplit):
     spl = np.sort(rng.integers(0, 2**32, nsplit, dtype=np.uint64).astype(np.uint32))
     t = torch.from_numpy(a).cuda()
     s = torch.from_numpy(spl).cuda()
-    out, counts = sharded.GpuOps().partition(t.view(torch.int32), _lib.DT_U32, s.view(torch.int32))
+    out = torch.empty_like(t)
+    counts = torch.zeros(nsplit + 1, dtype=torch.int64, device="cuda")
+    lib = _lib.load()
+    rc = lib.qmsort_gpu_partition(_lib.DT_U32, t.data_ptr(), t.shape[0], s.data_ptr(), nsplit, out.data_ptr(),
+                                  counts.data_ptr(), None, 0, torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "qmsort_gpu_partition")
     torch.cuda.synchronize()
     b = np.searchsorted(spl, a, side="left")
     np.testing.assert_array_equal(counts.cpu().numpy(), np.bincount(b, minlength=nsplit + 1))
-    got = out.cpu().numpy().view(np.uint32)
+    got = out.cpu().numpy()
     off = 0
     for j, c in enumerate(counts.cpu().numpy()):
         np.testing.assert_array_equal(np.sort(got[off:off + c]), np.sort(a[b == j]))
@@ -83,6 +88,15 @@ def test_emulated_fused_exchange_matches_oracle(oracle, P, cfg, dt):
     torch.cuda.synchronize()
     got = np.concatenate([o.cpu().numpy() for o in out])
     np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+def test_emulated_fused_exchange_leaves_input_untouched(oracle):
+    a = oracle.gen("f64_gauss", 100000, seed=1)
+    shards = shards_of(a, 4)
+    before = [t.clone() for t in shards]
+    out = sharded.sort_sharded_emulated_fused(shards, "less", dtype=DT_F64)
+    assert all(torch.equal(x, y) for x, y in zip(shards, before))
+    np.testing.assert_array_equal(np.concatenate([o.cpu().numpy() for o in out]), np.sort(a))
 
 
 def test_emulated_fused_exchange_descending_and_ragged(oracle):
@@ -144,3 +158,81 @@ def test_ipc_peer_exchange_processes(world):
     for rep, m in enumerate((n, n, 3 * n)):
         got = np.concatenate([parts[r][rep] for r in range(world)])
         np.testing.assert_array_equal(got, np.sort(full[:m * world]))
+
+
+# ---- the single-process C entry over several (here: repeated) devices ------
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+@pytest.mark.parametrize("cfg,dt", [("u32", DT_U32), ("u64", DT_U64), ("rec32", DT_REC32),
+                                    ("f64_gauss", DT_F64), ("f64_distinct16", DT_F64), ("i32", 0)])
+def test_c_sort_sharded_matches_oracle(oracle, P, cfg, dt):
+    """qmsort_gpu_sort_sharded with devices [0] * P: the same kernels and the
+    same peer-store exchange as P GPUs, driven by one host thread per rank."""
+    n = (1 << 19) + 777
+    if cfg == "i32":
+        a = np.random.default_rng(3).integers(-2**31, 2**31, n).astype(np.int32)
+    else:
+        a = oracle.gen(cfg, n, seed=11)
+    shards = shards_of(a, P)
+    before = [t.clone() for t in shards]
+    out, m = sharded.sort_sharded_devices(shards, [0] * P, "less", dtype=dt)
+    got = np.concatenate([o.cpu().numpy() for o in out])
+    np.testing.assert_array_equal(got, np.sort(a) if cfg == "i32" else oracle.sort(dt, a))
+    assert all(torch.equal(x, y) for x, y in zip(shards, before)), "input shards must be read only"
+    assert m.kernel_launches > 0 and m.elapsed_ns > 0
+
+
+@pytest.mark.parametrize("P", [2, 5, 8])
+def test_c_sort_sharded_descending_ragged_empty(oracle, P):
+    a = oracle.gen("u64", 300001, seed=4)
+    cuts = sorted(np.random.default_rng(P).integers(0, a.shape[0], P - 1).tolist())
+    parts = np.split(a, cuts)
+    if P > 2:
+        parts[1] = parts[1][:0]  # an empty shard
+    a = np.concatenate(parts)
+    shards = [torch.from_numpy(x.copy()).cuda() for x in parts]
+    out, _ = sharded.sort_sharded_devices(shards, [0] * P, "greater", dtype=DT_U64)
+    got = np.concatenate([o.cpu().numpy() for o in out])
+    np.testing.assert_array_equal(got, oracle.sort(DT_U64, a, greater=True))
+
+
+@pytest.mark.parametrize("path", ["c", "emulated_fused", "emulated_staged"])
+def test_sharded_duplicate_heavy_is_balanced(oracle, path):
+    """C4c-shaped input (16 distinct values) and a 70 % hot key: the ranks a
+    repeated splitter spans share its keys as fills -- no rank takes them all."""
+    for a in (oracle.gen("f64_distinct16", 1 << 20, seed=2),
+              np.where(np.random.default_rng(1).random(1 << 20) < 0.7, 3.0,
+                       np.random.default_rng(2).normal(size=1 << 20))):
+        a = a.copy()
+        a[a == 0] = 0.0
+        P = 8
+        shards = shards_of(a, P)
+        if path == "c":
+            out, _ = sharded.sort_sharded_devices(shards, [0] * P, "less", dtype=DT_F64)
+        elif path == "emulated_fused":
+            out = sharded.sort_sharded_emulated_fused(shards, "less", dtype=DT_F64)
+        else:
+            out = sharded.sort_sharded_emulated(shards, "less", dtype=DT_F64)
+        got = np.concatenate([o.cpu().numpy() for o in out])
+        np.testing.assert_array_equal(got, np.sort(a))
+        sizes = [o.shape[0] for o in out]
+        assert max(sizes) <= 0.2 * a.shape[0], sizes
+
+
+def test_c_sort_sharded_errors():
+    import ctypes
+    lib = _lib.load()
+    x = torch.arange(1000, dtype=torch.int64, device="cuda").view(torch.uint64)
+    din = (ctypes.c_void_p * 2)(x.data_ptr(), x.data_ptr())
+    nin = (ctypes.c_size_t * 2)(1000, 1000)
+    dev = (ctypes.c_int * 2)(0, 0)
+    small = torch.empty(10, dtype=torch.uint64, device="cuda")
+    dout = (ctypes.c_void_p * 2)(small.data_ptr(), small.data_ptr())
+    cap = (ctypes.c_size_t * 2)(10, 10)
+    on = (ctypes.c_size_t * 2)()
+    rc = lib.qmsort_gpu_sort_sharded(DT_U64, 0, 2, dev, din, nin, dout, cap, on, None, None)
+    assert rc == _lib.QMSORT_ENOWS and on[0] + on[1] == 2000
+    rc = lib.qmsort_gpu_sort_sharded(DT_U64, 0, 9, dev, din, nin, dout, cap, on, None, None)
+    assert rc == _lib.QMSORT_EINVAL
+    bad = (ctypes.c_int * 2)(0, 99)
+    rc = lib.qmsort_gpu_sort_sharded(DT_U64, 0, 2, bad, din, nin, dout, cap, on, None, None)
+    assert rc == _lib.QMSORT_EINVAL

@@ -110,16 +110,65 @@ def test_duplicate_heavy_keys_emulated():
     np.testing.assert_array_equal(np.concatenate([o.numpy() for o in out]), np.sort(full))
 
 
-@pytest.mark.parametrize("P", [1, 2, 5])
-def test_fused_exchange_offsets_tile_every_receive_buffer(P):
-    """_bucket_offsets: sender r's bucket j occupies [offs_r[j], offs_r[j] + C[r][j])
-    of rank j's buffer; the pieces tile [0, total_j) in sender order."""
+def test_duplicate_heavy_keys_balanced():
+    """A value that fills several splitter slots is spread over the ranks it
+    spans (fills), so no rank receives every copy of a frequent key."""
+    full = np.where(np.random.default_rng(4).random(40000) < 0.7, 5.0,
+                    np.random.default_rng(5).normal(size=40000))
+    full[full == 0] = 0.0
+    shards = [torch.from_numpy(x.copy()) for x in np.array_split(full, 8)]
+    out = sharded.sort_sharded_emulated(shards, "less", dtype=_lib.DT_F64, ops=NumpyOps(), oversample=16)
+    np.testing.assert_array_equal(np.concatenate([o.numpy() for o in out]), np.sort(full))
+    sizes = [o.shape[0] for o in out]
+    assert max(sizes) < 0.3 * full.shape[0], sizes
+
+
+def _plan_random(P, m, rng):
+    mult = [1] * m
+    for _ in range(P - 1 - m):
+        mult[int(rng.integers(0, m))] += 1
+    C = rng.integers(0, 50, (P, 2 * m + 1))
+    return mult, C
+
+
+@pytest.mark.parametrize("P", [1, 2, 5, 8])
+def test_plan_tiles_every_receive_buffer(P):
+    """qmsort_gpu_shard_plan: sender s's bin b occupies [bin_off[s][b],
+    bin_off[s][b] + C[s][b]) of rank bin_rank[b]'s buffer; the pieces tile
+    [0, recv_n[r]) in sender order, and each rank's slice (fills + received)
+    covers the global order exactly once."""
     rng = np.random.default_rng(P)
-    C = rng.integers(0, 50, (P, P)).tolist()
-    for j in range(P):
-        pos = 0
+    for trial in range(20):
+        m = int(rng.integers(0 if P == 1 else 1, P)) if P > 1 else 0
+        mult, C = _plan_random(P, m, rng)
+        pl = sharded.plan(P, mult, C)
+        br, bo = pl["bin_rank"], pl["bin_off"]
         for r in range(P):
-            totals, offs = sharded._bucket_offsets(C, P, r)
-            assert offs[j] == pos
-            pos += C[r][j]
-        assert pos == totals[j]
+            pos = 0
+            for s_ in range(P):
+                for b in range(2 * m + 1):
+                    if br[b] == r:
+                        assert bo[s_][b] == pos
+                        pos += C[s_][b]
+            assert pos == pl["recv_n"][r]
+        # global order: bin b's keys (all senders) precede bin b+1's
+        total = int(C.sum())
+        assert int((pl["recv_n"] + pl["lo_fill"] + pl["hi_fill"]).sum()) == total
+        for j in range(m):
+            e = int(C[:, 2 * j + 1].sum())
+            if mult[j] >= 2:
+                assert br[2 * j + 1] == -1
+                shares = [int(pl["hi_fill"][r]) for r in range(P) if pl["hi_val"][r] == j] + \
+                         [int(pl["lo_fill"][r]) for r in range(P) if pl["lo_val"][r] == j]
+                assert sum(shares) == e and max(shares) - min(shares) <= 1
+            else:
+                assert br[2 * j + 1] == br[2 * j]
+        assert list(br[::2]) == sorted(br[::2])
+
+
+def test_splitters_merge_duplicates():
+    smp = np.array([1, 1, 1, 1, 1, 1, 7, 9], dtype=np.uint32)  # quantiles at 1,2,...,7 of 8 for P=8
+    uniq, mult = sharded.splitters(_lib.DT_U32, smp, 8)
+    assert uniq.view(np.uint32).tolist() == [1, 7, 9] and mult == [5, 1, 1]
+    uniq, mult = sharded.splitters(_lib.DT_U32, smp, 1)
+    assert uniq.size == 0 and mult == []
