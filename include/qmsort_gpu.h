@@ -64,7 +64,11 @@ typedef struct {
                                         2 clever_quicksort                         */
     uint64_t base_case_size_threshold; /* BaseCasePolicy::size_threshold (10)     */
     int base_case_use_levels;        /* BaseCasePolicy::use_levels                 */
-    double beta;                     /* 0.5                                        */
+    double beta;                     /* 0.5; with base_case_use_levels the largest
+                                        bucket the block sorter takes is n^beta
+                                        (clamped to its size classes), the GPU
+                                        form of "X on blocks of ~n^beta"
+                                        (sort.hpp:91-96)                             */
     double delta;                    /* 1/16; hybrid: a bucket larger than
                                         (parent / buckets) / delta is re-split with
                                         the triple-median sample next level         */
@@ -100,6 +104,9 @@ typedef struct {
     uint32_t phase_launches[QMSORT_NUM_PHASES];
     uint32_t resplits;    /* hybrid pivot: buckets outside the delta band that
                              were re-sampled with triple medians (sort.hpp:114-118) */
+    uint64_t sample_keys; /* splitter-sample keys drawn over all levels (median_of_3:
+                             32 K per segment; median_of_sqrt_n: 2 floor(sqrt(len)/2)+1,
+                             the reference's s, partition.hpp:240-241) */
 } qmsort_gpu_metrics;
 
 /* Presets qms() / qmqs() / momqms() / hqms() (sort.hpp:37-66). */
@@ -204,6 +211,20 @@ int qmsort_gpu_partition_count(int core_dtype, const void* d_in, size_t n, const
 int qmsort_gpu_partition_scatter_peers(int core_dtype, const void* d_in, size_t n, uint32_t nsplit,
                                        void* const* dests, const uint64_t* dest_offsets,
                                        void* d_ws, size_t ws_bytes, void* stream);
+
+/* ---- PartitionResult (partition_result.hpp:12-17) ----------------------- */
+/* Three-way partition of d_data[0..n) around the pivot value *h_pivot (caller
+ * dtype, host memory) under cmp, in place: on return [0, c0) < pivot,
+ * [c0, c0 + c1) == pivot, [c0 + c1, n) > pivot, with h_counts3 = {c0, c1, c2}
+ * -- PartitionResult{lt_end = c0, gt_begin = c0 + c1, left_size = c0,
+ * right_size = c2} (the three-way contract of three_way_partition,
+ * partition.hpp:196-230).  The arrangement inside each part is unspecified. */
+size_t qmsort_gpu_partition3_workspace_bytes(int dtype, size_t n);
+int qmsort_gpu_partition3(int dtype, int cmp, void* d_data, size_t n, const void* h_pivot, uint64_t* h_counts3,
+                          const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes, qmsort_gpu_metrics* metrics,
+                          void* stream);
+int qmsort_gpu_partition3_host(int dtype, int cmp, void* h_data, size_t n, const void* h_pivot,
+                               uint64_t* h_counts3, const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics);
 
 /* ---- the distributed samplesort ------------------------ */
 /* Single-process entry over P <= 8 devices (one host thread drives them all):

@@ -23,6 +23,7 @@
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <vector>
 
 #include "qmsort_gpu.h"
 
@@ -80,10 +81,27 @@ struct Metrics {  // metrics.hpp:14-24 (comparisons/moves are not counted on the
     std::uint64_t elapsed_ns = 0;
 };
 
+// partition_result.hpp:12-17: [0, lt_end) < pivot, [lt_end, gt_begin) ==
+// pivot, [gt_begin, n) > pivot (the three-way contract, partition.hpp:196-230).
+struct PartitionResult {
+    std::size_t lt_end = 0;
+    std::size_t gt_begin = 0;
+    std::size_t left_size = 0;
+    std::size_t right_size = 0;
+};
+
 // Element type -> qmsort_dtype.  A user-defined 32-byte record is enabled by
-// specialising qmsort::gpu::is_rec32<T> (lexicographic over four uint64 words).
+// specialising qmsort::gpu::is_rec32<T>: a declaration that T is four uint64
+// words whose std::less order (T's operator<) is lexicographic over w0..w3.
+// A record comparator functor other than std::less / std::greater must be
+// declared the same way through qmsort::gpu::rec32_order<Less, T> (value
+// QMSORT_LESS for the lexicographic order, QMSORT_GREATER for its reverse);
+// any other comparator is rejected at compile time -- the GPU cannot run an
+// arbitrary functor, and a silent substitution would sort wrongly.
 template <class T>
 struct is_rec32 : std::false_type {};
+template <class Less, class T>
+struct rec32_order : std::integral_constant<int, -1> {};
 template <class T>
 constexpr int scalar_code() {
     if constexpr (std::is_integral_v<T> && std::is_signed_v<T> && sizeof(T) == 4) return QMSORT_DT_I32;
@@ -119,9 +137,11 @@ constexpr int cmp_code() {
     if constexpr (std::is_same_v<Less, std::less<>> || std::is_same_v<Less, std::less<T>>) return QMSORT_LESS;
     else if constexpr (std::is_same_v<Less, std::greater<>> || std::is_same_v<Less, std::greater<T>>)
         return QMSORT_GREATER;
-    else if constexpr (is_rec32<T>::value) return QMSORT_LESS;  // the record's lexicographic order
+    else if constexpr (is_rec32<T>::value && rec32_order<Less, T>::value >= 0) return rec32_order<Less, T>::value;
     else {
-        static_assert(sizeof(Less) == 0, "comparator must be std::less or std::greater");
+        static_assert(sizeof(Less) == 0,
+                      "comparator must be std::less or std::greater (records: or a functor declared through "
+                      "qmsort::gpu::rec32_order<Less, T>)");
         return -1;
     }
 }
@@ -150,31 +170,92 @@ inline void throw_on(int rc, const char* where) {
                                  "): " + qmsort_gpu_last_error());
 }
 
-// Host-range drop-in for qmsort::sort(first, last, cfg, less).
+// Is It a contiguous iterator (C++20 concept; pointers and the standard
+// contiguous containers' iterators before C++20)?
+template <class It>
+constexpr bool is_contiguous() {
+#if __cplusplus >= 202002L
+    return std::contiguous_iterator<It>;
+#else
+    using T = typename std::iterator_traits<It>::value_type;
+    return std::is_pointer_v<It> || std::is_same_v<It, typename std::vector<T>::iterator> ||
+           std::is_same_v<It, typename std::vector<T>::const_iterator>;
+#endif
+}
+
+template <class T, class Cfg, class Less>
+void sort_contiguous(T* p, std::size_t n, const Cfg& cfg, qmsort_gpu_metrics& gm) {
+    qmsort_gpu_config c = to_c(cfg);
+    if constexpr (is_keyed_element<T>::value && !is_rec32<T>::value) {
+        // Element<PayloadBytes>: ordered on the key alone (element.hpp:17-18)
+        using Key = std::remove_cv_t<decltype(std::declval<T&>().key)>;
+        throw_on(qmsort_gpu_sort_elements_host(scalar_code<Key>(), cmp_code<Less, T>(), p, n, sizeof(T),
+                                               offsetof(T, key), &c, &gm),
+                 "qmsort_gpu_sort_elements_host");
+    } else {
+        throw_on(qmsort_gpu_sort_host(dtype_code<T>(), cmp_code<Less, T>(), p, n, &c, &gm), "qmsort_gpu_sort_host");
+    }
+}
+
+// Host-range drop-in for qmsort::sort(first, last, cfg, less) (sort.hpp:215-226).
+// Any random-access range, like the reference's: a contiguous one is sorted
+// in place through the host-array call; another (std::deque ...) is gathered
+// into a contiguous buffer, sorted, and written back.
 template <class It, class Cfg = SortConfig, class Less = std::less<>, class Observer = void>
 Metrics sort(It first, It last, const Cfg& cfg = Cfg{}, Less = Less{}, Observer* = nullptr) {
     using T = typename std::iterator_traits<It>::value_type;
     static_assert(std::is_base_of_v<std::random_access_iterator_tag,
                                     typename std::iterator_traits<It>::iterator_category>,
-                  "contiguous random-access range required");
+                  "random-access range required");
     const std::size_t n = static_cast<std::size_t>(last - first);
     Metrics m;
     if (n == 0) return m;
-    qmsort_gpu_config c = to_c(cfg);
     qmsort_gpu_metrics gm{};
-    if constexpr (is_keyed_element<T>::value && !is_rec32<T>::value) {
-        // Element<PayloadBytes>: ordered on the key alone (element.hpp:17-18)
-        using Key = std::remove_cv_t<decltype(std::declval<T&>().key)>;
-        throw_on(qmsort_gpu_sort_elements_host(scalar_code<Key>(), cmp_code<Less, T>(), &*first, n,
-                                               sizeof(T), offsetof(T, key), &c, &gm),
-                 "qmsort_gpu_sort_elements_host");
+    if constexpr (is_contiguous<It>()) {
+        sort_contiguous<T, Cfg, Less>(&*first, n, cfg, gm);
     } else {
-        throw_on(qmsort_gpu_sort_host(dtype_code<T>(), cmp_code<Less, T>(), &*first, n, &c, &gm),
-                 "qmsort_gpu_sort_host");
+        std::vector<T> buf(first, last);
+        sort_contiguous<T, Cfg, Less>(buf.data(), n, cfg, gm);
+        std::copy(buf.begin(), buf.end(), first);
     }
     m.max_depth = gm.max_depth;
     m.elapsed_ns = gm.elapsed_ns;
     return m;
+}
+
+// sort_range_counted(first, last, cfg, cmp, m, obs) (sort.hpp:207-211): sort
+// with a caller-owned comparator object and Metrics; the counters accumulate
+// into m (elapsed_ns adds the device time, max_depth the deepest partition;
+// comparisons / moves are not counted on the GPU).  Cmp is std::less /
+// std::greater (or a declared record order); the reference's
+// CountingComparator<Less> wrapper is unwrapped to its Less by the caller.
+template <class It, class Cfg, class Cmp, class Observer = void>
+void sort_range_counted(It first, It last, const Cfg& cfg, Cmp& cmp, Metrics& m, Observer* obs = nullptr) {
+    const Metrics r = sort(first, last, cfg, cmp, obs);
+    m.elapsed_ns += r.elapsed_ns;
+    m.max_depth = std::max(m.max_depth, r.max_depth);
+}
+
+// Three-way partition of a host range around `pivot` (a value) under Less,
+// in place on the B200: the PartitionResult of partition_result.hpp:12-17.
+template <class It, class Less = std::less<>>
+PartitionResult partition(It first, It last, const typename std::iterator_traits<It>::value_type& pivot,
+                          Less = Less{}, Metrics* m = nullptr) {
+    using T = typename std::iterator_traits<It>::value_type;
+    static_assert(is_contiguous<It>(), "partition needs a contiguous range");
+    const std::size_t n = static_cast<std::size_t>(last - first);
+    std::uint64_t c[3] = {0, 0, 0};
+    qmsort_gpu_metrics gm{};
+    throw_on(qmsort_gpu_partition3_host(dtype_code<T>(), cmp_code<Less, T>(), n ? &*first : nullptr, n, &pivot, c,
+                                        nullptr, &gm),
+             "qmsort_gpu_partition3_host");
+    if (m) m->elapsed_ns += gm.elapsed_ns;
+    PartitionResult r;
+    r.lt_end = static_cast<std::size_t>(c[0]);
+    r.gt_begin = static_cast<std::size_t>(c[0] + c[1]);
+    r.left_size = r.lt_end;
+    r.right_size = static_cast<std::size_t>(c[2]);
+    return r;
 }
 
 // select_nth(first, last, k, cmp, m) (selection.hpp:207-212): k is 1-based;
@@ -184,6 +265,7 @@ template <class It, class Less = std::less<>>
 std::size_t select_nth(It first, It last, std::size_t k, Less = Less{}, Metrics* m = nullptr,
                        const SortConfig& cfg = SortConfig{}) {
     using T = typename std::iterator_traits<It>::value_type;
+    static_assert(is_contiguous<It>(), "select_nth needs a contiguous range");
     const std::size_t n = static_cast<std::size_t>(last - first);
     qmsort_gpu_config c = to_c(cfg);
     qmsort_gpu_metrics gm{};

@@ -19,6 +19,8 @@ reference (C++)                        here
   (element.hpp:13-20)                    payload moved; stable on the GPU)
 ``select_nth(first, last, k, cmp, m)`` :func:`select_nth` (1-based k, returns the
   (selection.hpp:207-212)                position; range partitioned around it)
+``PartitionResult``                    :class:`PartitionResult`, :func:`partition`
+  (partition_result.hpp:12-17)           (three-way, around a pivot value)
 =====================================  ============================================
 
 All compute goes through the CUDA library (``libqmsort_gpu.so``) via the C-ABI
@@ -40,6 +42,7 @@ __all__ = [
     "QmsortError",
     "DT_I32", "DT_U32", "DT_U64", "DT_F64", "DT_REC32", "DT_I64", "LESS", "GREATER",
     "workspace_bytes", "generate", "check", "dtype_of", "sort_elements", "select_nth",
+    "PartitionResult", "partition",
 ]
 
 
@@ -159,6 +162,7 @@ class Metrics:
     phase_ns: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
     phase_launches: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
     resplits: int = 0  # hybrid pivot: buckets re-sampled with triple medians (f1)
+    sample_keys: int = 0  # splitter-sample keys drawn (median_of_sqrt_n: the reference's s per segment)
 
     @classmethod
     def from_c(cls, m: _lib.GpuMetrics) -> "Metrics":
@@ -363,6 +367,48 @@ def select_nth(data: Any, k: int, cmp: Any = "less", metrics: Metrics | None = N
         metrics.levels += r.levels
         metrics.kernel_launches += r.kernel_launches
     return int(pos.value)
+
+
+@dataclasses.dataclass
+class PartitionResult:
+    """partition_result.hpp:12-17: [0, lt_end) < pivot, [lt_end, gt_begin) ==
+    pivot, [gt_begin, n) > pivot under the comparator."""
+
+    lt_end: int = 0
+    gt_begin: int = 0
+    left_size: int = 0
+    right_size: int = 0
+
+
+def partition(data: Any, pivot: Any, less: Any = "less", cfg: SortConfig | None = None, *,
+              dtype: int | None = None, stream: Any = None) -> PartitionResult:
+    """Three-way partition of ``data`` around the pivot value in place on the
+    GPU (``qmsort_gpu_partition3``; the contract of three_way_partition,
+    partition.hpp:196-230).  ``pivot`` is a scalar (or a 4-word record)."""
+    import numpy as np
+    lib = _lib.load()
+    c = (cfg or SortConfig()).to_c()
+    m = _lib.GpuMetrics()
+    dt = dtype_of(data) if dtype is None else int(dtype)
+    npdt = {DT_I32: np.int32, DT_U32: np.uint32, DT_U64: np.uint64, DT_F64: np.float64, DT_I64: np.int64,
+            DT_REC32: np.uint64}[dt]
+    pv = np.ascontiguousarray(np.asarray(pivot, dtype=npdt).reshape(-1))
+    if pv.nbytes != lib.qmsort_gpu_dtype_size(dt):
+        raise ValueError("pivot must be one element of the array's type")
+    cnt = (ctypes.c_uint64 * 3)()
+    n = int(data.shape[0])
+    if _is_torch_cuda(data):
+        if not data.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        rc = lib.qmsort_gpu_partition3(dt, _cmp_code(less), data.data_ptr(), n, pv.ctypes.data, cnt,
+                                       ctypes.byref(c), None, 0, ctypes.byref(m), _stream_ptr(stream))
+        _lib.check(rc, "qmsort_gpu_partition3")
+    else:
+        rc = lib.qmsort_gpu_partition3_host(dt, _cmp_code(less), _host_ptr(data), n, pv.ctypes.data, cnt,
+                                            ctypes.byref(c), ctypes.byref(m))
+        _lib.check(rc, "qmsort_gpu_partition3_host")
+    c0, c1, c2 = int(cnt[0]), int(cnt[1]), int(cnt[2])
+    return PartitionResult(c0, c0 + c1, c0, c2)
 
 
 def _host_ptr(data: Any) -> int:

@@ -65,6 +65,7 @@ class GpuMetrics(ctypes.Structure):
         ("phase_ns", ctypes.c_uint64 * 8),
         ("phase_launches", ctypes.c_uint32 * 8),
         ("resplits", ctypes.c_uint32),
+        ("sample_keys", ctypes.c_uint64),
     ]
 
 
@@ -104,6 +105,9 @@ EXPORTED = [
     "qmsort_gpu_shard_plan",
     "qmsort_gpu_shard_scatter",
     "qmsort_gpu_shard_finish",
+    "qmsort_gpu_partition3_workspace_bytes",
+    "qmsort_gpu_partition3",
+    "qmsort_gpu_partition3_host",
 ]
 
 _lib = None
@@ -164,6 +168,9 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_shard_scatter": (i, [i, i, vp, sz, u32, ctypes.POINTER(i32), ctypes.POINTER(u64),
                                          ctypes.POINTER(vp), u32, vp, sz, vp]),
         "qmsort_gpu_shard_finish": (i, [i, i, vp, sz, vp, i32, u64, i32, u64, vp, cfgp, vp, sz, mp, vp]),
+        "qmsort_gpu_partition3_workspace_bytes": (sz, [i, sz]),
+        "qmsort_gpu_partition3": (i, [i, i, vp, sz, vp, ctypes.POINTER(u64), cfgp, vp, sz, mp, vp]),
+        "qmsort_gpu_partition3_host": (i, [i, i, vp, sz, vp, ctypes.POINTER(u64), cfgp, mp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -156,6 +157,7 @@ enum Phase {
 struct Ledger {
     uint64_t alg_bytes = 0;
     uint32_t launches = 0, syncs = 0, levels = 0, merge_passes = 0, resplits = 0;
+    uint64_t sample_keys = 0;
     uint64_t ph_bytes[QMSORT_NUM_PHASES] = {};
     uint32_t ph_launches[QMSORT_NUM_PHASES] = {};
     bool prof = false;
@@ -314,26 +316,44 @@ struct WsLayout {
     size_t tree_off[2] = {0, 0}, sorted_off[2] = {0, 0}, lut_off[2] = {0, 0};
     size_t hist_off = 0, tasks_off = 0, fills_off = 0, misc_off = 0, total = 0;
     uint32_t seg_cap = 0, chunk_cap = 0, split_cap = 0, task_cap = 0, fill_cap = 0, hist_cap = 0;
+    uint32_t min_cap = 0;  // smallest block-sort takeover size the work lists are sized for
     uint64_t chunk_elems = 0;
 };
 
+// The largest bucket the block sorter takes: every bucket that fits one CTA,
+// or -- beta with base_case.use_levels (base_case_levels, sort.hpp:91-96:
+// X on blocks of about n^beta) -- n^beta clamped to the size classes.
 template <class K>
-static WsLayout make_layout(size_t n) {
+static uint32_t takeover_cap(size_t n, const qmsort_gpu_config* cfg) {
+    constexpr uint32_t cap_max = class_cap<K>(kNumClasses - 1);
+    if (!cfg || !cfg->base_case_use_levels || !(cfg->beta > 0.0 && cfg->beta < 1.0)) return cap_max;
+    const double t = std::pow((double)std::max<size_t>(n, 2), cfg->beta);
+    return (uint32_t)std::min<double>(cap_max, std::max<double>(class_cap<K>(0), t));
+}
+
+template <class K>
+static WsLayout make_layout(size_t n, uint32_t min_cap = class_cap<K>(kNumClasses - 1)) {
     using TU = Tune<K>;
-    constexpr uint64_t cap = class_cap<K>(kNumClasses - 1);
-    constexpr uint64_t target = cap / TU::TARGET_DIV;
+    const uint64_t cap = min_cap;
+    const uint64_t target = cap / TU::TARGET_DIV;
     constexpr uint64_t tile = (uint64_t)TU::XT * TU::XI;
     WsLayout L;
     // chunks of 16 tiles, dispensed dynamically to persistent CTAs
     const uint64_t ch = tile * 16;
     L.chunk_elems = ch;
+    L.min_cap = min_cap;
     L.seg_cap = (uint32_t)(n / cap + 2);
     L.chunk_cap = (uint32_t)(L.seg_cap + n / ch + 2);
     const uint64_t last_target = target * TU::LAST_NUM / TU::LAST_DEN;  // choose_logk's last level
     L.split_cap = (uint32_t)(2 * n / last_target + 2 * (uint64_t)L.seg_cap + 2 * (1u << TU::LOGKMAX) + 64);
     L.task_cap = 4 * L.split_cap + 64;  // per class, all levels of one sort
     L.fill_cap = L.split_cap;
-    L.hist_cap = (uint32_t)(2ull * (1u << TU::LOGKMAX) * (n / ch + 2) + 2ull * L.split_cap);
+    // histogram words of one level: a segment of len keys takes (nch + 1) 2K
+    // words with nch <= len/ch + 1 and 2K <= min(2 K_max, 4 len/last_target + 4)
+    // (choose_logk), so a level needs at most
+    //   2 K_max n/ch + 8 n/last_target + 8 segments
+    L.hist_cap = (uint32_t)(2ull * (1u << TU::LOGKMAX) * (n / ch + 4) + 8ull * (n / last_target + 1) +
+                            8ull * L.seg_cap + 4096);
     size_t o = 0;
     auto take = [&](size_t bytes) {
         size_t at = o;
@@ -469,7 +489,14 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                       const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf, const K* src0 = nullptr) {
     const bool fused = xf.a != 0 || xf.b != 0;
     using TU = Tune<K>;
-    constexpr uint32_t cap = class_cap<K>(kNumClasses - 1);
+    constexpr uint32_t cap_max = class_cap<K>(kNumClasses - 1);
+    // beta (sort.hpp:25-34, base_case_levels sort.hpp:91-96): with
+    // base_case.use_levels the reference runs X on blocks of about n^beta; here
+    // n^beta is the largest bucket the block sorter takes (clamped to the
+    // block sorter's classes); otherwise every bucket that fits one CTA does
+    // (never below what the work lists were sized for: other entry points
+    // lay out their workspace for the default takeover size)
+    const uint32_t cap = std::min(cap_max, std::max(takeover_cap<K>(n, &cfg), L.min_cap));
     PlanParams p;
     p.chunk_elems = L.chunk_elems;
     p.cap = cap;
@@ -533,6 +560,24 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
 
     K* src = src0 ? const_cast<K*>(src0) : A;  // level 0 only reads it
     K* dst = B;
+    // median_of_sqrt_n (median_of_sqrt_pivot, partition.hpp:235-251): level 0
+    // draws s = 2 floor(sqrt(n)/2) + 1 strided keys; more than one block sort
+    // holds are sorted here first (block sort + merge passes in B, which
+    // level 0's scatter only overwrites after its sample kernel has read them)
+    const K* presorted = nullptr;
+    uint32_t presorted_n = 0;
+    {
+        const uint64_t s0 = sqrt_sample_size(n);
+        if (cfg.pivot == 1 && s0 > (uint64_t)BSS::kCap && 2 * s0 <= n) {
+            const uint64_t stride = n / s0;
+            QLAUNCH(led, kPhSample, 0,
+                    gather_strided_kernel<K><<<(unsigned)std::min<uint64_t>((s0 + 255) / 256, 1184), 256, 0, st>>>(
+                        src, n, s0, stride, B, xf));
+            QTRY(mergesort_range<K>(B, B, B + s0, 0, s0, st, led));
+            presorted = B;
+            presorted_n = (uint32_t)s0;
+        }
+    }
     const int max_levels = std::min(cfg.max_levels > 0 ? cfg.max_levels : 8, kCntSlots - 2);
     int level = 0;
     int batch = std::max(1, estimate_levels(n, p));
@@ -551,7 +596,8 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             const Xf lxf = level == 0 ? xf : Xf{0, 0};  // only level 0 reads the caller's keys
             QLAUNCH(led, kPhSample, 0,
                     (level == 0 && fused ? sample_xf_fn : sample_fn)<<<sample_grid, TU::ST, BSS::kSmemBytes, st>>>(
-                        lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u, lxf));
+                        lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u, lxf,
+                        level == 0 ? presorted : nullptr, level == 0 ? presorted_n : 0u));
             QLAUNCH(led, kPhCount, 0,
                     count_fn<<<count_grid, TU::CT, 0, st>>>(lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks,
                                                             &c->work_count, src, tree[cur], sorted[cur],
@@ -608,6 +654,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         if (c.nsegs == 0) continue;
         ++led.levels;
         led.resplits += c.resplits;
+        led.sample_keys += c.sample_keys;
         led.ph_bytes[kPhCount] += c.nkeys * w;
         led.ph_bytes[kPhScatter] += 2 * c.nkeys * w;
         led.alg_bytes += 3 * c.nkeys * w;
@@ -662,11 +709,11 @@ static size_t dtype_size(int dt) {
     return 0;
 }
 
-static size_t ws_bytes_for(int dt, size_t n) {
+static size_t ws_bytes_for(int dt, size_t n, const qmsort_gpu_config* cfg = nullptr) {
     switch (core_dtype(dt)) {
-        case QMSORT_DT_U32: return make_layout<uint32_t>(n).total;
-        case QMSORT_DT_U64: return make_layout<uint64_t>(n).total;
-        case QMSORT_DT_REC32: return make_layout<Rec32>(n).total;
+        case QMSORT_DT_U32: return make_layout<uint32_t>(n, takeover_cap<uint32_t>(n, cfg)).total;
+        case QMSORT_DT_U64: return make_layout<uint64_t>(n, takeover_cap<uint64_t>(n, cfg)).total;
+        case QMSORT_DT_REC32: return make_layout<Rec32>(n, takeover_cap<Rec32>(n, cfg)).total;
     }
     return 0;
 }
@@ -730,6 +777,7 @@ static void fill_metrics(qmsort_gpu_metrics* m, Ledger& led, float ms) {
     m->kernel_launches = led.launches;
     m->host_syncs = led.syncs + 1;
     m->resplits = led.resplits;
+    m->sample_keys = led.sample_keys;
     for (int i = 0; i < QMSORT_NUM_PHASES; ++i) {
         m->phase_bytes[i] = led.ph_bytes[i];
         m->phase_launches[i] = led.ph_launches[i];
@@ -749,7 +797,7 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     qmsort_gpu_config cfg;
     if (cfgp) cfg = *cfgp;
     else qmsort_gpu_config_init(&cfg, 0);
-    const size_t need = ws_bytes_for(dt, n);
+    const size_t need = ws_bytes_for(dt, n, &cfg);
     void* ws = wsp;
     bool own = false;
     if (ws == nullptr && n > 1) {
@@ -773,15 +821,18 @@ static int sort_device(int dt, int cmp, void* d, size_t n, const qmsort_gpu_conf
     unsigned char* w = static_cast<unsigned char*>(ws);
     switch (core_dtype(dt)) {
         case QMSORT_DT_U32:
-            rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w, make_layout<uint32_t>(n), st, led, xf,
+            rc = sort_core<uint32_t>(static_cast<uint32_t*>(d), n, cfg, w,
+                                     make_layout<uint32_t>(n, takeover_cap<uint32_t>(n, &cfg)), st, led, xf,
                                      static_cast<const uint32_t*>(src));
             break;
         case QMSORT_DT_U64:
-            rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w, make_layout<uint64_t>(n), st, led, xf,
+            rc = sort_core<uint64_t>(static_cast<uint64_t*>(d), n, cfg, w,
+                                     make_layout<uint64_t>(n, takeover_cap<uint64_t>(n, &cfg)), st, led, xf,
                                      static_cast<const uint64_t*>(src));
             break;
         case QMSORT_DT_REC32:
-            rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n), st, led, xf,
+            rc = sort_core<Rec32>(static_cast<Rec32*>(d), n, cfg, w, make_layout<Rec32>(n, takeover_cap<Rec32>(n, &cfg)),
+                                  st, led, xf,
                                   static_cast<const Rec32*>(src));
             break;
     }
@@ -1292,7 +1343,7 @@ static int sort_host_one(int dtype, int cmp, void* h_data, size_t n, const qmsor
         return QMSORT_OK;
     }
     const size_t data_bytes = align_up(n * dtype_size(dtype), 256);
-    const size_t need = data_bytes + ws_bytes_for(dtype, n);
+    const size_t need = data_bytes + ws_bytes_for(dtype, n, cfg);
     unsigned char* base = nullptr;
     cudaStream_t st = nullptr;
     QTRY(host_arena(need, &base, &st));
@@ -1353,9 +1404,9 @@ size_t qmsort_gpu_dtype_size(int dtype) { return dtype_size(dtype); }
 
 int qmsort_gpu_core_dtype(int dtype) { return core_dtype(dtype); }
 
-size_t qmsort_gpu_workspace_bytes(int dtype, size_t n, const qmsort_gpu_config*) {
+size_t qmsort_gpu_workspace_bytes(int dtype, size_t n, const qmsort_gpu_config* cfg) {
     if (dtype_size(dtype) == 0) return 0;
-    return ws_bytes_for(dtype, n);
+    return ws_bytes_for(dtype, n, cfg);
 }
 
 int qmsort_gpu_sort(int dtype, int cmp, void* d_data, size_t n, const qmsort_gpu_config* cfg,
@@ -1381,7 +1432,7 @@ int qmsort_gpu_sort_host_batch(int dtype, int cmp, void* const* h_arrays, const 
     for (size_t i = 0; i < count; ++i) {
         if (ns[i] <= 1) continue;
         todo.push_back(i);
-        need = std::max(need, align_up(ns[i] * dtype_size(dtype), 256) + ws_bytes_for(dtype, ns[i]));
+        need = std::max(need, align_up(ns[i] * dtype_size(dtype), 256) + ws_bytes_for(dtype, ns[i], cfg));
     }
     if (todo.empty()) return QMSORT_OK;
     std::lock_guard<std::mutex> batch_lock(g_batch_mu);
@@ -1600,6 +1651,33 @@ int qmsort_gpu_partition_scatter_peers(int core, const void* d_in, size_t n, uin
     }
     return partition_entry(core, d_in, n, nullptr, nsplit, nullptr, nullptr, d_ws, ws_bytes, stream,
                            2, &pa);
+}
+
+size_t qmsort_gpu_partition3_workspace_bytes(int dtype, size_t n) {
+    if (dtype_size(dtype) == 0) return 0;
+    return ws_bytes_for(dtype, std::max<size_t>(n, 2)) + 256;
+}
+
+int qmsort_gpu_partition3(int dtype, int cmp, void* d_data, size_t n, const void* h_pivot, uint64_t* h_counts3,
+                          const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes, qmsort_gpu_metrics* metrics,
+                          void* stream) {
+    return partition3_device(dtype, cmp, d_data, n, h_pivot, h_counts3, cfg, d_ws, ws_bytes, metrics,
+                             static_cast<cudaStream_t>(stream));
+}
+
+int qmsort_gpu_partition3_host(int dtype, int cmp, void* h_data, size_t n, const void* h_pivot,
+                               uint64_t* h_counts3, const qmsort_gpu_config* cfg, qmsort_gpu_metrics* metrics) {
+    QTRY(validate(dtype, cmp, n, h_data));
+    const size_t data_bytes = align_up(std::max<size_t>(n, 1) * dtype_size(dtype), 256);
+    const size_t ws = qmsort_gpu_partition3_workspace_bytes(dtype, n);
+    unsigned char* base = nullptr;
+    cudaStream_t st = nullptr;
+    QTRY(host_arena(data_bytes + ws, &base, &st));
+    if (n) QCK(cudaMemcpyAsync(base, h_data, n * dtype_size(dtype), cudaMemcpyHostToDevice, st));
+    QTRY(partition3_device(dtype, cmp, base, n, h_pivot, h_counts3, cfg, base + data_bytes, ws, metrics, st));
+    if (n) QCK(cudaMemcpyAsync(h_data, base, n * dtype_size(dtype), cudaMemcpyDeviceToHost, st));
+    QCK(cudaStreamSynchronize(st));
+    return QMSORT_OK;
 }
 
 // ---- the distributed samplesort (shard.cuh) ----

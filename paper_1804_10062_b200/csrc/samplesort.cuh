@@ -33,6 +33,7 @@
 // only keys of cells that straddle a splitter finish with a binary search over
 // sorted[j_lo..j_hi).  Records (rec32) walk an Eytzinger search tree.
 #pragma once
+#include <cstddef>
 #include <type_traits>
 
 #include "blocksort.cuh"
@@ -68,7 +69,23 @@ struct SegDesc {
 // sample analogue of triple_median_pivot (selection.hpp:219-229), used at
 // every level by mom_of_thirds and, under hybrid, for a bucket that came out
 // outside the delta band (pivot_outside_band, sort.hpp:114-118).
-enum : uint32_t { kSampleRandom = 0, kSampleTriples = 1 };
+// kSampleSqrt: median_of_sqrt_n (median_of_sqrt_pivot, partition.hpp:235-251)
+// -- s = 2 floor(sqrt(len) / 2) + 1 keys at the strided positions i * floor(len / s),
+// at least 1024 so that the K-1 quantiles stay usable, at most one block sort
+// (a larger level-0 sample is sorted beforehand by the host path, see
+// samplesort()).
+enum : uint32_t { kSampleRandom = 0, kSampleTriples = 1, kSampleSqrt = 2 };
+
+__host__ __device__ inline uint64_t isqrt_u64(uint64_t x) {
+    uint64_t r = 0;
+    for (int b = 31; b >= 0; --b) {
+        const uint64_t t = r | (1ull << b);
+        if (t * t <= x) r = t;
+    }
+    return r;
+}
+// The reference's Median-of-sqrt(n) sample size (partition.hpp:240-241).
+__host__ __device__ inline uint64_t sqrt_sample_size(uint64_t len) { return 2 * (isqrt_u64(len) / 2) + 1; }
 
 struct ChunkDesc {
     uint32_t seg;
@@ -104,7 +121,29 @@ struct LevelCounters {
     unsigned long long nkeys;      // keys in this level's segments (pass ledger)
     unsigned long long task_keys;  // keys handed to the block sorter
     unsigned long long fill_keys;  // keys written by equal-bucket fills
+    unsigned long long sample_keys;  // keys the level's sample kernel drew (all segments)
 };
+
+// A level whose work lists overflowed (emit_segment / plan_kernel set
+// `overflow` after bumping the counts) has counts that cover unwritten
+// descriptors: every consumer kernel of that level exits at once and the
+// host reports QMSORT_EINTERNAL at its control read.  `field` points at a
+// member of the level's LevelCounters (null: a single caller-built segment).
+#define QMSORT_LEVEL_OVERFLOWED(field, member)                                                       \
+    ((field) != nullptr &&                                                                           \
+     reinterpret_cast<const volatile LevelCounters*>(reinterpret_cast<const char*>(field) -          \
+                                                     offsetof(LevelCounters, member))->overflow != 0)
+
+static_assert(offsetof(LevelCounters, nsegs) == 0, "sample_kernel finds its LevelCounters from &nsegs");
+
+// Median-of-sqrt(n) at level 0 when s exceeds one block sort: out[i] =
+// f(src[i * stride]), sorted afterwards by the host path.
+template <class K>
+__global__ void gather_strided_kernel(const K* __restrict__ src, uint64_t len, uint64_t s, uint64_t stride,
+                                      K* __restrict__ out, Xf xf) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < s; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = xf_fwd(src[min(i * stride, len - 1)], xf);
+}
 
 struct LevelBufs {  // one partition level's work description (device pointers)
     SegDesc* segs;
@@ -214,7 +253,8 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
 // threads of the grid.
 __global__ void init_level_kernel(LevelBufs nb, uint64_t n, uint64_t key_max, PlanParams p) {
     if (threadIdx.x == 0 && blockIdx.x == 0)
-        emit_segment(nb, 0, n, 0, key_max, p, p.pivot == 2 ? kSampleTriples : kSampleRandom, false);
+        emit_segment(nb, 0, n, 0, key_max, p,
+                     p.pivot == 2 ? kSampleTriples : p.pivot == 1 ? kSampleSqrt : kSampleRandom, false);
     const uint32_t nch = (uint32_t)((n + p.chunk_elems - 1) / p.chunk_elems);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nch && i < nb.chunk_cap;
          i += gridDim.x * blockDim.x) {
@@ -373,7 +413,9 @@ template <class K, int T, int ITEMS, bool XF>
 __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, const K* __restrict__ src,
                                                K* tree_store, K* sorted_store,
                                                uint32_t* lut_store, uint64_t seed,
-                                               uint32_t oversample, const Xf& xf) {
+                                               uint32_t oversample, const Xf& xf,
+                                               const K* __restrict__ presorted, uint32_t presorted_n,
+                                               unsigned long long* sample_keys) {
     using BS = BlockSorter<K, T, ITEMS>;
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
@@ -384,17 +426,32 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
 
     const SegDesc d = segs[seg];
     const uint32_t K_ = 1u << d.logk;
-    const int S = (int)min((uint32_t)BS::kCap, max(1024u, oversample * K_));
+    // presorted (level 0 of median_of_sqrt_n with s > one block sort): the
+    // host sorted the segment's s strided keys beforehand
+    const bool pre = presorted != nullptr && seg == 0;
+    int S = (int)min((uint32_t)BS::kCap, max(1024u, oversample * K_));
+    uint64_t stride = 1;
+    if (pre) {
+        S = (int)presorted_n;
+    } else if (d.sampler == kSampleSqrt) {
+        S = (int)min((uint64_t)BS::kCap, max((uint64_t)1024, sqrt_sample_size(d.len)));
+        stride = max((uint64_t)1, d.len / (uint64_t)S);
+    }
+    if (threadIdx.x == 0) atomicAdd(sample_keys, (unsigned long long)S);
 
     // kSampleRandom: seeded sample with replacement (counter-based SplitMix64
     // of the sample index; uniform position via a 64x64 high multiply).
     // kSampleTriples: median of the three keys at stride position idx.
+    // kSampleSqrt: the key at position idx * floor(len / s).
     K k[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int idx = (int)threadIdx.x * ITEMS + i;
-        if (idx >= S) {
+        if (pre || idx >= S) {
             k[i] = KT::max_key();
+        } else if (d.sampler == kSampleSqrt) {
+            k[i] = src[d.off + min((uint64_t)idx * stride, d.len - 1)];
+            if (XF) k[i] = xf_fwd(k[i], xf);
         } else if (d.sampler == kSampleTriples) {
             const uint64_t p0 = ((uint64_t)idx * d.len) / (uint64_t)S;
             const K* t = src + d.off + min(p0, d.len - 3);
@@ -414,11 +471,12 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
             if (XF) k[i] = xf_fwd(k[i], xf);
         }
     }
-    BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
+    if (!pre) BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
+    auto at = [&](int q) -> K { return pre ? presorted[q] : s[P::idx(q)]; };
     uint64_t pbase = 0;
     uint32_t psh = 0;
     if constexpr (std::is_same<K, Rec32>::value) {  // prefix window of the sampled w0 range
-        const uint64_t w0a = s[P::idx(0)].w[0], w0b = s[P::idx(S - 1)].w[0];
+        const uint64_t w0a = at(0).w[0], w0b = at(S - 1).w[0];
         pbase = w0a;
         psh = w0b > w0a ? (uint32_t)__clzll((long long)(w0b - w0a)) : 64u;
     }
@@ -426,8 +484,8 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
     // candidate splitter j (0 <= j < K-1): sample quantile (j+1)/K
     for (uint32_t j = threadIdx.x; j < K_ - 1; j += T) {
         const int q = (int)(((uint64_t)(j + 1) * S) / K_);
-        const K c = s[P::idx(q)];
-        const bool keep = (j == 0) || !KT::eq(c, s[P::idx((int)(((uint64_t)j * S) / K_))]);
+        const K c = at(q);
+        const bool keep = (j == 0) || !KT::eq(c, at((int)(((uint64_t)j * S) / K_)));
         flags[j] = keep ? 1u : 0u;
     }
     if (threadIdx.x == 0) flags[K_ - 1] = 0;
@@ -437,7 +495,7 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
     K* sorted = sorted_store + d.sp;
     for (uint32_t j = threadIdx.x; j < K_ - 1; j += T) {
         const int q = (int)(((uint64_t)(j + 1) * S) / K_);
-        if (flags[j + 1] != flags[j]) sorted[flags[j]] = s[P::idx(q)];
+        if (flags[j + 1] != flags[j]) sorted[flags[j]] = at(q);
     }
     __syncthreads();  // sorted[] (global) is visible block-wide after the barrier
     for (uint32_t j = threadIdx.x; j < m; j += T) s[P::idx(j)] = sorted[j];  // compacted copy
@@ -500,11 +558,14 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const uint32_t
                                                    const K* __restrict__ src, K* tree_store,
                                                    K* sorted_store, uint32_t* lut_store,
                                                    uint64_t seed, uint32_t oversample,
-                                                   Xf xf = Xf{0, 0}) {
+                                                   Xf xf = Xf{0, 0}, const K* presorted = nullptr,
+                                                   uint32_t presorted_n = 0) {
+    if (QMSORT_LEVEL_OVERFLOWED(nsegs, nsegs)) return;
     const uint32_t ns = *nsegs;
+    LevelCounters* lc = reinterpret_cast<LevelCounters*>(const_cast<uint32_t*>(nsegs));  // nsegs is its first member
     for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
         sample_segment<K, T, ITEMS, XF>(seg, segs, src, tree_store, sorted_store, lut_store, seed,
-                                        oversample, xf);
+                                        oversample, xf, presorted, presorted_n, &lc->sample_keys);
         __syncthreads();  // shared memory is reused by the next segment
     }
 }
@@ -570,6 +631,7 @@ __global__ void __launch_bounds__(T, 4) count_kernel(const SegDesc* __restrict__
     __shared__ ClassifierSmem<K, LOG_KMAX> cls;
     __shared__ uint32_t shist[2 * KMAX];
     __shared__ uint32_t next_chunk;
+    if (QMSORT_LEVEL_OVERFLOWED(nchunks_dev, nchunks)) return;
     const uint32_t nck = nchunks_dev ? *nchunks_dev : nchunks;  // device count: no host round trip
     uint32_t cur_seg = 0xFFFFFFFFu;
     for (;;) {
@@ -598,6 +660,7 @@ __global__ void __launch_bounds__(T, 4) count_kernel(const SegDesc* __restrict__
 __global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__ segs,
                                                      uint32_t* __restrict__ hist,
                                                      const LevelCounters* __restrict__ cnt) {
+    if (cnt && cnt->overflow) return;
     const uint32_t ns = cnt ? cnt->nsegs : 1u;
     const uint32_t NBMAX = cnt ? (2u << cnt->max_logk) : 1024u;  // bins incl. equality bins
     if (cnt && cnt->max_nchunks <= 16) {
@@ -678,6 +741,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
     __shared__ uint32_t warp_sums[32];
     __shared__ uint32_t cls_count[kNumClasses], cls_base[kNumClasses];
     __shared__ unsigned long long cls_keys;
+    if (*(volatile const uint32_t*)&cur_cnt->overflow) return;  // uniform: set before this kernel
     const uint32_t ns = cur_cnt->nsegs;  // device count: no host round trip
     for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
     __syncthreads();  // the previous segment's shared arrays are no longer read
@@ -759,7 +823,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
             // worst-case policy (f1): mom_of_thirds always samples triple
             // medians; hybrid does so for a child outside the delta band,
             // i.e. larger than (parent / buckets) / delta
-            uint32_t sampler = p.pivot == 2 ? kSampleTriples : kSampleRandom;
+            uint32_t sampler = p.pivot == 2 ? kSampleTriples : p.pivot == 1 ? kSampleSqrt : kSampleRandom;
             if (p.pivot == 3 &&
                 (uint64_t)len * (uint64_t)(1u << d.logk) * p.delta_q16 > d.len * 65536ull) {
                 sampler = kSampleTriples;
@@ -1002,6 +1066,7 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
             peer_base[b] = v;
         }
     }
+    if (QMSORT_LEVEL_OVERFLOWED(nchunks_dev, nchunks)) return;
     const uint32_t nck = nchunks_dev ? *nchunks_dev : nchunks;  // device count: no host round trip
     uint32_t cur_seg = 0xFFFFFFFFu;
     // persistent CTAs fetch chunks dynamically (no tail of idle SMs)

@@ -450,3 +450,82 @@ static int sort_sharded_sp(int dt, int cmp, uint32_t P, const int* devices, cons
     g_err.clear();
     return QMSORT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// PartitionResult (partition_result.hpp:12-17): a three-way partition of the
+// caller's range around one pivot value -- [0, lt_end) < pivot, [lt_end,
+// gt_begin) == pivot, [gt_begin, n) > pivot under cmp -- the one-splitter case
+// of the given-splitter partition (three-way bins), like three_way_partition
+// (partition.hpp:196-230) with the pivot passed by value.
+// ---------------------------------------------------------------------------
+static void xf_fwd_host(int dt, int cmp, const void* in, void* out) {
+    const Xf f = make_xf(dt, cmp);
+    const size_t w = dtype_size(dt);
+    if (w == 4) {
+        uint32_t x;
+        std::memcpy(&x, in, 4);
+        x ^= (uint32_t)f.b;
+        std::memcpy(out, &x, 4);
+    } else {
+        for (size_t i = 0; i < w / 8; ++i) {
+            uint64_t x;
+            std::memcpy(&x, static_cast<const char*>(in) + 8 * i, 8);
+            x = x ^ f.b ^ ((uint64_t)((int64_t)x >> 63) & f.a);
+            std::memcpy(static_cast<char*>(out) + 8 * i, &x, 8);
+        }
+    }
+}
+
+static int partition3_device(int dt, int cmp, void* d, size_t n, const void* h_pivot, uint64_t* h_counts3,
+                             const qmsort_gpu_config* cfgp, void* wsp, size_t ws_bytes, qmsort_gpu_metrics* m,
+                             cudaStream_t st) {
+    QTRY(validate(dt, cmp, n, d));
+    if (!h_pivot || !h_counts3) return fail(QMSORT_EINVAL, "null pivot or counts");
+    qmsort_gpu_config tmp;
+    const qmsort_gpu_config& cfg = cfg_or_default(cfgp, tmp);
+    const size_t w = dtype_size(dt);
+    const size_t nn = std::max<size_t>(n, 2);
+    const size_t need = ws_bytes_for(dt, nn) + 256;
+    CallFrame f(st);
+    QTRY(f.begin(cfg, wsp, ws_bytes, need));
+    unsigned char* ws = static_cast<unsigned char*>(f.ws);
+    unsigned char* extra = ws + ws_bytes_for(dt, nn);  // pivot (core key) | 3 counts
+    unsigned char pv[32];
+    xf_fwd_host(dt, cmp, h_pivot, pv);
+    uint64_t* dcnt = reinterpret_cast<uint64_t*>(extra + 64);
+    int rc = QMSORT_OK;
+    auto run = [&]() -> int {
+        QCK(cudaMemcpyAsync(extra, pv, w, cudaMemcpyHostToDevice, st));
+        if (n == 0) {
+            QCK(cudaMemsetAsync(dcnt, 0, 3 * sizeof(uint64_t), st));
+            return QMSORT_OK;
+        }
+        const Xf xf = make_xf(dt, cmp);
+        switch (core_dtype(dt)) {
+#define QPART3(K)                                                                                             \
+    {                                                                                                         \
+        const WsLayout L = make_layout<K>(nn);                                                                \
+        K* B = reinterpret_cast<K*>(ws + L.b_off);                                                            \
+        QTRY(partition_given<K>(static_cast<const K*>(d), n, reinterpret_cast<const K*>(extra), 1, B, dcnt,   \
+                                ws, L, st, f.led, 3, nullptr, true, xf));                                     \
+        QCK(cudaMemcpyAsync(d, B, n * sizeof(K), cudaMemcpyDeviceToDevice, st));                              \
+        if (xf.a | xf.b) QTRY(xf_range<K>(static_cast<K*>(d), n, xf, true, st, f.led));                       \
+        break;                                                                                                \
+    }
+            case QMSORT_DT_U32: QPART3(uint32_t)
+            case QMSORT_DT_U64: QPART3(uint64_t)
+            case QMSORT_DT_REC32: QPART3(Rec32)
+#undef QPART3
+        }
+        return QMSORT_OK;
+    };
+    rc = run();
+    if (rc == QMSORT_OK) {
+        uint64_t h[3] = {0, 0, 0};
+        const cudaError_t e = cudaMemcpyAsync(h, dcnt, sizeof(h), cudaMemcpyDeviceToHost, st);
+        rc = f.end(e == cudaSuccess ? QMSORT_OK : fail(QMSORT_ECUDA, cudaGetErrorString(e)), m);
+        if (rc == QMSORT_OK) std::memcpy(h_counts3, h, sizeof(h));
+        return rc;
+    }
+    return f.end(rc, m);
+}

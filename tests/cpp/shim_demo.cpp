@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <deque>
 #include <functional>
 #include <numeric>
 #include <vector>
@@ -26,9 +27,17 @@ static int fails = 0;
 struct Rec {
     std::uint64_t w[4];
 };
+// a record comparator functor, declared as the lexicographic word order
+struct RecLess {
+    bool operator()(const Rec& a, const Rec& b) const {
+        return std::lexicographical_compare(a.w, a.w + 4, b.w, b.w + 4);
+    }
+};
 namespace qmsort::gpu {
 template <>
 struct is_rec32<Rec> : std::true_type {};
+template <>
+struct rec32_order<RecLess, Rec> : std::integral_constant<int, QMSORT_LESS> {};
 }  // namespace qmsort::gpu
 
 int main() {
@@ -65,6 +74,49 @@ int main() {
     CHECK(std::is_sorted(r.begin(), r.end(), [](const Rec& a, const Rec& b) {
         return std::lexicographical_compare(a.w, a.w + 4, b.w, b.w + 4);
     }));
+    {
+        auto r2 = r;
+        std::reverse(r2.begin(), r2.end());
+        qmsort::gpu::sort(r2.begin(), r2.end(), qmsort::gpu::qms(), RecLess{});
+        CHECK(std::equal(r.begin(), r.end(), r2.begin(), [](const Rec& a, const Rec& b) {
+            return std::equal(a.w, a.w + 4, b.w);
+        }));
+    }
+    // a non-contiguous random-access range (std::deque) is gathered, sorted, written back
+    {
+        std::deque<std::int64_t> dq;
+        for (int i = 0; i < 100000; ++i) dq.push_back((std::int64_t)((i * 7919LL) % 100003) - 50000);
+        qmsort::gpu::sort(dq.begin(), dq.end());
+        CHECK(std::is_sorted(dq.begin(), dq.end()) && dq.size() == 100000);
+    }
+    // sort_range_counted (sort.hpp:207-211): counters accumulate into a caller Metrics
+    {
+        qmsort::gpu::Metrics acc;
+        std::less<> cmp;
+        std::vector<std::uint32_t> a(u.begin(), u.begin() + 300000);
+        qmsort::gpu::sort_range_counted(a.begin(), a.end(), qmsort::gpu::qms(), cmp, acc);
+        CHECK(std::is_sorted(a.begin(), a.end()));
+        const auto t1 = acc.elapsed_ns;
+        std::reverse(a.begin(), a.end());
+        qmsort::gpu::sort_range_counted(a.begin(), a.end(), qmsort::gpu::qms(), cmp, acc);
+        CHECK(std::is_sorted(a.begin(), a.end()) && t1 > 0 && acc.elapsed_ns > t1 && acc.comparisons == 0);
+    }
+    // PartitionResult (partition_result.hpp:12-17): three-way partition around a pivot value
+    {
+        std::vector<std::int32_t> v{7, 11, 4, 5, 6, 10, 9, 2, 3, 1, 0, 8, 7, 7};
+        const auto pr = qmsort::gpu::partition(v.begin(), v.end(), 7);
+        CHECK(pr.lt_end == 7 && pr.gt_begin == 10 && pr.left_size == 7 && pr.right_size == 4);
+        CHECK(std::all_of(v.begin(), v.begin() + 7, [](int x) { return x < 7; }));
+        CHECK(std::all_of(v.begin() + 7, v.begin() + 10, [](int x) { return x == 7; }));
+        CHECK(std::all_of(v.begin() + 10, v.end(), [](int x) { return x > 7; }));
+        std::vector<double> dv(200000);
+        for (std::size_t i = 0; i < dv.size(); ++i) dv[i] = (double)((i * 7919) % 1001) - 500.0;
+        const auto pd = qmsort::gpu::partition(dv.begin(), dv.end(), 0.0, std::greater<>{});
+        CHECK(std::all_of(dv.begin(), dv.begin() + pd.lt_end, [](double x) { return x > 0.0; }));
+        CHECK(std::all_of(dv.begin() + pd.lt_end, dv.begin() + pd.gt_begin, [](double x) { return x == 0.0; }));
+        CHECK(std::all_of(dv.begin() + pd.gt_begin, dv.end(), [](double x) { return x < 0.0; }));
+        CHECK(pd.gt_begin - pd.lt_end == (std::size_t)std::count(dv.begin(), dv.end(), 0.0));
+    }
     // int64 keys (the reference profile's Vec, test_sort.cpp:22)
     std::vector<std::int64_t> q64(200000);
     for (auto& x : q64) {

@@ -122,8 +122,7 @@ def _peer_worker(rank, world, port, n, seed, q):
         # rank grows its receive buffer and the handles are swapped again
         for rep, m in enumerate((n, n, 3 * n)):
             shard = torch.from_numpy(full[rank * m:(rank + 1) * m].copy()).cuda()
-            out = sharded.sort_sharded(shard, "less", dtype=DT_U64, exchange=ex, ops=ops,
-                                       force_exchange=True)
+            out = sharded.sort_sharded(shard, "less", dtype=DT_U64, exchange=ex, ops=ops)
             res.append(out.cpu().numpy().copy())
             ex.barrier()
         parts = [None] * world
@@ -150,7 +149,7 @@ def test_ipc_peer_exchange_processes(world):
     procs = [ctx.Process(target=_peer_worker, args=(r, world, port, 300000, 9, qq)) for r in range(world)]
     for p in procs:
         p.start()
-    full, parts = qq.get(timeout=600)
+    full, parts = qq.get(timeout=240)
     for p in procs:
         p.join(timeout=600)
         assert p.exitcode == 0
