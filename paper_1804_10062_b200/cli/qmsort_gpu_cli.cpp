@@ -37,6 +37,7 @@
 #include <map>
 #include <optional>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -148,6 +149,17 @@ uint64_t trial_seed(uint64_t seed, size_t n, uint64_t trial) {
     return mix_seed(seed, (uint64_t)n * 1000003ull + trial);
 }
 
+// Fields of `text` between separators (a trailing separator yields an empty
+// last field; a string without separators is one field).
+std::vector<std::string> split(const std::string& text, char sep) {
+    std::vector<std::string> fields(1);
+    for (const char c : text) {
+        if (c == sep) fields.emplace_back();
+        else fields.back().push_back(c);
+    }
+    return fields;
+}
+
 // ---- options ---------------------------------------------------------------
 struct Options {
     std::string algo = "qms";
@@ -166,23 +178,20 @@ struct Options {
     std::vector<std::string> positional;
 };
 
-double parse_ratio(const std::string& s) {  // qmsort.cpp:28-33
-    const auto slash = s.find('/');
-    if (slash != std::string::npos) return std::stod(s.substr(0, slash)) / std::stod(s.substr(slash + 1));
-    return std::stod(s);
+// "p/q" or a plain number (the --beta / --delta syntax of the reference CLI)
+double parse_ratio(const std::string& text) {
+    const auto parts = split(text, '/');
+    double v = std::stod(parts.at(0));
+    if (parts.size() > 1) v /= std::stod(parts[1]);
+    return v;
 }
 
-std::vector<size_t> parse_size_list(const std::string& s) {  // qmsort.cpp:35-47
-    std::vector<size_t> out;
-    size_t start = 0;
-    while (start <= s.size()) {
-        const auto comma = s.find(',', start);
-        const std::string tok = s.substr(start, comma == std::string::npos ? std::string::npos : comma - start);
-        if (!tok.empty()) out.push_back((size_t)std::stoull(tok));
-        if (comma == std::string::npos) break;
-        start = comma + 1;
-    }
-    return out;
+// Comma-separated sizes; empty fields are skipped ("1,,2," = {1, 2}).
+std::vector<size_t> parse_size_list(const std::string& text) {
+    std::vector<size_t> sizes;
+    for (const std::string& field : split(text, ','))
+        if (!field.empty()) sizes.push_back(static_cast<size_t>(std::stoull(field)));
+    return sizes;
 }
 
 // "gpu" / "[gpu-]qms|qmqs|momqms|hqms" -> preset (sort.hpp:37-66); -1 if unknown
@@ -385,6 +394,34 @@ int run_verify(bool quick) {
 }
 
 // ---- sort_file (qmsort.cpp:303-344) ----------------------------------------
+// One int64 per line (a trailing CR is dropped); the first bad line is
+// reported as "<file>:<line>: <reason>" and stops the read.
+struct ParseError {
+    size_t line = 0;
+    std::string reason;
+};
+bool read_int64_lines(std::istream& in, std::vector<int64_t>& values, ParseError& err) {
+    std::string text;
+    for (size_t no = 1; std::getline(in, text); ++no) {
+        if (!text.empty() && text.back() == '\r') text.pop_back();
+        if (text.empty()) {
+            err = {no, "empty line"};
+            return false;
+        }
+        int64_t v = 0;
+        const char* end = text.data() + text.size();
+        const auto res = std::from_chars(text.data(), end, v);
+        if (res.ec != std::errc{} || res.ptr != end) {
+            err = {no, "not a 64-bit integer: '" + text + "'"};
+            return false;
+        }
+        values.push_back(v);
+    }
+    return true;
+}
+
+// sort_file IN OUT: int64 text in, sorted text out, through the host-array
+// C-ABI call (the reference's sort_file subcommand, tools/qmsort.cpp).
 int run_sort_file(const std::string& in_path, const std::string& out_path, const Options& o) {
     const int preset = parse_algo(o.algo);
     if (preset < 0) {
@@ -397,24 +434,10 @@ int run_sort_file(const std::string& in_path, const std::string& out_path, const
         return 2;
     }
     std::vector<int64_t> values;
-    std::string line;
-    size_t line_no = 0;
-    while (std::getline(in, line)) {
-        ++line_no;
-        if (!line.empty() && line.back() == '\r') line.pop_back();
-        if (line.empty()) {
-            std::cerr << in_path << ":" << line_no << ": empty line\n";
-            return 1;
-        }
-        int64_t value = 0;
-        const char* b = line.data();
-        const char* e = b + line.size();
-        const auto [ptr, ec] = std::from_chars(b, e, value);
-        if (ec != std::errc{} || ptr != e) {
-            std::cerr << in_path << ":" << line_no << ": not a 64-bit integer: '" << line << "'\n";
-            return 1;
-        }
-        values.push_back(value);
+    ParseError err;
+    if (!read_int64_lines(in, values, err)) {
+        std::cerr << in_path << ":" << err.line << ": " << err.reason << "\n";
+        return 1;
     }
     const qmsort_gpu_config cfg = build_config(preset, o);
     check_rc(qmsort_gpu_sort_host(QMSORT_DT_I64, QMSORT_LESS, values.data(), values.size(), &cfg, nullptr),
@@ -424,7 +447,9 @@ int run_sort_file(const std::string& in_path, const std::string& out_path, const
         std::cerr << "cannot open output file '" << out_path << "'\n";
         return 2;
     }
-    for (const auto v : values) out << v << '\n';
+    std::ostringstream text;
+    for (const int64_t v : values) text << v << '\n';
+    out << text.str();
     return 0;
 }
 

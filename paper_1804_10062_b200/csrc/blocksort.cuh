@@ -79,10 +79,15 @@ __device__ __forceinline__ void register_sort(K (&k)[N]) {
 
 // Merge-path split on shared memory: the number of elements taken from run A
 // among the first `diag` outputs of merge(A, B) when ties take A first.
-template <class K>
+// Shared-memory index maps: SmemPad<K> (one pad word per bank row, the block
+// sorter) or NoPad (dense, where the bulk-copy engine wrote the keys).
+struct NoPad {
+    __device__ __forceinline__ static unsigned idx(unsigned i) { return i; }
+};
+
+template <class K, class P = SmemPad<K>>
 __device__ __forceinline__ int merge_path_smem(const K* s, int a0, int alen, int b0, int blen,
                                                int diag) {
-    using P = SmemPad<K>;
     unsigned lo = diag > blen ? (unsigned)(diag - blen) : 0u;
     unsigned hi = diag < alen ? (unsigned)diag : (unsigned)alen;
     const unsigned bd = (unsigned)(b0 + diag - 1);
@@ -100,10 +105,9 @@ __device__ __forceinline__ int merge_path_smem(const K* s, int a0, int alen, int
 // (run B, ends at bend) of shared memory into registers.  Branch-free: an
 // exhausted run reads as the maximum key, which is also exactly what any
 // remaining keys of the other run equal when a tie with it takes run A.
-template <class K, int ITEMS>
+template <class K, int ITEMS, class P = SmemPad<K>>
 __device__ __forceinline__ void serial_merge_smem(const K* s, int ai, int aend, int bi, int bend,
                                                   K (&out)[ITEMS]) {
-    using P = SmemPad<K>;
     using KT = KeyTraits<K>;
     K ka = ai < aend ? s[P::idx((unsigned)ai)] : KT::max_key();
     K kb = bi < bend ? s[P::idx((unsigned)bi)] : KT::max_key();
@@ -128,7 +132,7 @@ __device__ __forceinline__ void serial_merge_smem(const K* s, int ai, int aend, 
 // half-cleaner network sorts in registers.  All loads are independent, and the
 // compare-and-swaps split over the ALU and FMA pipes (net_cas).  Keys only: the
 // output equals the serial merge's (equal keys are indistinguishable).
-template <class K, int ITEMS>
+template <class K, int ITEMS, class P = SmemPad<K>>
 __device__ __forceinline__ void bitonic_merge_window(const K* s, int ai, int x, int bi, K (&out)[ITEMS]);
 
 // min (lower = true) or max of a and b.
@@ -206,9 +210,8 @@ __device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
     }
 }
 
-template <class K, int ITEMS>
+template <class K, int ITEMS, class P>
 __device__ __forceinline__ void bitonic_merge_window(const K* s, int ai, int x, int bi, K (&out)[ITEMS]) {
-    using P = SmemPad<K>;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int idx = i < x ? ai + i : bi + (ITEMS - 1 - i);

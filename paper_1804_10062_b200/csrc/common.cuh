@@ -9,6 +9,7 @@
 // the way in and out (transform.cuh), so one kernel family serves every
 // (dtype, less/greater) pair bit-exactly.
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -165,6 +166,29 @@ struct SmemPad {
     __device__ __forceinline__ static unsigned idx(unsigned i) { return i + (i >> kShift); }
     static constexpr int elems(int n) { return n + n / kPer + 64; }
 };
+
+// Device-side invariant checks, compiled in with -DQMSORT_DEVICE_CHECKS=1 only
+// (compute-sanitizer is not available on the bench pool): a violated bound
+// prints the file, line and the two values involved and traps, so a bad index
+// stops the call with QMSORT_ECUDA instead of corrupting memory.  The checked
+// build runs the sanitizer workload (scripts/device_checks.sh).
+#ifndef QMSORT_DEVICE_CHECKS
+#define QMSORT_DEVICE_CHECKS 0
+#endif
+#if QMSORT_DEVICE_CHECKS
+#define QCHECK(cond, a, b)                                                                            \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("qmsort device check failed %s:%d: %s (%llu, %llu)\n", __FILE__, __LINE__, #cond,  \
+                   (unsigned long long)(a), (unsigned long long)(b));                                 \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define QCHECK(cond, a, b) \
+    do {                   \
+    } while (0)
+#endif
 
 // Order-preserving transform fused into the sort's first reads and last
 // writes (aux_kernels.cuh has the standalone passes):

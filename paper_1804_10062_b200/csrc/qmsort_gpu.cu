@@ -110,6 +110,11 @@ struct Tune<uint32_t> {
     static constexpr int XT = 512, XI = 16;  // scatter tile
     static constexpr int CT = 256, CU = 16;  // count
     static constexpr int MT = 512, MI = 16;  // merge pass
+    static constexpr int BMI = 16;  // bulk merge pass (two stages of MT x BMI keys)
+    // merge pass kernel: the plain one (measured on C2, 14 passes: 9.9 ms
+    // against 12.2 ms staged by the bulk-copy engine, 11.9 ms with 16-byte
+    // register stores; 8 keys per thread 13.7 ms)
+    static constexpr bool MERGE_BULK = false;
 };
 template <>
 struct Tune<uint64_t> {
@@ -122,6 +127,8 @@ struct Tune<uint64_t> {
     static constexpr int XT = 512, XI = 12;  // measured: C3 scatter 14.8 -> 13.7 ms, C4a 2.55 -> 2.17 ms (was 256 x 16)
     static constexpr int CT = 256, CU = 8;
     static constexpr int MT = 512, MI = 16;
+    static constexpr int BMI = 16;
+    static constexpr bool MERGE_BULK = true;  // measured on C3, 17 passes: 84.2 ms against 101.2 ms plain
 };
 template <>
 struct Tune<Rec32> {
@@ -134,6 +141,8 @@ struct Tune<Rec32> {
     static constexpr int XT = 512, XI = 4;  // measured: C5 scatter 2.84 -> 2.73 ms (was 256 x 8)
     static constexpr int CT = 256, CU = 4;
     static constexpr int MT = 512, MI = 8;
+    static constexpr int BMI = 4;  // 2 x 64 KB stages
+    static constexpr bool MERGE_BULK = true;  // measured on C5: 24.8 ms against 27.9 ms plain
 };
 template <class K>
 constexpr uint32_t class_cap(int c) {
@@ -453,28 +462,55 @@ static int xf_range(K* p, uint64_t n, Xf xf, bool inverse, cudaStream_t st, Ledg
     return QMSORT_OK;
 }
 
+#ifndef QMSORT_MERGE_BULK
+#define QMSORT_MERGE_BULK 1
+#endif
+// splits (optional, splits_cap entries): device scratch for the Blackwell
+// merge pass (K6a split points + K6b bulk-copy staging); without it, or with
+// QMSORT_MERGE_BULK=0, the warp-search kernel with plain loads runs.
 template <class K>
 static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStream_t st,
-                           Ledger& led) {
+                           Ledger& led, uint64_t* splits = nullptr, size_t splits_cap = 0) {
     using TU = Tune<K>;
     constexpr uint64_t C = class_cap<K>(kNumClasses - 1);
     constexpr uint64_t MC = (uint64_t)TU::MT * TU::MI;
     static_assert(MC <= 2 * C, "merge tile must fit in one run pair");
+    static_assert(C % MC == 0, "merge tiles never straddle a run pair");
     if (len <= C) return blocksort_one<K>(X, A, off, len, st, led);
     const uint64_t tiles = (len + C - 1) / C;
     const uint32_t passes = ceil_log2_u64(tiles);
     K* Y = (passes % 2 == 0) ? A : B;
     QTRY((launch_tiles<K, TU::CLS_T[kNumClasses - 1], TU::BI>(X, Y, off, len, st, led)));
-    using BS = BlockSorter<K, TU::MT, TU::MI>;
-    auto fn = merge_pass_kernel<K, TU::MT, TU::MI>;
-    QCK(allow_smem((const void*)fn, BS::kSmemBytes));
     K* s = Y;
     K* d = (Y == A) ? B : A;
-    for (uint64_t run = C; run < len; run *= 2) {
-        QLAUNCH(led, kPhMerge, 2 * len * sizeof(K),
-                fn<<<(unsigned)((len + MC - 1) / MC), TU::MT, BS::kSmemBytes, st>>>(s + off, d + off, len, run));
-        ++led.merge_passes;
-        std::swap(s, d);
+    constexpr uint64_t BC = (uint64_t)TU::MT * TU::BMI;  // bulk merge tile
+    static_assert(C % BC == 0, "bulk merge tiles never straddle a run pair");
+    const uint64_t mtiles = (len + MC - 1) / MC;
+    const uint64_t btiles = (len + BC - 1) / BC;
+    if (QMSORT_MERGE_BULK && TU::MERGE_BULK && splits && splits_cap >= btiles) {
+        using BM = BulkMerge<K, TU::MT, TU::BMI>;
+        auto fn = merge_pass_bulk_kernel<K, TU::MT, TU::BMI>;
+        QCK(allow_smem((const void*)fn, BM::kSmemBytes));
+        const unsigned grid = (unsigned)std::min<uint64_t>(btiles, resident_grid((const void*)fn, TU::MT, BM::kSmemBytes));
+        for (uint64_t run = C; run < len; run *= 2) {
+            QLAUNCH(led, kPhMerge, 0,
+                    merge_split_kernel<K><<<(unsigned)std::min<uint64_t>((btiles + 255) / 256, 1184), 256, 0, st>>>(
+                        s + off, len, run, BC, btiles, splits));
+            QLAUNCH(led, kPhMerge, 2 * len * sizeof(K),
+                    fn<<<grid, TU::MT, BM::kSmemBytes, st>>>(s + off, d + off, len, run, splits, btiles));
+            ++led.merge_passes;
+            std::swap(s, d);
+        }
+    } else {
+        using BS = BlockSorter<K, TU::MT, TU::MI>;
+        auto fn = merge_pass_kernel<K, TU::MT, TU::MI>;
+        QCK(allow_smem((const void*)fn, BS::kSmemBytes));
+        for (uint64_t run = C; run < len; run *= 2) {
+            QLAUNCH(led, kPhMerge, 2 * len * sizeof(K),
+                    fn<<<(unsigned)mtiles, TU::MT, BS::kSmemBytes, st>>>(s + off, d + off, len, run));
+            ++led.merge_passes;
+            std::swap(s, d);
+        }
     }
     if (s != A) return fail(QMSORT_EINTERNAL, "merge passes ended outside the caller buffer");
     return QMSORT_OK;
@@ -573,7 +609,8 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             QLAUNCH(led, kPhSample, 0,
                     gather_strided_kernel<K><<<(unsigned)std::min<uint64_t>((s0 + 255) / 256, 1184), 256, 0, st>>>(
                         src, n, s0, stride, B, xf));
-            QTRY(mergesort_range<K>(B, B, B + s0, 0, s0, st, led));
+            QTRY(mergesort_range<K>(B, B, B + s0, 0, s0, st, led, reinterpret_cast<uint64_t*>(ws + L.hist_off),
+                                    L.hist_cap / 2));
             presorted = B;
             presorted_n = (uint32_t)s0;
         }
@@ -632,7 +669,8 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             QCK(spin_sync(st));
             ++led.syncs;
             for (const SegDesc& d : h) {
-                QTRY(mergesort_range<K>(src, A, B, d.off, d.len, st, led));
+                QTRY(mergesort_range<K>(src, A, B, d.off, d.len, st, led,
+                                        reinterpret_cast<uint64_t*>(ws + L.hist_off), L.hist_cap / 2));
                 if (fused) QTRY(xf_range<K>(A + d.off, d.len, xf, true, st, led));
             }
             break;
@@ -686,7 +724,8 @@ static int sort_core(K* A, size_t n, const qmsort_gpu_config& cfg, unsigned char
     if (src0) QCK(cudaMemcpyAsync(A, src0, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
     if (fused) QTRY(xf_range<K>(A, n, xf, false, st, led));
     if (n <= cap) QTRY(blocksort_one<K>(A, A, 0, n, st, led));
-    else QTRY(mergesort_range<K>(A, A, B, 0, n, st, led));
+    else QTRY(mergesort_range<K>(A, A, B, 0, n, st, led, reinterpret_cast<uint64_t*>(ws + L.hist_off),
+                                 L.hist_cap / 2));
     if (fused) QTRY(xf_range<K>(A, n, xf, true, st, led));
     return QMSORT_OK;
 }

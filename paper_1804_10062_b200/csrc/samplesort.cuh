@@ -394,6 +394,8 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
 #pragma unroll
         for (int u = 0; u < U; ++u) j[u] = t[u] - (1u << d.logk);
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) QCHECK(j[u] <= (1u << d.logk), j[u], d.m);
     if (d.eq) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -592,7 +594,10 @@ __device__ __forceinline__ void count_chunk(const ClassifierSmem<K, LOG_KMAX>& c
         for (int u = 0; u < U; ++u) k[u] = XF ? xf_fwd(p[base + u * T], xf) : p[base + u * T];
         classify_keys<K, LOG_KMAX, U>(k, cls, d, bin);
 #pragma unroll
-        for (int u = 0; u < U; ++u) atomicAdd(&shist[bin[u]], 1u);
+        for (int u = 0; u < U; ++u) {
+            QCHECK(bin[u] < nb, bin[u], nb);
+            atomicAdd(&shist[bin[u]], 1u);
+        }
     }
     if (base < len) {
         const uint32_t rem = len - base;
@@ -798,6 +803,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 }
             }
         } else if (len <= p.cap) {
+            QCHECK((uint64_t)start[b] + len <= d.len, start[b] + len, d.len);
             const uint32_t sl = slot[b];
             if (sl == 0xFFFFFFFFu) continue;  // single key already in place
             const uint32_t cls = sl >> 28;
@@ -911,8 +917,15 @@ template <class K>
 struct LocalSink {
     static constexpr bool kFewBinsOnly = false;
     K* out;
-    __device__ __forceinline__ void store(uint32_t dest, const K& key) const { out[dest] = key; }
-    __device__ __forceinline__ void store_bin(uint32_t, uint32_t dest, const K& key) const { out[dest] = key; }
+    uint64_t lim;  // the segment's length (checked builds)
+    __device__ __forceinline__ void store(uint32_t dest, const K& key) const {
+        QCHECK(dest < lim, dest, lim);
+        out[dest] = key;
+    }
+    __device__ __forceinline__ void store_bin(uint32_t, uint32_t dest, const K& key) const {
+        QCHECK(dest < lim, dest, lim);
+        out[dest] = key;
+    }
 };
 // The fused exchange: bin b's keys go to base[b] + (segment-relative
 // position) * sizeof(K), base[b] = dest[rank(b)] + (bin_off[b] - local start
@@ -1015,6 +1028,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         if (FULL || u * T + tid < m) {
             const uint2 sg = sm.sd[bin[u] >> 16];
             const uint32_t pos = sg.x + (bin[u] & 0xFFFFu);
+            QCHECK(pos < m, pos, m);
             typename SM::Rec r;
             if constexpr (SM::kStageIndex) r.key = u * T + tid;
             else r.key = k[u];
@@ -1113,7 +1127,7 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
                 if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
             }
         } else {
-            const LocalSink<K> out{dst + d.off};
+            const LocalSink<K> out{dst + d.off, d.len};
             if (xf.a | xf.b) {  // level 0 of a fused-transform sort
                 for (; t0 + TILE <= len; t0 += TILE)
                     scatter_tile<K, T, U, LOG_KMAX, true, true>(sm, d, p + t0, TILE, out, cursor, xf);
@@ -1152,12 +1166,16 @@ template <class K, int T, int ITEMS>
 // 64 regs 1735 us, 48-51 regs 1684 us, 40 regs 1673 us).  Other keys: the
 // compiler's choice (0) -- an explicit 1 lets it take ~50% more registers
 // (measured: u64 and record block sorts 30% slower).
-__global__ void __launch_bounds__(T, sizeof(K) == 4 ? 1536 / T : 0) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
+#ifndef QMSORT_BS_U32_THREADS
+#define QMSORT_BS_U32_THREADS 1536
+#endif
+__global__ void __launch_bounds__(T, sizeof(K) == 4 ? QMSORT_BS_U32_THREADS / T : 0) blocksort_tasks_kernel(const SortTask* __restrict__ tasks, K* A,
                                                             const K* B, Xf xf = Xf{0, 0}) {
     using BS = BlockSorter<K, T, ITEMS>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* s = reinterpret_cast<K*>(smem_raw);
     const SortTask t = tasks[blockIdx.x];
+    QCHECK(t.len <= (uint32_t)BS::kCap, t.len, BS::kCap);
     BS::sort_tile((t.in_a ? A : B) + t.off, A + t.off, (int)t.len, s, xf);
 }
 
