@@ -21,6 +21,13 @@
 
 #include "common.cuh"
 
+#ifndef QMSORT_SELECT_PRED
+#define QMSORT_SELECT_PRED 1
+#endif
+#ifndef QMSORT_SELECT_PRED16
+#define QMSORT_SELECT_PRED16 0
+#endif
+
 namespace qmsort_b200 {
 
 // Batcher odd-even merge sort network on N register-resident keys.  The
@@ -138,8 +145,12 @@ __device__ __forceinline__ void bitonic_merge_window(const K* s, int ai, int x, 
 // min (lower = true) or max of a and b.
 template <class K>
 __device__ __forceinline__ K select_minmax(const K& a, const K& b, bool lower) {
-    const bool b_less = KeyTraits<K>::lt(b, a);
-    return (b_less == lower) ? b : a;
+    if constexpr (std::is_same<K, uint32_t>::value && QMSORT_SELECT_PRED) {
+        return lower ? min(a, b) : max(a, b);  // two predicated VIMNMX
+    } else {
+        const bool b_less = KeyTraits<K>::lt(b, a);
+        return (b_less == lower) ? b : a;
+    }
 }
 
 // Two 16-bit keys in one register: the halves are two independent sequences
@@ -163,12 +174,19 @@ struct KeyTraits<U16x2> {
         return U16x2{__shfl_xor_sync(0xffffffffu, a.v, m)};
     }
 };
-// Both halves' min and max, then one LOP3 picks per lane (a branch-free
-// select; `lower ? vmin : vmax` compiles to predicated moves).
+// min or max of both halves, chosen per lane: both min and max and one LOP3
+// (three issue slots).  QMSORT_SELECT_PRED16: `lower ? vmin : vmax`, which
+// ptxas emits as two predicated VIMNMX.U16x2 -- measured slower in the packed
+// block sort (C2: 1683 against 1640 us), while the unpacked uint32 select
+// (QMSORT_SELECT_PRED) gains (C2 sample kernel 146 -> 130 us).
 __device__ __forceinline__ U16x2 select_minmax(const U16x2& a, const U16x2& b, bool lower) {
+#if QMSORT_SELECT_PRED16
+    return U16x2{lower ? __vminu2(a.v, b.v) : __vmaxu2(a.v, b.v)};
+#else
     const uint32_t msk = 0u - (uint32_t)lower;
     const uint32_t mn = __vminu2(a.v, b.v), mx = __vmaxu2(a.v, b.v);
     return U16x2{(mn & msk) | (mx & ~msk)};
+#endif
 }
 
 // One warp-level merge round: every pair of ascending runs of `lr` lanes x

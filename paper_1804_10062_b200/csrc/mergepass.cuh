@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(T) merge_pass_bulk_kernel(const K* __restrict_
     using BM = BulkMerge<K, T, ITEMS>;
     using BS = BlockSorter<K, T, ITEMS>;
     constexpr int C = BM::C;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t mbar[2];
     __shared__ uint32_t s_off[2][2];  // element offsets of the A and B slices in each stage
     unsigned char* stage[2] = {smem_raw, smem_raw + BM::kStageBytes};
