@@ -197,21 +197,6 @@ int qmsort_gpu_partition(int core_dtype, const void* d_in, size_t n, const void*
                          uint32_t nsplit, void* d_out, uint64_t* d_counts, void* d_ws,
                          size_t ws_bytes, void* stream);
 
-/* The same partition split in two so that the exchange is fused into the
- * scatter: partition_count classifies and counts (bucket
- * sizes into d_counts) and keeps its plan in d_ws; partition_scatter_peers
- * then writes bucket b's keys, in bucket order, straight to
- * dests[b] + dest_offsets[b] elements -- rank b's receive buffer, a peer GPU's
- * memory mapped with qmsort_gpu_ipc_open (NVLink), or this GPU's own -- with
- * no staging copy and no collective on the data.  nsplit + 1 <= 8.  Both
- * calls take the same d_in, n and caller workspace. */
-int qmsort_gpu_partition_count(int core_dtype, const void* d_in, size_t n, const void* d_splitters,
-                               uint32_t nsplit, uint64_t* d_counts, void* d_ws, size_t ws_bytes,
-                               void* stream);
-int qmsort_gpu_partition_scatter_peers(int core_dtype, const void* d_in, size_t n, uint32_t nsplit,
-                                       void* const* dests, const uint64_t* dest_offsets,
-                                       void* d_ws, size_t ws_bytes, void* stream);
-
 /* ---- PartitionResult (partition_result.hpp:12-17) ----------------------- */
 /* Three-way partition of d_data[0..n) around the pivot value *h_pivot (caller
  * dtype, host memory) under cmp, in place: on return [0, c0) < pivot,
@@ -252,33 +237,58 @@ int qmsort_gpu_sort_sharded(int dtype, int cmp, uint32_t P, const int* devices,
  *   1. shard_sample: s seeded keys of the rank's caller-dtype data, mapped
  *      into the core key domain (seed: cfg.seed ^ 0x9E3779B97F4A7C15 * (r+1));
  *   2. (all ranks' samples gathered and sorted as core keys, e.g. with
- *      qmsort_gpu_sort) shard_splitters: P-1 quantile splitters, merged into
- *      nuniq distinct values with multiplicities (host only);
+ *      qmsort_gpu_sort) shard_splitters: nbuckets - 1 quantile splitters,
+ *      merged into nuniq distinct values with multiplicities (host only);
+ *      nbuckets = P * shard_subbuckets(dtype, P, n_total) for the folded
+ *      exchange (n_total: the keys of all ranks), P
+ *      for the plain one;
  *   3. shard_count: three-way counts, 2 nuniq + 1 bins (bin 2j: keys between
- *      splitters j-1 and j; 2j+1: keys equal to splitter j); the plan stays
- *      in d_ws (shard_workspace_bytes);
- *   4. shard_plan (host only, identical on every rank) from the P x (2 nuniq
- *      + 1) count matrix (row = sender): bin -> rank (-1: an equal-key run
- *      spread over several ranks as fills), per-sender offsets in the
- *      receivers' buffers, receive sizes and fills;
+ *      splitters j-1 and j; 2j+1: keys equal to splitter j), or -- three_way
+ *      = 0, for distinct splitters (every multiplicity 1) -- two-way counts,
+ *      nuniq + 1 bins (bin j: keys above splitter j-1 up to splitter j; read
+ *      them as the open bins 2j of the plan, equal bins 0); the plan stays in
+ *      d_ws (shard_workspace_bytes); shard_scatter takes the same flag;
+ *   4. the plan (host only, identical on every rank) from the P x (2 nuniq
+ *      + 1) count matrix (row = sender):
+ *      - folded (shard_plan_folded): every rank's slice as a three-way bin
+ *        list of its own -- loc_m[r] local distinct splitters (indices into
+ *        the global ones, P x (K0+1)), 2 loc_m[r] + 1 bin counts (P x
+ *        (2K0+3)) -- the level 0 of its local sort; out_n[r] keys in all;
+ *      - plain (shard_plan): receive sizes and lower / upper fills;
+ *      both give bin -> rank (-1: equal keys, filled by the receivers) and
+ *      per-sender offsets in the receivers' buffers;
  *   5. shard_scatter: the rank's bins straight into rank_dest[] (its row of
- *      bin_off), peer memory or local;
- *   6. shard_finish: [lo fill | sorted received keys | hi fill] into d_out,
- *      the received keys sorted out of place (d_recv is only read).
- * Receive buffers and d_out hold caller-dtype keys. */
+ *      bin_off; recv_n[r] keys in rank r's buffer), peer memory or local;
+ *      raw = 0 ships core keys (folded), 1 the caller's (plain);
+ *   6. folded: shard_finish_presplit sorts rank r's keys -- core keys already
+ *      at their level-0 offsets in the B half (offset 0) of the workspace d_ws
+ *      that served as its receive buffer (>= workspace_bytes(dtype, n)) --
+ *      into d_out, fills included; plain: shard_finish writes [lo fill |
+ *      sorted received keys | hi fill] into d_out (d_recv is only read). */
 size_t qmsort_gpu_shard_workspace_bytes(int dtype, size_t n);
+uint32_t qmsort_gpu_shard_subbuckets(int dtype, uint32_t P, uint64_t n_total);
 int qmsort_gpu_shard_sample(int dtype, int cmp, const void* d_in, size_t n, size_t s, uint64_t seed,
                             void* d_out_core, void* stream);
-int qmsort_gpu_shard_splitters(int core_dtype, const void* h_sorted_sample, size_t m, uint32_t P,
+int qmsort_gpu_shard_splitters(int core_dtype, const void* h_sorted_sample, size_t m, uint32_t nbuckets,
                                void* h_uniq, uint32_t* h_mult, uint32_t* nuniq);
 int qmsort_gpu_shard_count(int dtype, int cmp, const void* d_in, size_t n, const void* d_uniq,
-                           uint32_t nuniq, uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream);
+                           uint32_t nuniq, int three_way, uint64_t* d_counts, void* d_ws, size_t ws_bytes,
+                           void* stream);
 int qmsort_gpu_shard_plan(uint32_t P, uint32_t nuniq, const uint32_t* h_mult, const uint64_t* h_counts,
                           int32_t* h_bin_rank, uint64_t* h_bin_off, uint64_t* h_recv_n,
                           uint64_t* h_lo_fill, uint64_t* h_hi_fill, int32_t* h_lo_val, int32_t* h_hi_val);
-int qmsort_gpu_shard_scatter(int dtype, int cmp, const void* d_in, size_t n, uint32_t nuniq,
+int qmsort_gpu_shard_plan_folded(uint32_t P, uint32_t K0, uint32_t nuniq, const uint32_t* h_mult,
+                                 const uint64_t* h_counts, int32_t* h_bin_rank, uint64_t* h_bin_off,
+                                 uint64_t* h_out_n, uint32_t* h_loc_m, int32_t* h_loc_uniq,
+                                 uint64_t* h_loc_counts);
+int qmsort_gpu_shard_scatter(int dtype, int cmp, const void* d_in, size_t n, uint32_t nuniq, int three_way,
                              const int32_t* h_bin_rank, const uint64_t* h_bin_off, void* const* rank_dest,
-                             uint32_t P, void* d_ws, size_t ws_bytes, void* stream);
+                             const uint64_t* h_recv_n, uint32_t P, int raw, void* d_ws, size_t ws_bytes,
+                             void* stream);
+int qmsort_gpu_shard_finish_presplit(int dtype, int cmp, void* d_out, size_t n, const void* d_local_uniq,
+                                     uint32_t local_m, const uint64_t* h_local_counts,
+                                     const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes,
+                                     qmsort_gpu_metrics* metrics, void* stream);
 int qmsort_gpu_shard_finish(int dtype, int cmp, const void* d_recv, size_t n_recv, const void* d_uniq,
                             int32_t lo_val, uint64_t lo_fill, int32_t hi_val, uint64_t hi_fill, void* d_out,
                             const qmsort_gpu_config* cfg, void* d_ws, size_t ws_bytes,

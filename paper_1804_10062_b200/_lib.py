@@ -92,8 +92,6 @@ EXPORTED = [
     "qmsort_gpu_select_nth",
     "qmsort_gpu_select_nth_host",
     "qmsort_gpu_sort_host_batch",
-    "qmsort_gpu_partition_count",
-    "qmsort_gpu_partition_scatter_peers",
     "qmsort_gpu_ipc_handle",
     "qmsort_gpu_ipc_open",
     "qmsort_gpu_ipc_close",
@@ -105,6 +103,9 @@ EXPORTED = [
     "qmsort_gpu_shard_plan",
     "qmsort_gpu_shard_scatter",
     "qmsort_gpu_shard_finish",
+    "qmsort_gpu_shard_subbuckets",
+    "qmsort_gpu_shard_plan_folded",
+    "qmsort_gpu_shard_finish_presplit",
     "qmsort_gpu_partition3_workspace_bytes",
     "qmsort_gpu_partition3",
     "qmsort_gpu_partition3_host",
@@ -150,9 +151,6 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_select_nth": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, vp, sz, mp, vp]),
         "qmsort_gpu_select_nth_host": (i, [i, i, vp, sz, sz, ctypes.POINTER(sz), cfgp, mp]),
         "qmsort_gpu_sort_host_batch": (i, [i, i, ctypes.POINTER(vp), ctypes.POINTER(sz), sz, cfgp, mp]),
-        "qmsort_gpu_partition_count": (i, [i, vp, sz, vp, ctypes.c_uint32, vp, vp, sz, vp]),
-        "qmsort_gpu_partition_scatter_peers": (i, [i, vp, sz, ctypes.c_uint32, ctypes.POINTER(vp),
-                                                   ctypes.POINTER(u64), vp, sz, vp]),
         "qmsort_gpu_ipc_handle": (i, [vp, vp, ctypes.POINTER(u64)]),
         "qmsort_gpu_ipc_open": (i, [vp, u64, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
         "qmsort_gpu_ipc_close": (i, [vp]),
@@ -161,12 +159,17 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "qmsort_gpu_shard_workspace_bytes": (sz, [i, sz]),
         "qmsort_gpu_shard_sample": (i, [i, i, vp, sz, sz, u64, vp, vp]),
         "qmsort_gpu_shard_splitters": (i, [i, vp, sz, u32, vp, ctypes.POINTER(u32), ctypes.POINTER(u32)]),
-        "qmsort_gpu_shard_count": (i, [i, i, vp, sz, vp, u32, vp, vp, sz, vp]),
+        "qmsort_gpu_shard_count": (i, [i, i, vp, sz, vp, u32, i, vp, vp, sz, vp]),
         "qmsort_gpu_shard_plan": (i, [u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u64), ctypes.POINTER(i32),
                                       ctypes.POINTER(u64), ctypes.POINTER(u64), ctypes.POINTER(u64),
                                       ctypes.POINTER(u64), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
-        "qmsort_gpu_shard_scatter": (i, [i, i, vp, sz, u32, ctypes.POINTER(i32), ctypes.POINTER(u64),
-                                         ctypes.POINTER(vp), u32, vp, sz, vp]),
+        "qmsort_gpu_shard_scatter": (i, [i, i, vp, sz, u32, i, ctypes.POINTER(i32), ctypes.POINTER(u64),
+                                         ctypes.POINTER(vp), ctypes.POINTER(u64), u32, i, vp, sz, vp]),
+        "qmsort_gpu_shard_subbuckets": (u32, [i, u32, u64]),
+        "qmsort_gpu_shard_plan_folded": (i, [u32, u32, u32, ctypes.POINTER(u32), ctypes.POINTER(u64),
+                                             ctypes.POINTER(i32), ctypes.POINTER(u64), ctypes.POINTER(u64),
+                                             ctypes.POINTER(u32), ctypes.POINTER(i32), ctypes.POINTER(u64)]),
+        "qmsort_gpu_shard_finish_presplit": (i, [i, i, vp, sz, vp, u32, ctypes.POINTER(u64), cfgp, vp, sz, mp, vp]),
         "qmsort_gpu_shard_finish": (i, [i, i, vp, sz, vp, i32, u64, i32, u64, vp, cfgp, vp, sz, mp, vp]),
         "qmsort_gpu_partition3_workspace_bytes": (sz, [i, sz]),
         "qmsort_gpu_partition3": (i, [i, i, vp, sz, vp, ctypes.POINTER(u64), cfgp, vp, sz, mp, vp]),

@@ -356,7 +356,7 @@ static WsLayout make_layout(size_t n, uint32_t min_cap = class_cap<K>(kNumClasse
     const uint64_t last_target = target * TU::LAST_NUM / TU::LAST_DEN;  // choose_logk's last level
     L.split_cap = (uint32_t)(2 * n / last_target + 2 * (uint64_t)L.seg_cap + 2 * (1u << TU::LOGKMAX) + 64);
     L.task_cap = 4 * L.split_cap + 64;  // per class, all levels of one sort
-    L.fill_cap = L.split_cap;
+    L.fill_cap = 2 * L.split_cap;  // small fills from the front, large from the back (each <= split_cap)
     // histogram words of one level: a segment of len keys takes (nch + 1) 2K
     // words with nch <= len/ch + 1 and 2K <= min(2 K_max, 4 len/last_target + 4)
     // (choose_logk), so a level needs at most
@@ -518,11 +518,24 @@ static int mergesort_range(K* X, K* A, K* B, uint64_t off, uint64_t len, cudaStr
 
 // xf (fused transform): level 0 reads the caller's keys through f, every
 // final write (block sort, fills, merge fallback) goes through f^-1.
+// A level 0 done elsewhere (the folded sharded exchange): B holds the n core
+// keys grouped into the three-way bins of the m distinct splitters uniq
+// (device, core keys) -- open, equal, open, ..., open, with the host's
+// counts[2m+1] -- equal bins unwritten (they become fills).
+template <class K>
+struct Presplit {
+    const K* uniq;
+    uint32_t m;
+    const uint64_t* counts;
+};
+
 // src0 (optional): level 0 reads the keys from there instead of A (an
-// out-of-place sort; src0 is only read).
+// out-of-place sort; src0 is only read).  pre (optional): start at level 1
+// from a level 0 done elsewhere.
 template <class K>
 static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsigned char* ws,
-                      const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf, const K* src0 = nullptr) {
+                      const WsLayout& L, cudaStream_t st, Ledger& led, Xf xf, const K* src0 = nullptr,
+                      const Presplit<K>* pre = nullptr) {
     const bool fused = xf.a != 0 || xf.b != 0;
     using TU = Tune<K>;
     constexpr uint32_t cap_max = class_cap<K>(kNumClasses - 1);
@@ -576,7 +589,8 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     // every level's counters start at zero; level l reads its segment and
     // chunk counts from cnts[l] (written by level l-1) on the device
     QCK(cudaMemsetAsync(cnts, 0, sizeof(LevelCounters) * kCntSlots, st));
-    QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<16, 256, 0, st>>>(lv[0], n, ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K))), p));
+    const uint64_t key_max = ~0ull >> (64 - 8 * (int)std::min<size_t>(8, sizeof(K)));
+    if (!pre) QLAUNCH(led, kPhPlan, 0, init_level_kernel<<<16, 256, 0, st>>>(lv[0], n, key_max, p));
 
     using BSS = BlockSorter<K, TU::ST, TU::SI>;
     auto sample_fn = sample_kernel<K, TU::ST, TU::SI>;
@@ -596,6 +610,45 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
 
     K* src = src0 ? const_cast<K*>(src0) : A;  // level 0 only reads it
     K* dst = B;
+    int level = 0;
+    int batch = std::max(1, estimate_levels(n, p));
+    if (pre) {
+        // level 0's result is in B: its segment (one, three-way, no chunks:
+        // the bin totals are the plan's histogram) and the plan of its
+        // children, then the level loop from level 1 (B -> A)
+        const uint32_t logk = std::max<uint32_t>(1, ceil_log2_u64((uint64_t)pre->m + 1));
+        if (logk > (uint32_t)TU::LOGKMAX) return fail(QMSORT_EINVAL, "presplit: too many splitters");
+        SegDesc d{};
+        d.off = 0;
+        d.len = n;
+        d.lo = 0;
+        d.hi = key_max;
+        d.logk = logk;
+        d.m = pre->m;
+        d.eq = 1;
+        d.lutbits = std::min(logk + 4, (uint32_t)kLutMaxBits);
+        std::vector<uint32_t> hh(2u << logk, 0);
+        uint64_t biggest = 0;
+        for (uint32_t b = 0; b < 2 * pre->m + 1; ++b) {
+            hh[b] = (uint32_t)pre->counts[b];
+            if (!(b & 1)) biggest = std::max<uint64_t>(biggest, pre->counts[b]);
+        }
+        const uint32_t one = 1;
+        QCK(cudaMemcpyAsync(lv[0].segs, &d, sizeof(d), cudaMemcpyHostToDevice, st));
+        QCK(cudaMemcpyAsync(hist, hh.data(), hh.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        QCK(cudaMemcpyAsync(&cnts[0].nsegs, &one, sizeof(one), cudaMemcpyHostToDevice, st));
+        if (pre->m) QCK(cudaMemcpyAsync(sorted[0], pre->uniq, sizeof(K) * pre->m, cudaMemcpyDeviceToDevice, st));
+        p.dst_is_a = 0;  // level 0 "wrote" B
+        lv[0].cnt = &cnts[0];
+        lv[1].cnt = &cnts[1];
+        QLAUNCH(led, kPhPlan, 0,
+                plan_fn<<<plan_grid, 512, 0, st>>>(lv[0].segs, hist, sorted[0], lv[1], p, tasks, fills, &cnts[0], tot));
+        level = 1;
+        src = B;
+        dst = A;
+        batch = std::max(1, estimate_levels(biggest, p));
+        // the fake level 0 adds nothing to the pass ledger (its nkeys is 0)
+    }
     // median_of_sqrt_n (median_of_sqrt_pivot, partition.hpp:235-251): level 0
     // draws s = 2 floor(sqrt(n)/2) + 1 strided keys; more than one block sort
     // holds are sorted here first (block sort + merge passes in B, which
@@ -604,7 +657,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     uint32_t presorted_n = 0;
     {
         const uint64_t s0 = sqrt_sample_size(n);
-        if (cfg.pivot == 1 && s0 > (uint64_t)BSS::kCap && 2 * s0 <= n) {
+        if (!pre && cfg.pivot == 1 && s0 > (uint64_t)BSS::kCap && 2 * s0 <= n) {
             const uint64_t stride = n / s0;
             QLAUNCH(led, kPhSample, 0,
                     gather_strided_kernel<K><<<(unsigned)std::min<uint64_t>((s0 + 255) / 256, 1184), 256, 0, st>>>(
@@ -615,9 +668,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             presorted_n = (uint32_t)s0;
         }
     }
-    const int max_levels = std::min(cfg.max_levels > 0 ? cfg.max_levels : 8, kCntSlots - 2);
-    int level = 0;
-    int batch = std::max(1, estimate_levels(n, p));
+    const int max_levels = std::max(level + 1, std::min(cfg.max_levels > 0 ? cfg.max_levels : 8, kCntSlots - 2));
     LevelCounters hc[kCntSlots];
     for (;;) {
         // enqueue a batch of levels back to back: every grid is persistent
@@ -683,8 +734,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     for (int c = 0; c < kNumClasses; ++c)
         if (nt[c] > L.task_cap) return fail(QMSORT_EINTERNAL, "block-sort task list capacity exceeded");
     QTRY((launch_classes_from<K, 0>(tasks, L.task_cap, nt, A, B, st, led, xf)));
-    if (hc[kCntSlots - 1].nfill)
-        QLAUNCH(led, kPhFill, 0, fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, L.fill_cap, A, xf));
+    if (hc[kCntSlots - 1].nfill || hc[kCntSlots - 1].nfill_big)
+        QLAUNCH(led, kPhFill, 0,
+                fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, &tot->nfill_big, L.fill_cap, A, xf));
     // pass ledger from the device counters (count 1, scatter 2, block sort 2, fill 1)
     const uint64_t w = sizeof(K);
     for (int l = 0; l < level; ++l) {
@@ -1668,29 +1720,6 @@ int qmsort_gpu_partition(int core, const void* d_in, size_t n, const void* spl, 
                            nullptr);
 }
 
-int qmsort_gpu_partition_count(int core, const void* d_in, size_t n, const void* d_splitters,
-                               uint32_t nsplit, uint64_t* d_counts, void* d_ws, size_t ws_bytes,
-                               void* stream) {
-    return partition_entry(core, d_in, n, d_splitters, nsplit, nullptr, d_counts, d_ws, ws_bytes,
-                           stream, 1, nullptr);
-}
-
-int qmsort_gpu_partition_scatter_peers(int core, const void* d_in, size_t n, uint32_t nsplit,
-                                       void* const* dests, const uint64_t* dest_offsets,
-                                       void* d_ws, size_t ws_bytes, void* stream) {
-    if (nsplit + 1 > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "at most 8 destination ranks");
-    if (n > 0 && (dests == nullptr || dest_offsets == nullptr))
-        return fail(QMSORT_EINVAL, "null destination list");
-    PeerArgs pa{};
-    pa.nbins = nsplit + 1;
-    for (uint32_t b = 0; n > 0 && b < pa.nbins; ++b) {  // bucket b -> rank b
-        pa.dest[b] = reinterpret_cast<unsigned long long>(dests[b]);
-        pa.bin_rank[b] = (signed char)b;
-        pa.bin_off[b] = dest_offsets[b];
-    }
-    return partition_entry(core, d_in, n, nullptr, nsplit, nullptr, nullptr, d_ws, ws_bytes, stream,
-                           2, &pa);
-}
 
 size_t qmsort_gpu_partition3_workspace_bytes(int dtype, size_t n) {
     if (dtype_size(dtype) == 0) return 0;
@@ -1738,18 +1767,42 @@ int qmsort_gpu_shard_sample(int dtype, int cmp, const void* d_in, size_t n, size
     return dispatch_sample(dtype, cmp, d_in, n, s, seed, d_out, static_cast<cudaStream_t>(stream));
 }
 
-int qmsort_gpu_shard_splitters(int core, const void* h_sorted, size_t m, uint32_t P, void* h_uniq,
+int qmsort_gpu_shard_splitters(int core, const void* h_sorted, size_t m, uint32_t nbuckets, void* h_uniq,
                                uint32_t* h_mult, uint32_t* nuniq) {
     if (!h_sorted || !h_uniq || !h_mult || !nuniq) return fail(QMSORT_EINVAL, "null argument");
-    return shard_splitters_host(core, h_sorted, m, P, h_uniq, h_mult, nuniq);
+    return shard_splitters_host(core, h_sorted, m, nbuckets, h_uniq, h_mult, nuniq);
+}
+
+uint32_t qmsort_gpu_shard_subbuckets(int dtype, uint32_t P, uint64_t n_total) {
+    if (dtype_size(dtype) == 0 || P < 1 || P > (uint32_t)kMaxPeers) return 0;
+    return shard_subbuckets(dtype, P, n_total);
+}
+
+int qmsort_gpu_shard_plan_folded(uint32_t P, uint32_t K0, uint32_t nuniq, const uint32_t* mult,
+                                 const uint64_t* counts, int32_t* bin_rank, uint64_t* bin_off, uint64_t* out_n,
+                                 uint32_t* loc_m, int32_t* loc_uniq, uint64_t* loc_counts) {
+    if ((nuniq && !mult) || !counts || !bin_rank || !bin_off || !out_n || !loc_m || !loc_uniq || !loc_counts)
+        return fail(QMSORT_EINVAL, "null argument");
+    return shard_plan_folded_host(P, K0, nuniq, mult, counts, bin_rank, bin_off, out_n, loc_m, loc_uniq, loc_counts);
+}
+
+int qmsort_gpu_shard_finish_presplit(int dtype, int cmp, void* d_out, size_t n, const void* d_local_uniq,
+                                     uint32_t local_m, const uint64_t* h_local_counts, const qmsort_gpu_config* cfg,
+                                     void* d_ws, size_t ws_bytes, qmsort_gpu_metrics* metrics, void* stream) {
+    if (!h_local_counts) return fail(QMSORT_EINVAL, "null counts");
+    uint64_t tot = 0;
+    for (uint32_t b = 0; b < 2 * local_m + 1; ++b) tot += h_local_counts[b];
+    if (tot != n) return fail(QMSORT_EINVAL, "local bin counts must sum to n");
+    return sort_presplit_device(dtype, cmp, d_out, n, d_local_uniq, local_m, h_local_counts, cfg, d_ws, ws_bytes,
+                                metrics, static_cast<cudaStream_t>(stream));
 }
 
 int qmsort_gpu_shard_count(int dtype, int cmp, const void* d_in, size_t n, const void* d_uniq, uint32_t nuniq,
-                           uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream) {
+                           int three_way, uint64_t* d_counts, void* d_ws, size_t ws_bytes, void* stream) {
     if (!d_counts || (nuniq && !d_uniq)) return fail(QMSORT_EINVAL, "null argument");
     Ledger led;
     return shard_partition(dtype, cmp, d_in, n, d_uniq, nuniq, d_counts, d_ws, ws_bytes,
-                           static_cast<cudaStream_t>(stream), 1, nullptr, led);
+                           static_cast<cudaStream_t>(stream), 1, nullptr, led, three_way != 0);
 }
 
 int qmsort_gpu_shard_plan(uint32_t P, uint32_t nuniq, const uint32_t* mult, const uint64_t* counts,
@@ -1761,16 +1814,15 @@ int qmsort_gpu_shard_plan(uint32_t P, uint32_t nuniq, const uint32_t* mult, cons
     return shard_plan_host(P, nuniq, mult, counts, bin_rank, bin_off, recv_n, lo_fill, hi_fill, lo_val, hi_val);
 }
 
-int qmsort_gpu_shard_scatter(int dtype, int cmp, const void* d_in, size_t n, uint32_t nuniq,
-                             const int32_t* bin_rank, const uint64_t* bin_off, void* const* rank_dest, uint32_t P,
-                             void* d_ws, size_t ws_bytes, void* stream) {
+int qmsort_gpu_shard_scatter(int dtype, int cmp, const void* d_in, size_t n, uint32_t nuniq, int three_way,
+                             const int32_t* bin_rank, const uint64_t* bin_off, void* const* rank_dest,
+                             const uint64_t* recv_n, uint32_t P, int raw, void* d_ws, size_t ws_bytes, void* stream) {
     if (n == 0) return validate(dtype, cmp, n, d_in);
-    if (!bin_rank || !bin_off || !rank_dest) return fail(QMSORT_EINVAL, "null argument");
-    PeerArgs pa;
-    QTRY(make_peer_args(nuniq, bin_rank, bin_off, rank_dest, P, &pa));
+    if (!bin_rank || !bin_off || !rank_dest || !recv_n) return fail(QMSORT_EINVAL, "null argument");
+    const ShardRoute rt{bin_rank, bin_off, rank_dest, recv_n, P, raw != 0};
     Ledger led;
     return shard_partition(dtype, cmp, d_in, n, nullptr, nuniq, nullptr, d_ws, ws_bytes,
-                           static_cast<cudaStream_t>(stream), 2, &pa, led);
+                           static_cast<cudaStream_t>(stream), 2, &rt, led, three_way != 0);
 }
 
 int qmsort_gpu_shard_finish(int dtype, int cmp, const void* d_recv, size_t n_recv, const void* d_uniq,

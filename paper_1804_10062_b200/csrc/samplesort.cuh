@@ -100,6 +100,7 @@ struct SortTask {  // one bucket for the block sorter
     uint32_t in_a;  // the bucket was scattered into A (else into B); it is sorted into A
 };
 
+constexpr uint64_t kFillWarp = 4096;  // fills up to this many keys get a warp each
 struct FillTask {  // equal-key bucket: every key equals the segment's splitter
     uint64_t off;
     uint64_t len;
@@ -111,7 +112,8 @@ struct LevelCounters {
     uint32_t nchunks;
     uint32_t nsplit;  // splitter storage used
     uint32_t nhist;   // histogram words used
-    uint32_t nfill;
+    uint32_t nfill;      // equal-key fills of <= kFillWarp keys, from the front of the list
+    uint32_t nfill_big;  // larger fills, from the back
     uint32_t ntasks[kNumClasses];
     uint32_t overflow;  // capacity exceeded somewhere (host reports an error)
     uint32_t work_count, work_scatter;  // dynamic chunk dispensers of this level's kernels
@@ -789,14 +791,16 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
         const uint64_t off = d.off + start[b];
         if (d.eq && (b & 1)) {  // equal-key bucket: final once it is in the caller's buffer
             if (!p.dst_is_a || p.xf_fix) {  // (fused transform: its fill writes f^-1)
-                const uint32_t f = atomicAdd(&sort_cnt->nfill, 1u);
-                if (f < p.fill_cap) {
+                // small fills from the front (a warp each), large ones from the back
+                const bool big = len > kFillWarp;
+                const uint32_t f = atomicAdd(big ? &sort_cnt->nfill_big : &sort_cnt->nfill, 1u);
+                if (f < p.fill_cap / 2) {
                     FillTask ft;
                     ft.off = off;
                     ft.len = len;
                     const K v = sorted_store[d.sp + (b >> 1)];
                     memcpy(ft.value, &v, sizeof(K));
-                    fills[f] = ft;
+                    fills[big ? p.fill_cap - 1 - f : f] = ft;
                     atomicAdd(&sort_cnt->fill_keys, (unsigned long long)len);
                 } else {
                     atomicExch(&cur_cnt->overflow, 1u);
@@ -902,20 +906,26 @@ __device__ __forceinline__ void vec_store(uint32_t* p, const uint32_t (&v)[N]) {
 // with coalesced stores.
 // Where a scatter writes: the segment's range of the destination buffer
 // (every level of the sort), or -- the sharded exchange fused into the
-// partition -- bucket b's keys straight into rank b's receive buffer, a peer
-// GPU's memory mapped through CUDA IPC, at that rank's offset for this sender.
+// partition -- every bin's keys straight into its rank's receive buffer, a
+// peer GPU's memory mapped through CUDA IPC (or this GPU's own), at that
+// rank's offset for this sender.  The ranks' buffers are laid end to end in
+// one virtual key space: rank r owns positions [vbase[r], vbase[r+1]); a
+// bin's write cursor starts at its virtual position for this sender
+// (bin_base, from the host's plan), so the scatter's own position arithmetic
+// is unchanged and each store maps its position to (rank, offset).
+// Positions >= vbase[nranks] belong to bins that are not sent (equal-key
+// runs the receivers fill).
 constexpr int kMaxPeers = 8;
-constexpr int kMaxPeerBins = 64;  // the few-bin (unstaged) scatter path handles <= 64 bins
+constexpr int kMaxPeerBins = 1024;  // bins of one exchange (2 x 512 with equality bins)
 struct PeerArgs {
-    unsigned long long dest[kMaxPeers];   // receive buffer of rank r (device pointer)
-    unsigned long long bin_off[kMaxPeerBins];  // element offset of this sender's bin b in its rank's buffer
-    signed char bin_rank[kMaxPeerBins];   // rank of bin b; -1: not sent (an equal-key share
-                                          // the receivers fill, see qmsort_gpu_shard_plan)
-    uint32_t nbins;
+    unsigned long long dest[kMaxPeers];  // receive buffer of rank r (device pointer)
+    uint32_t vbase[kMaxPeers + 1];       // virtual key positions of the ranks' buffers
+    uint32_t nranks;
+    uint32_t raw;                        // ship the caller's bit patterns (else core keys)
+    const uint32_t* bin_base;            // device: this sender's first virtual position per bin
 };
 template <class K>
 struct LocalSink {
-    static constexpr bool kFewBinsOnly = false;
     K* out;
     uint64_t lim;  // the segment's length (checked builds)
     __device__ __forceinline__ void store(uint32_t dest, const K& key) const {
@@ -927,17 +937,25 @@ struct LocalSink {
         out[dest] = key;
     }
 };
-// The fused exchange: bin b's keys go to base[b] + (segment-relative
-// position) * sizeof(K), base[b] = dest[rank(b)] + (bin_off[b] - local start
-// of b) * sizeof(K); 0 = the bin is not sent.
+// The fused exchange: a virtual position -> its rank (a three-step binary
+// search over the ranks' bases in shared memory; one rank: none) -> one
+// store at dmv[rank] + v * sizeof(K) (dmv = buffer - base * sizeof(K)).
 template <class K>
 struct PeerSink {
-    static constexpr bool kFewBinsOnly = true;  // <= kMaxPeerBins bins: never staged
-    const unsigned long long* base;  // shared memory, one per bin
-    __device__ __forceinline__ void store_bin(uint32_t b, uint32_t dest, const K& key) const {
-        const unsigned long long p = base[b];
-        if (p) *reinterpret_cast<K*>(p + (unsigned long long)dest * sizeof(K)) = key;
+    const unsigned long long* dmv;  // shared memory
+    const uint32_t* vb;             // shared memory: kMaxPeers + 1 bases, unused ranks = end
+    uint32_t nranks;
+    __device__ __forceinline__ void store(uint32_t v, const K& key) const {
+        if (v >= vb[kMaxPeers]) return;  // a bin that is not sent
+        uint32_t r = 0;
+        if (nranks > 1) {
+            r = v >= vb[4] ? 4u : 0u;
+            r += v >= vb[r + 2] ? 2u : 0u;
+            r += v >= vb[r + 1] ? 1u : 0u;
+        }
+        *reinterpret_cast<K*>(dmv[r] + (unsigned long long)v * sizeof(K)) = key;
     }
+    __device__ __forceinline__ void store_bin(uint32_t, uint32_t v, const K& key) const { store(v, key); }
 };
 
 template <class K, int T, int U, int LOG_KMAX, bool FULL, bool XF, class Sink, bool RAW = false>
@@ -959,7 +977,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
     }
     classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
     // rank within the tile's bucket; pack (bin, rank) into one word
-    if (Sink::kFewBinsOnly || ((1u << d.logk) << d.eq) <= 64) {
+    if (((1u << d.logk) << d.eq) <= 64) {
         // Few bins (the sharded exchange's P buckets, small segments): no
         // staging.  Warp-aggregated ranks give the lanes of one bin
         // consecutive slots after the bin's cursor, so every key is stored
@@ -986,7 +1004,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         __syncthreads();
         return;
     }
-    if constexpr (!Sink::kFewBinsOnly) {
+    {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         if (FULL || u * T + tid < m) bin[u] = (bin[u] << 16) | atomicAdd(&sm.hist[bin[u]], 1u);
@@ -1042,8 +1060,8 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         const uint32_t i = u * T + tid;
         if (FULL || i < m) {
             const typename SM::Rec r = stage[i];
-            if constexpr (SM::kStageIndex) out.store(r.dest, XF ? xf_fwd(p[r.key], xf) : p[r.key]);
-            else out.store(r.dest, r.key);
+            if constexpr (SM::kStageIndex) out.store(r.dest, XF && !RAW ? xf_fwd(p[r.key], xf) : p[r.key]);
+            else out.store(r.dest, RAW && XF ? xf_inv(r.key, xf) : r.key);
         }
     }
     __syncthreads();
@@ -1067,19 +1085,11 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
     __shared__ uint32_t next_chunk;
-    __shared__ unsigned long long peer_base[PEER ? kMaxPeerBins : 1];
-    if (PEER) {  // single segment: bin starts of the local grouping from the plan
-        const SegDesc d0 = segs[0];
-        const uint32_t nb0 = (1u << d0.logk) << d0.eq;
-        for (uint32_t b = threadIdx.x; b < kMaxPeerBins; b += T) {
-            unsigned long long v = 0;
-            if (b < nb0 && b < peers.nbins && peers.bin_rank[b] >= 0) {
-                const uint32_t st = hist[d0.hist_base + b * (d0.nchunks + 1) + d0.nchunks];
-                v = peers.dest[peers.bin_rank[b]] + (peers.bin_off[b] - st) * sizeof(K);
-            }
-            peer_base[b] = v;
-        }
-    }
+    __shared__ unsigned long long peer_dmv[PEER ? kMaxPeers : 1];
+    __shared__ uint32_t peer_vb[PEER ? kMaxPeers + 1 : 1];
+    if (PEER && threadIdx.x < kMaxPeers)
+        peer_dmv[threadIdx.x] = peers.dest[threadIdx.x] - (unsigned long long)peers.vbase[threadIdx.x] * sizeof(K);
+    if (PEER && threadIdx.x <= kMaxPeers) peer_vb[threadIdx.x] = peers.vbase[threadIdx.x];
     if (QMSORT_LEVEL_OVERFLOWED(nchunks_dev, nchunks)) return;
     const uint32_t nck = nchunks_dev ? *nchunks_dev : nchunks;  // device count: no host round trip
     uint32_t cur_seg = 0xFFFFFFFFu;
@@ -1105,7 +1115,8 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
             cursor[i] = 0;
             if (b < nb) {
                 const uint32_t* col = hist + d.hist_base + b * stride;
-                cursor[i] = col[d.nchunks] + col[ci];  // bucket start + chunk prefix
+                // bucket start (local) or the bin's virtual position (peers) + chunk prefix
+                cursor[i] = (PEER ? peers.bin_base[b] : col[d.nchunks]) + col[ci];
             }
             sm.hist[b] = 0;
         }
@@ -1115,12 +1126,17 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
         const uint32_t len = (uint32_t)(c.end - c.begin);
         uint32_t t0 = 0;
         if constexpr (PEER) {
-            const PeerSink<K> out{peer_base};
-            if (xf.a | xf.b) {
+            const PeerSink<K> out{peer_dmv, peer_vb, peers.nranks};
+            if ((xf.a | xf.b) && peers.raw) {  // ship the caller's keys
                 for (; t0 + TILE <= len; t0 += TILE)
                     scatter_tile<K, T, U, LOG_KMAX, true, true, PeerSink<K>, true>(sm, d, p + t0, TILE, out, cursor, xf);
                 if (t0 < len)
                     scatter_tile<K, T, U, LOG_KMAX, false, true, PeerSink<K>, true>(sm, d, p + t0, len - t0, out, cursor, xf);
+            } else if (xf.a | xf.b) {  // ship core keys
+                for (; t0 + TILE <= len; t0 += TILE)
+                    scatter_tile<K, T, U, LOG_KMAX, true, true, PeerSink<K>, false>(sm, d, p + t0, TILE, out, cursor, xf);
+                if (t0 < len)
+                    scatter_tile<K, T, U, LOG_KMAX, false, true, PeerSink<K>, false>(sm, d, p + t0, len - t0, out, cursor, xf);
             } else {
                 for (; t0 + TILE <= len; t0 += TILE)
                     scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
@@ -1141,14 +1157,27 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
     }
 }
 
-// Equal-key buckets that landed in the workspace: write the splitter value.
+// Equal-key buckets: write the splitter value (f^-1 of it) over the bucket.
 // The fill count is read on the device (written by the level's plan).
+// Buckets up to kFillWarp keys get a warp each (many small equal runs, e.g.
+// the exchange's equal-key shares); larger ones the whole grid in turn.
 template <class K>
 __global__ void fill_kernel(const FillTask* __restrict__ fills, const uint32_t* __restrict__ nfill,
-                            uint32_t fill_cap, K* __restrict__ dst, Xf xf = Xf{0, 0}) {
-    const uint32_t nf = min(*nfill, fill_cap);
-    for (uint32_t f = 0; f < nf; ++f) {
+                            const uint32_t* __restrict__ nfill_big, uint32_t fill_cap, K* __restrict__ dst,
+                            Xf xf = Xf{0, 0}) {
+    const uint32_t ns = min(*nfill, fill_cap / 2), nbig = min(*nfill_big, fill_cap / 2);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t f = gw; f < ns; f += nw) {
         const FillTask ft = fills[f];
+        K v;
+        memcpy(&v, ft.value, sizeof(K));
+        v = xf_inv(v, xf);
+        for (uint64_t i = lane; i < ft.len; i += 32) dst[ft.off + i] = v;
+    }
+    for (uint32_t f = 0; f < nbig; ++f) {
+        const FillTask ft = fills[fill_cap - 1 - f];
         K v;
         memcpy(&v, ft.value, sizeof(K));
         v = xf_inv(v, xf);

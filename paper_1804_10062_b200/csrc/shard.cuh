@@ -23,6 +23,13 @@
 //      mappings across processes) -- the exchange IS the partition's scatter;
 //   6. each rank sorts its received keys into its output (out of place,
 //      transform fused) between its lower and upper fill.
+// Folded form (the default of both drivers): step 2 picks P * K0 - 1
+// splitters, K0 per rank, and the exchange scatter of step 5 IS level 0 of
+// every rank's local sort -- each receive buffer is the B half of that rank's
+// sort workspace, holding its K0 sub-buckets at their final offsets (core
+// keys), and every equal-key run is a fill -- so the local sort starts at
+// level 1 (shard_plan_folded_host, shard_finish_presplit): 8 n w of HBM per
+// rank instead of 11 n w.
 // Rank r's output is the r-th slice of the global order.  The reference has
 // no distributed sort (single-threaded); the algorithm is the
 // north star's "global splitter selection, one all-to-all, local sorts".
@@ -70,22 +77,61 @@ static int dispatch_sample(int dt, int cmp, const void* d, size_t n, size_t s, u
     return QMSORT_OK;
 }
 
+// The local sort of a folded sharded exchange: the n keys (core keys,
+// grouped into the three-way bins of uniq / counts) sit in the B half of the
+// workspace ws (offset 0 of make_layout); the sorted caller-dtype keys land in
+// d, fills included.
+static int sort_presplit_device(int dt, int cmp, void* d, size_t n, const void* d_uniq, uint32_t m,
+                                const uint64_t* counts, const qmsort_gpu_config* cfgp, void* wsp, size_t ws_bytes,
+                                qmsort_gpu_metrics* mt, cudaStream_t st) {
+    QTRY(validate(dt, cmp, n, d));
+    if (m && !d_uniq) return fail(QMSORT_EINVAL, "null splitters");
+    qmsort_gpu_config tmp;
+    const qmsort_gpu_config& cfg = cfg_or_default(cfgp, tmp);
+    const size_t nn = std::max<size_t>(n, 2);
+    CallFrame f(st);
+    if (!wsp || ws_bytes < ws_bytes_for(dt, nn)) return fail(QMSORT_ENOWS, "presplit: workspace too small");
+    QTRY(f.begin(cfg, wsp, ws_bytes, ws_bytes_for(dt, nn)));
+    unsigned char* w = static_cast<unsigned char*>(f.ws);
+    const Xf xf = make_xf(dt, cmp);
+    int rc = QMSORT_OK;
+    if (n > 0) {
+        switch (core_dtype(dt)) {
+#define QPRE(K)                                                                                             \
+    {                                                                                                       \
+        const WsLayout L = make_layout<K>(nn);                                                              \
+        const Presplit<K> pre{static_cast<const K*>(d_uniq), m, counts};                                    \
+        rc = samplesort<K>(static_cast<K*>(d), reinterpret_cast<K*>(w + L.b_off), n, cfg, w, L, st, f.led,  \
+                           xf, nullptr, &pre);                                                              \
+        break;                                                                                              \
+    }
+            case QMSORT_DT_U32: QPRE(uint32_t)
+            case QMSORT_DT_U64: QPRE(uint64_t)
+            case QMSORT_DT_REC32: QPRE(Rec32)
+#undef QPRE
+        }
+    }
+    return f.end(rc, mt);
+}
+
 // Sample seed of rank r (the same on every path).
 static uint64_t shard_seed(uint64_t seed, uint32_t r) { return seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(r + 1)); }
 
-// Host: P-1 splitters at sample ranks ((i+1) m) / P of the sorted sample,
-// merged into distinct values (byte equality of core keys = key equality).
-static int shard_splitters_host(int core, const void* sorted, size_t m, uint32_t P, void* uniq,
+// Host: the splitters at sample ranks ((i+1) m) / nbuckets of the sorted
+// sample, merged into distinct values (byte equality of core keys = key
+// equality) with their multiplicities.
+// nbuckets - 1 splitters (P for the plain exchange, P * K0 folded).
+static int shard_splitters_host(int core, const void* sorted, size_t m, uint32_t nbuckets, void* uniq,
                                 uint32_t* mult, uint32_t* nuniq) {
     const size_t w = dtype_size(core);
     if (w == 0 || core != core_dtype(core)) return fail(QMSORT_EINVAL, "splitters expect a core dtype");
-    if (P < 1 || P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
-    if (m < P) return fail(QMSORT_EINVAL, "sample smaller than the rank count");
+    if (nbuckets < 1 || nbuckets > (uint32_t)(kMaxPeerBins / 2)) return fail(QMSORT_EINVAL, "1 <= buckets <= 512");
+    if (m < nbuckets) return fail(QMSORT_EINVAL, "sample smaller than the bucket count");
     const unsigned char* s = static_cast<const unsigned char*>(sorted);
     unsigned char* u = static_cast<unsigned char*>(uniq);
     uint32_t k = 0;
-    for (uint32_t i = 0; i + 1 < P; ++i) {
-        const unsigned char* v = s + ((uint64_t)(i + 1) * m / P) * w;
+    for (uint32_t i = 0; i + 1 < nbuckets; ++i) {
+        const unsigned char* v = s + ((uint64_t)(i + 1) * m / nbuckets) * w;
         if (k > 0 && std::memcmp(u + (k - 1) * w, v, w) == 0) {
             ++mult[k - 1];
         } else {
@@ -150,13 +196,160 @@ static int shard_plan_host(uint32_t P, uint32_t m, const uint32_t* mult, const u
     return QMSORT_OK;
 }
 
+// Sub-buckets per rank of the folded exchange.  The exchange's bucket count
+// P * K0 starts at 256 -- an exchange tile writes runs of ~TILE / (P K0)
+// keys per bucket, and 512-way runs measured 1.5x slower than 256-way (C2 at
+// P = 1: 1.50 ms against 0.99 ms) -- and doubles (up to 2^LOGKMAX) only while
+// a sub-bucket of n_total / (P K0) keys would need more than one further
+// partition level (C3 at P = 1: 2^30 uint64 keys in 256 sub-buckets need two
+// local levels, 45.0 ms; in 512, one, 37.3 ms).
+template <class K>
+static uint32_t shard_subbuckets_t(uint32_t P, uint64_t n_total) {
+    using TU = Tune<K>;
+    constexpr uint64_t cap = class_cap<K>(kNumClasses - 1);
+    const uint64_t one_level = (cap * 3 / 4) << TU::LOGKMAX;  // choose_logk's single-level bound
+    const uint32_t kmax = 1u << TU::LOGKMAX;
+    uint32_t k0 = 1;
+    while (P * k0 * 2 <= std::min<uint32_t>(kmax, 256)) k0 *= 2;
+    while (P * k0 * 2 <= kmax && n_total > one_level * P * k0) k0 *= 2;
+    return k0;
+}
+static uint32_t shard_subbuckets(int dt, uint32_t P, uint64_t n_total) {
+    switch (core_dtype(dt)) {
+        case QMSORT_DT_U32: return shard_subbuckets_t<uint32_t>(P, n_total);
+        case QMSORT_DT_U64: return shard_subbuckets_t<uint64_t>(P, n_total);
+        case QMSORT_DT_REC32: return shard_subbuckets_t<Rec32>(P, n_total);
+    }
+    return 1;
+}
+
+// Host: the folded plan from the P x (2M+1) count matrix of the P*K0 - 1
+// global splitters (M distinct values u_j, multiplicities c_j; p_j = number
+// of splitters below u_j).  Rank r takes the splitter indices [r K0, (r+1) K0):
+// the open bin O_j goes to rank floor(p_j / K0); the keys equal to u_j go to
+// the ranks floor(p_j / K0) .. floor((p_j + c_j) / K0), in even shares, as
+// fills (never sent).  Every rank's slice is then a three-way bin list of its
+// own -- local distinct values loc_uniq (indices into u) with loc_m entries
+// and 2 loc_m + 1 bin counts loc_cnt (open, equal, open, ... , open) -- the
+// level-0 result of its local sort.  bin_off[s][b]: where sender s's open
+// bin b starts in its rank's buffer (that bin's local offset plus the
+// earlier senders' parts).  LM = K0 + 1 local values at most.
+static int shard_plan_folded_host(uint32_t P, uint32_t K0, uint32_t M, const uint32_t* mult, const uint64_t* C,
+                                  int32_t* bin_rank, uint64_t* bin_off, uint64_t* out_n, uint32_t* loc_m,
+                                  int32_t* loc_uniq, uint64_t* loc_cnt) {
+    if (P < 1 || P > (uint32_t)kMaxPeers || K0 < 1) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks, K0 >= 1");
+    const uint32_t nb = 2 * M + 1, LM = K0 + 1, LB = 2 * LM + 1;
+    if (nb > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
+    uint64_t S = 0;
+    std::vector<uint64_t> pj(M + 1, 0);
+    for (uint32_t j = 0; j < M; ++j) {
+        if (mult[j] == 0) return fail(QMSORT_EINVAL, "splitter multiplicity 0");
+        pj[j] = S;
+        S += mult[j];
+    }
+    pj[M] = S;
+    if (S != (uint64_t)P * K0 - 1) return fail(QMSORT_EINVAL, "splitter multiplicities must sum to P*K0-1");
+    auto rank_of_open = [&](uint32_t j) { return (uint32_t)std::min<uint64_t>(P - 1, pj[j] / K0); };
+    std::vector<uint64_t> tot(nb, 0);
+    for (uint32_t s = 0; s < P; ++s)
+        for (uint32_t b = 0; b < nb; ++b) tot[b] += C[(size_t)s * nb + b];
+    std::vector<int32_t> open_local(M + 1, -1);  // local bin index of global open bin j (in its rank)
+    for (uint32_t r = 0; r < P; ++r) {
+        uint32_t k = 0;  // local distinct values so far; the current open bin is 2k
+        uint64_t* cnt = loc_cnt + (size_t)r * LB;
+        for (uint32_t i = 0; i < LB; ++i) cnt[i] = 0;
+        for (uint32_t j = 0; j <= M; ++j) {
+            if (rank_of_open(j) == r) {
+                cnt[2 * k] += tot[2 * j];
+                open_local[j] = (int32_t)(2 * k);
+            }
+            if (j == M) break;
+            const uint32_t lo = rank_of_open(j), hi = rank_of_open(j + 1);
+            if (lo <= r && r <= hi) {
+                if (k >= LM) return fail(QMSORT_EINTERNAL, "folded plan: too many local values");
+                const uint64_t e = tot[2 * j + 1], parts = hi - lo + 1, i = r - lo;
+                loc_uniq[(size_t)r * LM + k] = (int32_t)j;
+                cnt[2 * k + 1] = e * (i + 1) / parts - e * i / parts;
+                ++k;
+            }
+        }
+        loc_m[r] = k;
+        uint64_t n = 0;
+        for (uint32_t i = 0; i < 2 * k + 1; ++i) n += cnt[i];
+        out_n[r] = n;
+    }
+    // sender offsets: open bin j at its local bin's start in rank r, senders in order
+    for (uint32_t j = 0; j <= M; ++j) {
+        const uint32_t r = rank_of_open(j);
+        bin_rank[2 * j] = (int32_t)r;
+        if (j < M) bin_rank[2 * j + 1] = -1;
+        uint64_t start = 0;
+        const uint64_t* cnt = loc_cnt + (size_t)r * LB;
+        for (int32_t i = 0; i < open_local[j]; ++i) start += cnt[i];
+        for (uint32_t s = 0; s < P; ++s) {
+            bin_off[(size_t)s * nb + 2 * j] = start;
+            start += C[(size_t)s * nb + 2 * j];
+            if (j < M) bin_off[(size_t)s * nb + 2 * j + 1] = 0;
+        }
+    }
+    return QMSORT_OK;
+}
+
 // Partition workspace of one rank's count + scatter (the plan stays in it).
 static size_t shard_ws_bytes(int dt, size_t n) { return ws_bytes_for(dt, std::max<size_t>(n, 2)); }
 
-// Count (parts 1) or scatter to peers (parts 2) of one rank's n caller keys.
+// Where one sender's bins go (host side of PeerArgs): bin b of the 2 nuniq + 1
+// three-way bins -> rank bin_rank[b] (-1: not sent) at offset bin_off[b] of
+// that rank's buffer rank_dest[r], which holds recv_n[r] keys.
+struct ShardRoute {
+    const int32_t* bin_rank;
+    const uint64_t* bin_off;
+    void* const* rank_dest;
+    const uint64_t* recv_n;
+    uint32_t P;
+    bool raw;  // ship the caller's keys (else core keys)
+};
+
+// PeerArgs from a route: the ranks' virtual bases and every bin's first
+// virtual position for this sender, copied into the workspace's misc area.
+// three_way = false: the classifier's bin j is the route's open bin 2j (the
+// splitters are distinct, so the keys equal to one go with the open bin below
+// it -- the same rank; nothing is filled).
+static int make_peer_args(uint32_t nbins, bool three_way, const ShardRoute& rt, size_t n_sender,
+                          uint32_t* d_bin_base, cudaStream_t st, PeerArgs* pa) {
+    if (rt.P < 1 || rt.P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
+    if (nbins > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
+    *pa = PeerArgs{};
+    pa->nranks = rt.P;
+    pa->raw = rt.raw ? 1u : 0u;
+    uint64_t v = 0;
+    for (uint32_t r = 0; r < rt.P; ++r) {
+        pa->dest[r] = reinterpret_cast<unsigned long long>(rt.rank_dest[r]);
+        pa->vbase[r] = (uint32_t)v;
+        v += rt.recv_n[r];
+    }
+    for (uint32_t r = rt.P; r <= (uint32_t)kMaxPeers; ++r) pa->vbase[r] = (uint32_t)v;
+    if (v + n_sender >= (1ull << 32)) return fail(QMSORT_EINVAL, "the exchange moves >= 2^32 keys");
+    uint32_t base[kMaxPeerBins];
+    for (uint32_t b = 0; b < (uint32_t)kMaxPeerBins; ++b) base[b] = (uint32_t)v;  // empty / not-sent bins
+    for (uint32_t b = 0; b < nbins; ++b) {
+        const int32_t r = rt.bin_rank[b];
+        if (r >= (int32_t)rt.P) return fail(QMSORT_EINVAL, "bin routed to a rank >= P");
+        if (r < 0) continue;
+        if (!three_way && (b & 1)) continue;  // two-way: no equal bins (their counts are 0)
+        if (rt.rank_dest[r] == nullptr) return fail(QMSORT_EINVAL, "null receive buffer");
+        base[three_way ? b : b / 2] = pa->vbase[r] + (uint32_t)rt.bin_off[b];
+    }
+    QCK(cudaMemcpyAsync(d_bin_base, base, sizeof(base), cudaMemcpyHostToDevice, st));
+    pa->bin_base = d_bin_base;
+    return QMSORT_OK;
+}
+
+// Count (parts 1) or scatter to the route (parts 2) of one rank's n caller keys.
+// three_way = false (distinct splitters): two-way bins, nuniq + 1 counts.
 static int shard_partition(int dt, int cmp, const void* d_in, size_t n, const void* uniq, uint32_t nuniq,
                            uint64_t* counts, void* ws, size_t ws_bytes, cudaStream_t st, int parts,
-                           const PeerArgs* peers, Ledger& led) {
+                           const ShardRoute* route, Ledger& led, bool three_way = true) {
     QTRY(validate(dt, cmp, n, d_in));
     if (2 * nuniq + 1 > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
     if (!ws) return fail(QMSORT_EINVAL, "the shard partition needs a caller workspace");
@@ -164,36 +357,30 @@ static int shard_partition(int dt, int cmp, const void* d_in, size_t n, const vo
     if (ws_bytes < shard_ws_bytes(dt, n)) return fail(QMSORT_ENOWS, "shard workspace too small");
     unsigned char* w = static_cast<unsigned char*>(ws);
     const Xf xf = make_xf(dt, cmp);
+    PeerArgs pa{};
+    const PeerArgs* peers = nullptr;
+    if (route) {
+        size_t misc = 0;
+        switch (core_dtype(dt)) {
+            case QMSORT_DT_U32: misc = make_layout<uint32_t>(nn).misc_off; break;
+            case QMSORT_DT_U64: misc = make_layout<uint64_t>(nn).misc_off; break;
+            case QMSORT_DT_REC32: misc = make_layout<Rec32>(nn).misc_off; break;
+        }
+        QTRY(make_peer_args(2 * nuniq + 1, three_way, *route, n, reinterpret_cast<uint32_t*>(w + misc), st, &pa));
+        peers = &pa;
+    }
     switch (core_dtype(dt)) {
         case QMSORT_DT_U32:
             return partition_given<uint32_t>((const uint32_t*)d_in, n, (const uint32_t*)uniq, nuniq, nullptr, counts,
-                                             w, make_layout<uint32_t>(nn), st, led, parts, peers, true, xf);
+                                             w, make_layout<uint32_t>(nn), st, led, parts, peers, three_way, xf);
         case QMSORT_DT_U64:
             return partition_given<uint64_t>((const uint64_t*)d_in, n, (const uint64_t*)uniq, nuniq, nullptr, counts,
-                                             w, make_layout<uint64_t>(nn), st, led, parts, peers, true, xf);
+                                             w, make_layout<uint64_t>(nn), st, led, parts, peers, three_way, xf);
         case QMSORT_DT_REC32:
             return partition_given<Rec32>((const Rec32*)d_in, n, (const Rec32*)uniq, nuniq, nullptr, counts, w,
-                                          make_layout<Rec32>(nn), st, led, parts, peers, true, xf);
+                                          make_layout<Rec32>(nn), st, led, parts, peers, three_way, xf);
     }
     return fail(QMSORT_EINVAL, "unknown dtype");
-}
-
-static int make_peer_args(uint32_t nuniq, const int32_t* bin_rank, const uint64_t* bin_off,
-                          void* const* rank_dest, uint32_t P, PeerArgs* pa) {
-    if (P < 1 || P > (uint32_t)kMaxPeers) return fail(QMSORT_EINVAL, "1 <= P <= 8 ranks");
-    const uint32_t nb = 2 * nuniq + 1;
-    if (nb > (uint32_t)kMaxPeerBins) return fail(QMSORT_EINVAL, "too many splitters");
-    *pa = PeerArgs{};
-    pa->nbins = nb;
-    for (uint32_t r = 0; r < P; ++r) pa->dest[r] = reinterpret_cast<unsigned long long>(rank_dest[r]);
-    for (uint32_t b = 0; b < nb; ++b) {
-        if (bin_rank[b] >= (int32_t)P) return fail(QMSORT_EINVAL, "bin routed to a rank >= P");
-        pa->bin_rank[b] = (signed char)(bin_rank[b] < 0 ? -1 : bin_rank[b]);
-        pa->bin_off[b] = bin_off[b];
-        if (bin_rank[b] >= 0 && rank_dest[bin_rank[b]] == nullptr)
-            return fail(QMSORT_EINVAL, "null receive buffer");
-    }
-    return QMSORT_OK;
 }
 
 // One rank's output: [lo fill | sorted received keys | hi fill], the received
@@ -286,7 +473,9 @@ static int sort_sharded_sp(int dt, int cmp, uint32_t P, const int* devices, cons
             if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) QCK(e);
             cudaGetLastError();  // clear "already enabled"
         }
-    const uint32_t s = 64 * P;  // samples per rank (oversampling 64 per rank)
+    const uint32_t K0 = shard_subbuckets(dt, P, total);  // folded exchange: K0 sub-buckets per rank
+    const uint32_t LM = K0 + 1;                   // local distinct splitters per rank, at most
+    const uint32_t s = std::max(64 * P, 32 * K0);  // samples per rank: >= 32 per global bucket
     std::vector<ShardRank> R(P);
     uint32_t launches = 0;
     uint64_t alg = 0;
@@ -314,7 +503,7 @@ static int sort_sharded_sp(int dt, int cmp, uint32_t P, const int* devices, cons
         QCK(cudaEventCreateWithFlags(&x.scattered, cudaEventDisableTiming));
         QCK(cudaEventCreateWithFlags(&x.ready, cudaEventDisableTiming));
         QCK(cudaMalloc(&x.smp, (size_t)s * P * w));
-        QCK(cudaMalloc(&x.uniq, kMaxPeers * w));
+        QCK(cudaMalloc(&x.uniq, (size_t)(kMaxPeerBins / 2 + LM) * w));  // global | local distinct splitters
         QCK(cudaMalloc(&x.counts, kMaxPeerBins * sizeof(uint64_t)));
         x.pws_bytes = shard_ws_bytes(dt, n_in[r]);
         QCK(cudaMalloc(&x.pws, x.pws_bytes));
@@ -347,58 +536,74 @@ static int sort_sharded_sp(int dt, int cmp, uint32_t P, const int* devices, cons
         QCK(cudaMemcpyAsync(smp_h.data(), R[0].smp, smp_h.size(), cudaMemcpyDeviceToHost, R[0].st));
         QCK(cudaStreamSynchronize(R[0].st));
     }
-    // 2. splitters (host), to every device
-    unsigned char uniq_h[kMaxPeers * 32];
-    uint32_t mult[kMaxPeers] = {}, nuniq = 0;
-    QTRY(shard_splitters_host(core, smp_h.data(), (size_t)s * P, P, uniq_h, mult, &nuniq));
+    // 2. the P*K0 - 1 global splitters (host), to every device
+    std::vector<unsigned char> uniq_h((size_t)(kMaxPeerBins / 2) * w);
+    std::vector<uint32_t> mult(kMaxPeerBins / 2, 0);
+    uint32_t nuniq = 0;
+    QTRY(shard_splitters_host(core, smp_h.data(), (size_t)s * P, P * K0, uniq_h.data(), mult.data(), &nuniq));
     const uint32_t nb = 2 * nuniq + 1;
-    // 3. three-way counts of every rank
-    std::vector<uint64_t> C((size_t)P * nb, 0);
+    // 3. counts of every rank: three-way when a splitter value repeats (its
+    // equal keys are spread as fills), else two-way (cheaper; no equal bins)
+    bool three_way = false;
+    for (uint32_t j = 0; j < nuniq; ++j) three_way |= mult[j] > 1;
+    const uint32_t ncnt = three_way ? nb : nuniq + 1;
+    std::vector<uint64_t> C((size_t)P * nb, 0), C2((size_t)P * ncnt, 0);
     for (uint32_t r = 0; r < P; ++r) {
         ShardRank& x = R[r];
         QCK(cudaSetDevice(x.dev));
-        if (nuniq) QCK(cudaMemcpyAsync(x.uniq, uniq_h, nuniq * w, cudaMemcpyHostToDevice, x.st));
+        if (nuniq) QCK(cudaMemcpyAsync(x.uniq, uniq_h.data(), nuniq * w, cudaMemcpyHostToDevice, x.st));
         Ledger led;
         QTRY(shard_partition(dt, cmp, d_in[r], n_in[r], x.uniq, nuniq, (uint64_t*)x.counts, x.pws, x.pws_bytes,
-                             x.st, 1, nullptr, led));
+                             x.st, 1, nullptr, led, three_way));
         launches += led.launches;
         alg += led.alg_bytes;
-        QCK(cudaMemcpyAsync(&C[(size_t)r * nb], x.counts, nb * sizeof(uint64_t), cudaMemcpyDeviceToHost, x.st));
+        QCK(cudaMemcpyAsync(&C2[(size_t)r * ncnt], x.counts, ncnt * sizeof(uint64_t), cudaMemcpyDeviceToHost, x.st));
     }
     for (uint32_t r = 0; r < P; ++r) {
         QCK(cudaSetDevice(R[r].dev));
         QCK(cudaStreamSynchronize(R[r].st));
     }
-    // 4. the plan (host, identical for every rank)
-    int32_t bin_rank[kMaxPeerBins];
-    std::vector<uint64_t> bin_off((size_t)P * nb);
-    uint64_t recv_n[kMaxPeers], lo_fill[kMaxPeers], hi_fill[kMaxPeers];
-    int32_t lo_val[kMaxPeers], hi_val[kMaxPeers];
-    QTRY(shard_plan_host(P, nuniq, mult, C.data(), bin_rank, bin_off.data(), recv_n, lo_fill, hi_fill, lo_val,
-                         hi_val));
+    for (uint32_t r = 0; r < P; ++r)  // as three-way bins (two-way: bin j = open bin 2j)
+        for (uint32_t b = 0; b < ncnt; ++b) C[(size_t)r * nb + (three_way ? b : 2 * b)] = C2[(size_t)r * ncnt + b];
+    // 4. the folded plan (host, identical for every rank)
+    std::vector<int32_t> bin_rank(nb);
+    std::vector<uint64_t> bin_off((size_t)P * nb), recv_n(P), loc_cnt((size_t)P * (2 * LM + 1));
+    std::vector<uint32_t> loc_m(P);
+    std::vector<int32_t> loc_uniq((size_t)P * LM);
+    QTRY(shard_plan_folded_host(P, K0, nuniq, mult.data(), C.data(), bin_rank.data(), bin_off.data(), recv_n.data(),
+                                loc_m.data(), loc_uniq.data(), loc_cnt.data()));
     bool fits = true;
     for (uint32_t r = 0; r < P; ++r) {
-        out_n[r] = recv_n[r] + lo_fill[r] + hi_fill[r];
+        out_n[r] = recv_n[r];
         if (out_n[r] > out_cap[r]) fits = false;
         if (out_n[r] > 0 && d_out[r] == nullptr) return fail(QMSORT_EINVAL, "null output buffer");
     }
     if (!fits) return fail(QMSORT_ENOWS, "an output buffer is smaller than its slice (see out_n)");
-    // receive buffers, then 5. every rank's scatter stores into the peers' buffers
+    // every rank's local-sort workspace is its receive buffer (its B half),
+    // and its local distinct splitters go next to the global ones
     std::vector<void*> dest(P, nullptr);
     for (uint32_t r = 0; r < P; ++r) {
         ShardRank& x = R[r];
         QCK(cudaSetDevice(x.dev));
-        QCK(cudaMalloc(&x.recv, std::max<uint64_t>(1, recv_n[r]) * w));
-        dest[r] = x.recv;
+        x.fws_bytes = ws_bytes_for(dt, std::max<uint64_t>(2, recv_n[r]));
+        QCK(cudaMalloc(&x.fws, x.fws_bytes));
+        dest[r] = x.fws;
+        std::vector<unsigned char> lu((size_t)LM * w);
+        for (uint32_t k = 0; k < loc_m[r]; ++k)
+            std::memcpy(&lu[(size_t)k * w], &uniq_h[(size_t)loc_uniq[(size_t)r * LM + k] * w], w);
+        if (loc_m[r])
+            QCK(cudaMemcpy(static_cast<unsigned char*>(x.uniq) + (size_t)(kMaxPeerBins / 2) * w, lu.data(),
+                           (size_t)loc_m[r] * w, cudaMemcpyHostToDevice));
     }
+    // 5. every rank's scatter stores its open bins into the peers' buffers:
+    // level 0 of their local sorts (core keys)
     for (uint32_t r = 0; r < P; ++r) {
         ShardRank& x = R[r];
         QCK(cudaSetDevice(x.dev));
-        PeerArgs pa;
-        QTRY(make_peer_args(nuniq, bin_rank, &bin_off[(size_t)r * nb], dest.data(), P, &pa));
+        const ShardRoute rt{bin_rank.data(), &bin_off[(size_t)r * nb], dest.data(), recv_n.data(), P, false};
         Ledger led;
-        QTRY(shard_partition(dt, cmp, d_in[r], n_in[r], x.uniq, nuniq, nullptr, x.pws, x.pws_bytes, x.st, 2, &pa,
-                             led));
+        QTRY(shard_partition(dt, cmp, d_in[r], n_in[r], x.uniq, nuniq, nullptr, x.pws, x.pws_bytes, x.st, 2, &rt,
+                             led, three_way));
         launches += led.launches;
         alg += led.alg_bytes;
         QCK(cudaEventRecord(x.scattered, x.st));
@@ -414,13 +619,11 @@ static int sort_sharded_sp(int dt, int cmp, uint32_t P, const int* devices, cons
             QCK(cudaSetDevice(x.dev));
             for (uint32_t q = 0; q < P; ++q)
                 if (q != r) QCK(cudaStreamWaitEvent(x.st, R[q].scattered, 0));
-            x.fws_bytes = ws_bytes_for(dt, std::max<uint64_t>(2, recv_n[r]));
-            QCK(cudaMallocAsync(&x.fws, x.fws_bytes, x.st));
             std::memset(&ms[r], 0, sizeof(ms[r]));
-            const int rc2 = shard_finish(dt, cmp, x.recv, recv_n[r], x.uniq, lo_val[r], lo_fill[r], hi_val[r],
-                                         hi_fill[r], d_out[r], &cfg, x.fws, x.fws_bytes, &ms[r], x.st);
-            cudaFreeAsync(x.fws, x.st);
-            x.fws = nullptr;
+            const int rc2 = sort_presplit_device(dt, cmp, d_out[r], recv_n[r],
+                                                 static_cast<unsigned char*>(x.uniq) + (size_t)(kMaxPeerBins / 2) * w,
+                                                 loc_m[r], &loc_cnt[(size_t)r * (2 * LM + 1)], &cfg, x.fws,
+                                                 x.fws_bytes, &ms[r], x.st);
             if (rc2 != QMSORT_OK) return rc2;
             QCK(cudaStreamSynchronize(x.st));
             return QMSORT_OK;

@@ -62,17 +62,25 @@ def wire(t, dt: int):
 # ---------------------------------------------------------------------------
 # host-only plan (C, no device work): identical on every rank
 # ---------------------------------------------------------------------------
-def splitters(core: int, sorted_sample: np.ndarray, P: int) -> tuple[np.ndarray, list]:
-    """P-1 quantile splitters of the sorted core-key sample, merged into
-    distinct values: (unique splitters as uint8 rows, multiplicities)."""
+MAX_BINS = 1024  # three-way bins of one exchange (kMaxPeerBins)
+
+
+def subbuckets(dt: int, P: int, n_total: int) -> int:
+    """K0: sub-buckets per rank of the folded exchange (qmsort_gpu_shard_subbuckets)."""
+    return int(_lib.load().qmsort_gpu_shard_subbuckets(dt, P, n_total))
+
+
+def splitters(core: int, sorted_sample: np.ndarray, nbuckets: int) -> tuple[np.ndarray, list]:
+    """nbuckets - 1 quantile splitters of the sorted core-key sample, merged
+    into distinct values: (unique splitters as uint8 rows, multiplicities)."""
     lib = _lib.load()
     w = KEY_BYTES[core]
     smp = np.ascontiguousarray(sorted_sample).view(np.uint8).reshape(-1)
     m = smp.shape[0] // w
-    uniq = np.zeros(MAX_RANKS * w, dtype=np.uint8)
-    mult = (ctypes.c_uint32 * MAX_RANKS)()
+    uniq = np.zeros(MAX_BINS // 2 * w, dtype=np.uint8)
+    mult = (ctypes.c_uint32 * (MAX_BINS // 2))()
     nu = ctypes.c_uint32(0)
-    _lib.check(lib.qmsort_gpu_shard_splitters(core, smp.ctypes.data, m, P, uniq.ctypes.data, mult,
+    _lib.check(lib.qmsort_gpu_shard_splitters(core, smp.ctypes.data, m, nbuckets, uniq.ctypes.data, mult,
                                               ctypes.byref(nu)), "qmsort_gpu_shard_splitters")
     k = int(nu.value)
     return uniq[:k * w].copy(), [int(mult[i]) for i in range(k)]
@@ -99,6 +107,37 @@ def plan(P: int, mult: Sequence[int], C: np.ndarray) -> dict:
     return {"bin_rank": bin_rank, "bin_off": bin_off, "recv_n": recv_n.astype(np.int64),
             "lo_fill": lo_fill.astype(np.int64), "hi_fill": hi_fill.astype(np.int64),
             "lo_val": lo_val, "hi_val": hi_val, "C": C.astype(np.int64)}
+
+
+def plan_folded(P: int, K0: int, mult: Sequence[int], C: np.ndarray) -> dict:
+    """The folded plan (qmsort_gpu_shard_plan_folded): every rank's slice as
+    the three-way bin list of its local sort's level 0."""
+    lib = _lib.load()
+    m = len(mult)
+    nb = 2 * m + 1
+    LM = K0 + 1
+    C = np.ascontiguousarray(np.asarray(C, dtype=np.uint64).reshape(P, nb))
+    u64p, i32p, u32p = (ctypes.POINTER(t) for t in (ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32))
+    bin_rank = np.zeros(nb, dtype=np.int32)
+    bin_off = np.zeros((P, nb), dtype=np.uint64)
+    out_n = np.zeros(P, dtype=np.uint64)
+    loc_m = np.zeros(P, dtype=np.uint32)
+    loc_uniq = np.zeros((P, LM), dtype=np.int32)
+    loc_cnt = np.zeros((P, 2 * LM + 1), dtype=np.uint64)
+    mu = (ctypes.c_uint32 * max(1, m))(*mult)
+    _lib.check(lib.qmsort_gpu_shard_plan_folded(P, K0, m, mu, C.ctypes.data_as(u64p), bin_rank.ctypes.data_as(i32p),
+                                                bin_off.ctypes.data_as(u64p), out_n.ctypes.data_as(u64p),
+                                                loc_m.ctypes.data_as(u32p), loc_uniq.ctypes.data_as(i32p),
+                                                loc_cnt.ctypes.data_as(u64p)), "qmsort_gpu_shard_plan_folded")
+    return {"bin_rank": bin_rank, "bin_off": bin_off, "out_n": out_n.astype(np.int64), "loc_m": loc_m,
+            "loc_uniq": loc_uniq, "loc_cnt": loc_cnt, "C": C.astype(np.int64)}
+
+
+def local_splitters(uniq_h: np.ndarray, w: int, pl: dict, r: int) -> np.ndarray:
+    """Rank r's local distinct splitters (uint8 rows) for its presplit sort."""
+    rows = uniq_h.reshape(-1, w)
+    k = int(pl["loc_m"][r])
+    return np.ascontiguousarray(rows[pl["loc_uniq"][r][:k]]).reshape(-1) if k else np.zeros(0, np.uint8)
 
 
 def staging_offsets(pl: dict, r: int) -> tuple[np.ndarray, list]:
@@ -177,19 +216,30 @@ class GpuOps:
         t = self.torch.from_numpy(np.ascontiguousarray(host_bytes)).to(like.device)
         return t
 
-    def count(self, t, dt: int, cmp: int, uniq, m: int):
-        counts = self.torch.zeros(2 * m + 1, dtype=self.torch.int64, device=t.device)
+    def count(self, t, dt: int, cmp: int, uniq, m: int, three_way: bool = True):
+        """Bin counts as three-way bins (2m + 1).  three_way = False (distinct
+        splitters): two-way classification, counted into the open bins 2j."""
+        torch = self.torch
+        nc = 2 * m + 1 if three_way else m + 1
+        counts = torch.zeros(nc, dtype=torch.int64, device=t.device)
         n = t.shape[0]
         ws = self._ws(self.lib.qmsort_gpu_shard_workspace_bytes(dt, n), t.device)
         _lib.check(self.lib.qmsort_gpu_shard_count(dt, cmp, t.data_ptr(), n, uniq.data_ptr() if m else None, m,
-                                                   counts.data_ptr(), ws.data_ptr(), ws.numel(), self._s()),
-                   "qmsort_gpu_shard_count")
+                                                   int(three_way), counts.data_ptr(), ws.data_ptr(), ws.numel(),
+                                                   self._s()), "qmsort_gpu_shard_count")
         self.alg_bytes += n * KEY_BYTES[dt]
-        return counts
+        if three_way:
+            return counts
+        full = torch.zeros(2 * m + 1, dtype=torch.int64, device=t.device)
+        full[0::2] = counts
+        return full
 
-    def scatter(self, t, dt: int, cmp: int, m: int, bin_rank, bin_off, dests: Sequence[Any]) -> None:
-        """Bin b of t (planned by count) -> dests[bin_rank[b]] + bin_off[b] keys.
-        dests: device pointers (ints, e.g. IPC-mapped peers) or tensors."""
+    def scatter(self, t, dt: int, cmp: int, m: int, bin_rank, bin_off, dests: Sequence[Any],
+                recv_n: Sequence[int], raw: bool = True, three_way: bool = True) -> None:
+        """Bin b of t (planned by count) -> dests[bin_rank[b]] + bin_off[b] keys;
+        rank r's buffer holds recv_n[r] keys.  dests: device pointers (ints,
+        e.g. IPC-mapped peers) or tensors.  raw: ship the caller's keys (else
+        core keys)."""
         n = t.shape[0]
         if not n:
             return
@@ -197,13 +247,44 @@ class GpuOps:
         nb = 2 * m + 1
         br = (ctypes.c_int32 * nb)(*[int(x) for x in bin_rank])
         bo = (ctypes.c_uint64 * nb)(*[int(x) for x in bin_off])
+        rn = (ctypes.c_uint64 * P)(*[int(x) for x in recv_n])
         # an empty receive buffer may report a null pointer; no key goes there
         d = (ctypes.c_void_p * P)(*[int(x) if isinstance(x, int) else (x.data_ptr() or t.data_ptr())
                                     for x in dests])
         ws = self.wsbuf
-        _lib.check(self.lib.qmsort_gpu_shard_scatter(dt, cmp, t.data_ptr(), n, m, br, bo, d, P, ws.data_ptr(),
-                                                     ws.numel(), self._s()), "qmsort_gpu_shard_scatter")
+        _lib.check(self.lib.qmsort_gpu_shard_scatter(dt, cmp, t.data_ptr(), n, m, int(three_way), br, bo, d, rn, P,
+                                                     int(raw),
+                                                     ws.data_ptr(), ws.numel(), self._s()),
+                   "qmsort_gpu_shard_scatter")
         self.alg_bytes += 2 * n * KEY_BYTES[dt]
+
+    def recv_workspace(self, n: int, dt: int, device):
+        """A receive buffer for the folded exchange: the workspace of the local
+        sort of n keys (its B half, offset 0, receives the keys)."""
+        nbytes = int(self.lib.qmsort_gpu_workspace_bytes(dt, max(2, n), None))
+        return self.torch.empty(nbytes, dtype=self.torch.uint8, device=device)
+
+    def finish_presplit(self, ws, n: int, dt: int, cmp: int, luniq, lm: int, lcnt, like, out=None):
+        """The local sort of a folded exchange: ws's B half holds the n core
+        keys at their level-0 offsets; returns the sorted slice (caller dtype)
+        -- in `out` (wire dtype, >= n rows) when given, else a fresh tensor."""
+        torch = self.torch
+        if out is None or out.shape[0] < n:
+            out = torch.empty((max(1, n),) + tuple(like.shape[1:]), dtype=like.dtype, device=like.device)
+        out = out[:n]
+        if n == 0:
+            return out
+        from . import SortConfig
+        c = SortConfig().to_c()
+        mt = _lib.GpuMetrics()
+        cnt = np.ascontiguousarray(np.asarray(lcnt[:2 * lm + 1], dtype=np.uint64))
+        _lib.check(self.lib.qmsort_gpu_shard_finish_presplit(
+            dt, cmp, out.data_ptr(), n, luniq.data_ptr() if lm else None, lm,
+            cnt.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(c), ws.data_ptr(), ws.numel(),
+            ctypes.byref(mt), self._s()), "qmsort_gpu_shard_finish_presplit")
+        self.launches += mt.kernel_launches
+        self.alg_bytes += mt.alg_bytes
+        return out
 
     def alloc(self, n: int, like):
         # never a null pointer, even for 0 keys (a peer's scatter is handed every buffer)
@@ -248,6 +329,11 @@ class TorchExchange:
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
 
+    def all_gather_object(self, obj) -> list:
+        out = [None] * self.P
+        self.dist.all_gather_object(out, obj, group=self.group)
+        return out
+
     def _cpu_group(self) -> bool:
         return self.dist.get_backend(self.group) == "gloo"
 
@@ -277,7 +363,7 @@ class PeerExchange(TorchExchange):
     every call returns a fresh output tensor (the local sort reads the
     receive buffer out of place)."""
 
-    fused = True
+    fused = True  # the folded exchange: the receive buffer is the local sort's workspace
 
     def __init__(self, group: Any = None):
         super().__init__(group)
@@ -344,9 +430,11 @@ def _np_rows(t) -> np.ndarray:
 
 
 def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchange: Any = None,
-                 ops: Any = None, oversample: int = 64, seed: int = 42):
+                 ops: Any = None, oversample: int = 64, seed: int = 42, out: Any = None):
     """Globally sort the keys held by all ranks; returns this rank's slice
-    (a fresh tensor of the caller's dtype).  ``local`` is only read."""
+    (of the caller's dtype): a view of ``out`` when that has room for it
+    (e.g. a buffer reused across calls), else a fresh tensor.  ``local`` is
+    only read."""
     from . import _cmp_code, dtype_of
     dt = dtype_of(local) if dtype is None else dtype
     core = CORE[dt]
@@ -356,32 +444,52 @@ def sort_sharded(local, less: Any = "less", *, dtype: int | None = None, exchang
     P, r = ex.P, ex.rank
     if P > MAX_RANKS:
         raise ValueError(f"at most {MAX_RANKS} ranks")
-    s = oversample * P
+    w = KEY_BYTES[dt]
+    wl = wire(local, dt)
+    folded = getattr(ex, "fused", False)
+    n_total = int(local.shape[0])
+    if folded and P > 1:  # every rank's size (one small all-gather of a tensor)
+        import torch
+        sz = torch.tensor([int(local.shape[0])], dtype=torch.int64,
+                          device=local.device if local.is_cuda else "cpu")
+        n_total = int(ex.all_gather(sz).sum().item())
+    K0 = subbuckets(dt, P, n_total) if folded else 1
+    s = max(oversample * P, 32 * K0)
     smp = _pad_sample(ops.sample(local, dt, cmp, s, rank_seed(seed, r)), s, local)
     all_smp = ex.all_gather(smp).contiguous()
     if all_smp.device != local.device:
         all_smp = all_smp.to(local.device)
     ops.sort_core(all_smp, core)
-    uniq_h, mult = splitters(core, _np_rows(all_smp), P)
+    uniq_h, mult = splitters(core, _np_rows(all_smp), P * K0)
     m = len(mult)
     uniq = ops.put(uniq_h, local)
-    counts = ops.count(local, dt, cmp, uniq, m)
+    tw = any(c > 1 for c in mult)  # a repeated splitter value: its equal keys become fills
+    counts = ops.count(local, dt, cmp, uniq, m, tw)
     C = _np_rows(ex.all_gather(counts)).reshape(P, 2 * m + 1)
-    pl = plan(P, mult, C)
-    w = KEY_BYTES[dt]
-    wl = wire(local, dt)
-    n_recv = int(pl["recv_n"][r])
-    if getattr(ex, "fused", False):
-        ex.ensure_capacity(int(pl["recv_n"].max()) * w, local.device)
-        ex.barrier(ops)  # every receiver is done reading its buffer and holds the handles
-        ops.scatter(local, dt, cmp, m, pl["bin_rank"], pl["bin_off"][r], ex.ptrs)
+    if folded:
+        # the exchange scatter is level 0 of every rank's local sort: core keys
+        # straight into the B half of the receivers' sort workspaces
+        pl = plan_folded(P, K0, mult, C)
+        n_out = int(pl["out_n"][r])
+        need = int(ops.lib.qmsort_gpu_workspace_bytes(dt, max(2, n_out), None))
+        ex.ensure_capacity(need, local.device)
+        ex.barrier(ops)  # every receiver is done with its buffer and holds the handles
+        ops.scatter(local, dt, cmp, m, pl["bin_rank"], pl["bin_off"][r], ex.ptrs, pl["out_n"], raw=False,
+                    three_way=tw)
         ex.barrier(ops)  # every sender's stores into this rank's buffer have landed
-        recv = ex.recv[: n_recv * w].view(wl.dtype).view((n_recv,) + tuple(wl.shape[1:]))
-    else:
-        off, send = staging_offsets(pl, r)
-        staging = ops.alloc(local.shape[0], wl)
-        ops.scatter(local, dt, cmp, m, pl["bin_rank"], off, [staging] * P)
-        recv = ex.all_to_all_v(staging, send, recv_counts(pl, r)).contiguous()
+        luniq = ops.put(local_splitters(uniq_h, w, pl, r), local)
+        res = ops.finish_presplit(ex.recv, n_out, dt, cmp, luniq, int(pl["loc_m"][r]), pl["loc_cnt"][r], wl,
+                                  out=None if out is None else wire(out, dt))
+        return res.view(local.dtype)
+    # plain exchange (the NCCL baseline): local staging grouped by rank, one
+    # all-to-all, then the out-of-place local sort between the fills
+    pl = plan(P, mult, C)
+    n_recv = int(pl["recv_n"][r])
+    off, send = staging_offsets(pl, r)
+    staging = ops.alloc(local.shape[0], wl)
+    ops.scatter(local, dt, cmp, m, pl["bin_rank"], off, [staging] * P, [local.shape[0]] * P, raw=True,
+                three_way=tw)
+    recv = ex.all_to_all_v(staging, send, recv_counts(pl, r)).contiguous()
     out = ops.finish(recv, n_recv, dt, cmp, uniq, int(pl["lo_val"][r]), int(pl["lo_fill"][r]),
                      int(pl["hi_val"][r]), int(pl["hi_fill"][r]), wl)
     return out.view(local.dtype)
@@ -409,35 +517,43 @@ def _emulated(shards, less, dtype, opss, oversample, seed, fused):
     core = CORE[dt]
     cmp = _cmp_code(less)
     P = len(shards)
+    w = KEY_BYTES[dt]
     wl = [wire(t, dt) for t in shards]
-    s = oversample * P
+    K0 = subbuckets(dt, P, sum(int(t.shape[0]) for t in shards)) if fused else 1
+    s = max(oversample * P, 32 * K0)
     smps = [_pad_sample(opss[r].sample(t, dt, cmp, s, rank_seed(seed, r)), s, t) for r, t in enumerate(shards)]
     all_smp = torch.cat(smps).contiguous()
     opss[0].sort_core(all_smp, core)
-    uniq_h, mult = splitters(core, _np_rows(all_smp), P)
+    uniq_h, mult = splitters(core, _np_rows(all_smp), P * K0)
     m = len(mult)
     uniqs = [opss[r].put(uniq_h, t) for r, t in enumerate(shards)]
-    C = np.stack([_np_rows(opss[r].count(t, dt, cmp, uniqs[r], m)) for r, t in enumerate(shards)])
-    pl = plan(P, mult, C)
-    if fused:
-        recvs = [opss[j].alloc(int(pl["recv_n"][j]), wl[j]) for j in range(P)]
-        for r, t in enumerate(shards):  # ops[r] still holds rank r's plan in its workspace
-            opss[r].scatter(t, dt, cmp, m, pl["bin_rank"], pl["bin_off"][r], recvs)
-    else:
-        stagings, sends = [], []
-        for r, t in enumerate(shards):
-            off, send = staging_offsets(pl, r)
-            st = opss[r].alloc(t.shape[0], wl[r])
-            opss[r].scatter(t, dt, cmp, m, pl["bin_rank"], off, [st] * P)
-            stagings.append(st)
-            sends.append(np.concatenate([[0], np.cumsum(send)]).astype(np.int64))
-        recvs = []
-        for j in range(P):  # rank j receives, in sender order, what each sender grouped for it
-            pieces = [stagings[r][int(sends[r][j]):int(sends[r][j + 1])] for r in range(P)]
-            recvs.append(torch.cat(pieces).contiguous() if pieces else opss[j].alloc(0, wl[j]))
+    tw = any(c > 1 for c in mult)
+    C = np.stack([_np_rows(opss[r].count(t, dt, cmp, uniqs[r], m, tw)) for r, t in enumerate(shards)])
     out = []
-    for j in range(P):
-        o = opss[j].finish(recvs[j], int(pl["recv_n"][j]), dt, cmp, uniqs[j], int(pl["lo_val"][j]),
+    if fused:  # folded: the receive buffers are the local sorts' workspaces
+        pl = plan_folded(P, K0, mult, C)
+        wss = [opss[j].recv_workspace(int(pl["out_n"][j]), dt, shards[j].device) for j in range(P)]
+        for r, t in enumerate(shards):  # ops[r] still holds rank r's plan in its workspace
+            opss[r].scatter(t, dt, cmp, m, pl["bin_rank"], pl["bin_off"][r], wss, pl["out_n"], raw=False,
+                            three_way=tw)
+        for j in range(P):
+            luniq = opss[j].put(local_splitters(uniq_h, w, pl, j), shards[j])
+            o = opss[j].finish_presplit(wss[j], int(pl["out_n"][j]), dt, cmp, luniq, int(pl["loc_m"][j]),
+                                        pl["loc_cnt"][j], wl[j])
+            out.append(o.view(shards[j].dtype))
+        return out
+    pl = plan(P, mult, C)
+    stagings, sends = [], []
+    for r, t in enumerate(shards):
+        off, send = staging_offsets(pl, r)
+        st = opss[r].alloc(t.shape[0], wl[r])
+        opss[r].scatter(t, dt, cmp, m, pl["bin_rank"], off, [st] * P, [t.shape[0]] * P, raw=True, three_way=tw)
+        stagings.append(st)
+        sends.append(np.concatenate([[0], np.cumsum(send)]).astype(np.int64))
+    for j in range(P):  # rank j receives, in sender order, what each sender grouped for it
+        pieces = [stagings[r][int(sends[r][j]):int(sends[r][j + 1])] for r in range(P)]
+        recv = torch.cat(pieces).contiguous() if pieces else opss[j].alloc(0, wl[j])
+        o = opss[j].finish(recv, int(pl["recv_n"][j]), dt, cmp, uniqs[j], int(pl["lo_val"][j]),
                            int(pl["lo_fill"][j]), int(pl["hi_val"][j]), int(pl["hi_fill"][j]), wl[j])
         out.append(o.view(shards[j].dtype))
     return out
@@ -529,11 +645,17 @@ def bench_main(args: Any, metric: str, unit: str) -> None:
     ops = GpuOps()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+    # two output buffers, alternated: a slice stays valid for one more step,
+    # and no step allocates
+    outs = [torch.empty((n_loc * 3 // 2 + 65536,) + tail, dtype=pristine.dtype, device=dev) for _ in range(2)]
+    cnt = [0]
+
     def step():
         torch.cuda.synchronize()
         dist.barrier()
+        cnt[0] += 1
         e0.record()
-        out = sort_sharded(pristine, "less", dtype=dt, exchange=ex, ops=ops)
+        out = sort_sharded(pristine, "less", dtype=dt, exchange=ex, ops=ops, out=outs[cnt[0] & 1])
         e1.record()
         torch.cuda.synchronize()
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)

@@ -89,25 +89,25 @@ class NumpyOps:
         u = uniq.numpy().view(np.uint32 if core == _lib.DT_U32 else np.uint64)
         return _keys(u.reshape(m, 4) if core == _lib.DT_REC32 else u[:m], core)
 
-    def _bins(self, t, dt, cmp, uniq, m):
+    def _bins(self, t, dt, cmp, uniq, m, three_way=True):
         core = CORE[dt]
         keys = _keys(to_core(self._np(t, dt), dt, cmp), core)
         us = self._uniq(uniq, core, m) if m else []
         out = []
         for k in keys:
             j = bisect.bisect_left(us, k)
-            out.append(2 * j + (1 if j < m and us[j] == k else 0))
+            out.append(2 * j + (1 if three_way and j < m and us[j] == k else 0))
         return np.array(out, dtype=np.int64)
 
-    def count(self, t, dt, cmp, uniq, m):
+    def count(self, t, dt, cmp, uniq, m, three_way=True):
         # the plan stays with the rank's data (one double may serve every emulated rank)
         if not hasattr(self, "_plans"):
             self._plans = {}
-        b = self._bins(t, dt, cmp, uniq, m)
+        b = self._bins(t, dt, cmp, uniq, m, three_way)
         self._plans[t.data_ptr()] = b
         return torch.from_numpy(np.bincount(b, minlength=2 * m + 1).astype(np.int64))
 
-    def scatter(self, t, dt, cmp, m, bin_rank, bin_off, dests):
+    def scatter(self, t, dt, cmp, m, bin_rank, bin_off, dests, recv_n=None, raw=True, three_way=True):
         b = self._plans[t.data_ptr()]
         src = t.numpy()
         pos = {bb: int(bin_off[bb]) for bb in range(2 * m + 1)}

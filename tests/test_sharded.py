@@ -172,3 +172,56 @@ def test_splitters_merge_duplicates():
     assert uniq.view(np.uint32).tolist() == [1, 7, 9] and mult == [5, 1, 1]
     uniq, mult = sharded.splitters(_lib.DT_U32, smp, 1)
     assert uniq.size == 0 and mult == []
+
+
+def _folded_random(P, rng):
+    K0 = sharded.subbuckets(_lib.DT_U64, P, 1 << 30)
+    S = P * K0 - 1
+    m = int(rng.integers(1, S + 1))
+    mult = [1] * m
+    for _ in range(S - m):
+        mult[int(rng.integers(0, m))] += 1
+    C = rng.integers(0, 40, (P, 2 * m + 1))
+    return K0, mult, C
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_folded_plan_is_every_ranks_level_zero(P):
+    """qmsort_gpu_shard_plan_folded: every key lands exactly once -- open bins
+    sent to one rank at disjoint offsets inside that rank's own bin list,
+    equal-key bins never sent but filled in even shares -- and each rank's
+    local bins alternate open / equal with counts summing to its slice."""
+    rng = np.random.default_rng(P + 7)
+    for _ in range(30):
+        K0, mult, C = _folded_random(P, rng)
+        m = len(mult)
+        pl = sharded.plan_folded(P, K0, mult, C)
+        br, bo, out_n = pl["bin_rank"], pl["bin_off"], pl["out_n"]
+        assert int(out_n.sum()) == int(C.sum())
+        assert all(br[2 * j + 1] == -1 for j in range(m))
+        assert list(br[::2]) == sorted(br[::2])
+        for r in range(P):
+            lm = int(pl["loc_m"][r])
+            cnt = pl["loc_cnt"][r][:2 * lm + 1].astype(np.int64)
+            assert int(cnt.sum()) == int(out_n[r])
+            starts = np.concatenate([[0], np.cumsum(cnt)])
+            # the open bins routed here tile their local bins, senders in order
+            covered = np.zeros(int(out_n[r]), dtype=np.int64)
+            for j in range(m + 1):
+                if br[2 * j] != r:
+                    continue
+                for s_ in range(P):
+                    a = int(bo[s_][2 * j])
+                    covered[a:a + int(C[s_][2 * j])] += 1
+            eq_slots = sum(int(cnt[2 * k + 1]) for k in range(lm))
+            assert int(covered.sum()) + eq_slots == int(out_n[r])
+            assert covered.max(initial=0) <= 1
+            # local values are increasing global indices
+            lu = pl["loc_uniq"][r][:lm]
+            assert list(lu) == sorted(lu) and len(set(lu)) == lm
+        # equal keys: every global value's total is split, never lost
+        for j in range(m):
+            tot = int(C[:, 2 * j + 1].sum())
+            got = sum(int(pl["loc_cnt"][r][2 * k + 1]) for r in range(P)
+                      for k in range(int(pl["loc_m"][r])) if pl["loc_uniq"][r][k] == j)
+            assert got == tot
