@@ -5,7 +5,8 @@
 Inputs (written by gpurun):
   gpurun_out/<prefix>_bench.json     python bench.py (the driver's default line)
   gpurun_out/<prefix>_launches.csv   ncu --metrics gpu__time_duration.sum --csv launch list
-  gpurun_out/<prefix>_full.ncu-rep   ncu --set full capture of the sort's kernels
+  gpurun_out/<prefix>_full_raw.csv   its raw page (METRICS), converted on the box
+                                     (or gpurun_out/<prefix>_full.ncu-rep itself)
 Outputs:
   profiles/r<round>_bench_c2.json, r<round>_launches.csv, r<round>_ncu_summary.txt,
   traffic.json (dram bytes per launch of the dominant kernel families, read by bench.py)
@@ -83,9 +84,13 @@ def main() -> None:
             fh.write(f"{i},{k},{u:.1f}\n")
 
     # full capture: one row per launch
-    rep = os.path.join(G, f"{prefix}_full.ncu-rep")
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
-                         capture_output=True, text=True, check=True).stdout
+    rawcsv = os.path.join(G, f"{prefix}_full_raw.csv")  # converted on the GPU box (scripts/gpu_profile.sh)
+    if os.path.exists(rawcsv):
+        raw = open(rawcsv).read()
+    else:
+        rep = os.path.join(G, f"{prefix}_full.ncu-rep")
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                             capture_output=True, text=True, check=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
     h = r[0]
     lines = [f"# ncu --set full --clock-control none, bench.py --quick (C2 2^28 uint32), round {rnd}",
