@@ -24,6 +24,11 @@
 #ifndef QMSORT_SELECT_PRED
 #define QMSORT_SELECT_PRED 1
 #endif
+// the packed path's five warp rounds fully unrolled (compile-time shuffle
+// distances and lane masks)
+#ifndef QMSORT_UNROLL_WARP_ROUNDS
+#define QMSORT_UNROLL_WARP_ROUNDS 0
+#endif
 #ifndef QMSORT_SELECT_PRED16
 #define QMSORT_SELECT_PRED16 0
 #endif
@@ -214,7 +219,11 @@ __device__ __forceinline__ void warp_merge_round(K (&k)[ITEMS], int lr) {
             }
         }
     }
+#if QMSORT_UNROLL_WARP_ROUNDS
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int s = lr >> 1; s >= 1; s >>= 1) {
         const bool lower = (lane & s) == 0;
 #pragma unroll
@@ -490,7 +499,11 @@ struct BlockSorter {
                 pk[j].v = k0 | (k1 << 16);
             }
             register_sort<U16x2, kPI>(pk);
+#if QMSORT_UNROLL_WARP_ROUNDS
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
             for (int lr = 1; lr < 32; lr <<= 1) warp_merge_round<U16x2, kPI>(pk, lr);
             cross_half_round(pk);
             // each warp reads and writes only its own 1024 positions
