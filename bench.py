@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_DEFAULT, help="keys per GPU")
+    ap.add_argument("--n", "--keys", dest="n", type=int, default=N_DEFAULT, help="keys per GPU")
     ap.add_argument("--algorithm", choices=["samplesort", "mergesort"], default="samplesort")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -294,7 +294,7 @@ def run_ours(args) -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if os.environ.get("QMSORT_BENCH_ONE_GPU") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
         from paper_1804_10062_b200 import sharded
@@ -455,13 +455,17 @@ def relaunch_under_torchrun(args) -> None:
 
     import torch
     have = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+    if os.environ.get("QMSORT_BENCH_ONE_GPU") == "1":  # test aid: every rank on GPU 0
+        have = args.gpus
     if have < args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} GPU(s) visible")
     with socket.socket() as s_:
         s_.bind(("127.0.0.1", 0))
         port = s_.getsockname()[1]
+    # "--n" would be taken for an abbreviation of torchrun's own options
+    own = ["--keys" if a == "--n" else ("--keys=" + a[4:] if a.startswith("--n=") else a) for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *own]
     sys.stdout.flush()
     os.execv(sys.executable, cmd)
 

@@ -37,22 +37,34 @@ def sha(a):
     return h.hexdigest()
 
 
-def one(name):
+# more seeds at full size (BASELINE.md parity seeds {42, 1, 2}) and C3 through
+# the reference's own qms() (the "u64" entry uses std::sort; the sorted order
+# is unique, so the digests must agree)
+EXTRA = {"u32@1": ("u32", 1, None), "u32@2": ("u32", 2, None), "rec32@1": ("rec32", 1, None),
+         "rec32@2": ("rec32", 2, None), "u64@qms": ("u64", 42, "qms")}
+
+
+def one(key):
+    name, seed, how_over = EXTRA.get(key, (key, 42, None))
     n, dt, how = FULL[name]
+    how = how_over or how
     o = Oracle()
-    a = o.gen(name, n, seed=42)
-    rec = {"n": n, "dtype": dt, "seed": 42, "input_sha256": sha(a), "routine": how}
+    a = o.gen(name, n, seed=seed)
+    rec = {"n": n, "dtype": dt, "seed": seed, "config": name, "input_sha256": sha(a), "routine": how}
     t = time.time()
     b = o.ref_sort(dt, a, use_std=(how == "std"))
     rec["cpu_seconds"] = time.time() - t
     rec["sorted_sha256"] = sha(b)
-    json.dump(rec, open(f"/tmp/fullgold/{name}.json", "w"))
-    print(name, rec["cpu_seconds"])
+    os.makedirs("/tmp/fullgold", exist_ok=True)
+    json.dump(rec, open(f"/tmp/fullgold/{key}.json", "w"))
+    print(key, rec["cpu_seconds"])
 
 
 if __name__ == "__main__":
     if sys.argv[1:] == ["--merge"]:
-        out = {os.path.basename(p)[:-5]: json.load(open(p)) for p in glob.glob("/tmp/fullgold/*.json")}
+        old = json.load(open(os.path.join(HERE, "golden_full.json")))
+        out = dict(old)
+        out.update({os.path.basename(p)[:-5]: json.load(open(p)) for p in glob.glob("/tmp/fullgold/*.json")})
         json.dump(out, open(os.path.join(HERE, "golden_full.json"), "w"), indent=1)
         print(sorted(out))
     else:

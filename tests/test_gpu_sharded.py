@@ -235,3 +235,29 @@ def test_c_sort_sharded_errors():
     bad = (ctypes.c_int * 2)(0, 99)
     rc = lib.qmsort_gpu_sort_sharded(DT_U64, 0, 2, bad, din, nin, dout, cap, on, None, None)
     assert rc == _lib.QMSORT_EINVAL
+
+
+@pytest.mark.parametrize("P,cfg", [(2, "c2"), (3, "c5")])
+def test_bench_multi_rank_path(tmp_path, P, cfg):
+    """bench.py --gpus P: re-launched under torch.distributed.run, P ranks
+    (here all on GPU 0, QMSORT_BENCH_ONE_GPU=1, gloo host collectives), the
+    folded peer exchange through real IPC handles; rank 0 prints one line with
+    n_gpus = P and the cross-rank verification."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QMSORT_BENCH_ONE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    args = [sys.executable, os.path.join(root, "bench.py"), "--gpus", str(P), "--steps", "2", "--warmup", "1",
+            "--config", cfg]
+    if cfg == "c2":
+        args += ["--n", str(1 << 22)]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == P
+    assert line["verify"] == {"order_violations_within_slices": 0, "slices_ordered_across_ranks": True,
+                              "multiset_preserved": True}
+    assert 7.9 < line["roofline"]["ledger_bytes_over_nw"] < 8.5
