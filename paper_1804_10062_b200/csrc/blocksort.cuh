@@ -29,6 +29,7 @@
 #ifndef QMSORT_UNROLL_WARP_ROUNDS
 #define QMSORT_UNROLL_WARP_ROUNDS 0
 #endif
+
 #ifndef QMSORT_SELECT_PRED16
 #define QMSORT_SELECT_PRED16 0
 #endif
@@ -462,11 +463,12 @@ struct BlockSorter {
     // rest: a sorted run of 1024, as the unpacked warp stage produces.
     static constexpr bool kPackedPath = std::is_same<K, uint32_t>::value && ITEMS == 32;
     static constexpr int kPI = ITEMS / 2;  // packed registers per lane
-    __device__ __forceinline__ static void cross_half_round(U16x2 (&pk)[kPI]) {
+    template <int NPI>
+    __device__ __forceinline__ static void cross_half_round(U16x2 (&pk)[NPI]) {
         const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int j = 0; j < kPI / 2; ++j) {
-            const int jj = kPI - 1 - j;
+        for (int j = 0; j < NPI / 2; ++j) {
+            const int jj = NPI - 1 - j;
             const uint32_t y0 = __shfl_xor_sync(0xffffffffu, pk[jj].v, 31);
             const uint32_t y1 = __shfl_xor_sync(0xffffffffu, pk[j].v, 31);
             const uint32_t s0 = __byte_perm(y0, 0, 0x1032), s1 = __byte_perm(y1, 0, 0x1032);  // swap halves
@@ -477,44 +479,57 @@ struct BlockSorter {
         for (int sd = 16; sd >= 1; sd >>= 1) {
             const bool lower = (lane & sd) == 0;
 #pragma unroll
-            for (int j = 0; j < kPI; ++j) pk[j] = select_minmax(pk[j], KeyTraits<U16x2>::shfl_xor(pk[j], sd), lower);
+            for (int j = 0; j < NPI; ++j) pk[j] = select_minmax(pk[j], KeyTraits<U16x2>::shfl_xor(pk[j], sd), lower);
         }
 #pragma unroll
-        for (int sd = kPI / 2; sd >= 1; sd >>= 1) {
+        for (int sd = NPI / 2; sd >= 1; sd >>= 1) {
 #pragma unroll
-            for (int j = 0; j < kPI; ++j)
+            for (int j = 0; j < NPI; ++j)
                 if ((j & sd) == 0) net_cas<U16x2>(pk[j], pk[j + sd], j + sd);
         }
     }
-    __device__ __forceinline__ static void sort_tile_packed(K* s, int m, uint32_t lo) {
-        const int tid = threadIdx.x;
-        const int base = (int)(tid & ~31u) * ITEMS + (tid & 31) * kPI;
-        if ((int)(tid & ~31u) * ITEMS < m) {  // warps holding keys
-            U16x2 pk[kPI];
+    // One warp sorts positions [wb, wb + 64 NPI) of s (keys - lo, two per
+    // register) into a sorted run; positions past the warp's span up to its
+    // 32 ITEMS slots get the maximum key.
+    template <int NPI>
+    __device__ __forceinline__ static void packed_warp_sort(K* s, int m, uint32_t lo, int wb) {
+        const int base = wb + (int)(threadIdx.x & 31) * NPI;
+        U16x2 pk[NPI];
 #pragma unroll
-            for (int j = 0; j < kPI; ++j) {
-                const int p0 = base + j, p1 = p0 + 32 * kPI;
-                const uint32_t k0 = p0 < m ? s[P::idx(p0)] - lo : 0xFFFFu;
-                const uint32_t k1 = p1 < m ? s[P::idx(p1)] - lo : 0xFFFFu;
-                pk[j].v = k0 | (k1 << 16);
-            }
-            register_sort<U16x2, kPI>(pk);
+        for (int j = 0; j < NPI; ++j) {
+            const int p0 = base + j, p1 = p0 + 32 * NPI;
+            const uint32_t k0 = p0 < m ? s[P::idx(p0)] - lo : 0xFFFFu;
+            const uint32_t k1 = p1 < m ? s[P::idx(p1)] - lo : 0xFFFFu;
+            pk[j].v = k0 | (k1 << 16);
+        }
+        register_sort<U16x2, NPI>(pk);
 #if QMSORT_UNROLL_WARP_ROUNDS
 #pragma unroll
 #else
 #pragma unroll 1
 #endif
-            for (int lr = 1; lr < 32; lr <<= 1) warp_merge_round<U16x2, kPI>(pk, lr);
-            cross_half_round(pk);
-            // each warp reads and writes only its own 1024 positions
+        for (int lr = 1; lr < 32; lr <<= 1) warp_merge_round<U16x2, NPI>(pk, lr);
+        cross_half_round<NPI>(pk);
+        // each warp reads and writes only its own positions
 #pragma unroll
-            for (int j = 0; j < kPI; ++j) {
-                const int p0 = base + j;
-                const uint32_t v0 = pk[j].v & 0xFFFFu, v1 = pk[j].v >> 16;
-                s[P::idx(p0)] = v0 == 0xFFFFu ? KT::max_key() : v0 + lo;  // 0xFFFF: padding only
-                s[P::idx(p0 + 32 * kPI)] = v1 == 0xFFFFu ? KT::max_key() : v1 + lo;
-            }
+        for (int j = 0; j < NPI; ++j) {
+            const int p0 = base + j;
+            const uint32_t v0 = pk[j].v & 0xFFFFu, v1 = pk[j].v >> 16;
+            s[P::idx(p0)] = v0 == 0xFFFFu ? KT::max_key() : v0 + lo;  // 0xFFFF: padding only
+            s[P::idx(p0 + 32 * NPI)] = v1 == 0xFFFFu ? KT::max_key() : v1 + lo;
         }
+        if constexpr (NPI < kPI) {  // the rest of the warp's run: padding
+            for (int i = wb + 64 * NPI + (int)(threadIdx.x & 31); i < wb + 32 * ITEMS; i += 32)
+                s[P::idx(i)] = KT::max_key();
+        }
+    }
+    __device__ __forceinline__ static void sort_tile_packed(K* s, int m, uint32_t lo) {
+        const int wb = (int)(threadIdx.x & ~31u) * ITEMS;  // the warp's first position
+        // (a tail warp holding at most half its span sorting it with half the
+        // registers, packed_warp_sort<kPI / 2>, measured slower: block sort
+        // 1627 -> 1750 us on C2 -- the second instantiation of the unrolled
+        // network and warp rounds in one kernel)
+        if (wb < m) packed_warp_sort<kPI>(s, m, lo, wb);  // warps holding keys
         K k[ITEMS];
         merge_rounds(k, s, m, 32 * ITEMS, true);
     }
