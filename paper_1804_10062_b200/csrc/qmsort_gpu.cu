@@ -106,7 +106,10 @@ struct Tune<uint32_t> {
     // last level: 3/4 of the target, so most tiles stay inside the packed
     // 16-bit block sort's span (measured: block sort 1817 -> 1716 us on C2)
     static constexpr int LAST_NUM = 3, LAST_DEN = 4;
-    static constexpr int ST = 512, SI = 16;  // sampler
+#ifndef QMSORT_U32_SAMPLE_THREADS
+#define QMSORT_U32_SAMPLE_THREADS 512
+#endif
+    static constexpr int ST = QMSORT_U32_SAMPLE_THREADS, SI = 16;  // sampler
     static constexpr int XT = 512, XI = 16;  // scatter tile
     static constexpr int CT = 256, CU = 16;  // count
     static constexpr int MT = 512, MI = 16;  // merge pass
