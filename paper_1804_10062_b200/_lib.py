@@ -66,6 +66,8 @@ class GpuMetrics(ctypes.Structure):
         ("phase_launches", ctypes.c_uint32 * 8),
         ("resplits", ctypes.c_uint32),
         ("sample_keys", ctypes.c_uint64),
+        ("table_buckets", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
     ]
 
 

@@ -40,6 +40,7 @@
 #include "elements.cuh"
 #include "mergepass.cuh"
 #include "samplesort.cuh"
+#include "tablesort.cuh"
 
 namespace qmsort_b200 {
 
@@ -102,6 +103,12 @@ struct Tune<uint32_t> {
     // block sort classes (96: tiles just over 2048 keys keep all three warps
     // busy; trailing repeats are never chosen -- kNumClasses is the widest list)
     static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512};
+    // task list 5 (a repeat the size rule never picks): the buckets the plan
+    // finds eligible for the table sort (tablesort.cuh)
+#ifndef QMSORT_TABLE_SORT
+#define QMSORT_TABLE_SORT 1
+#endif
+    static constexpr int TABLE_CLASS = QMSORT_TABLE_SORT ? 5 : kNumClasses;
     static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     // last level: 3/4 of the target, so most tiles stay inside the packed
     // 16-bit block sort's span (measured: block sort 1817 -> 1716 us on C2)
@@ -124,6 +131,7 @@ struct Tune<uint64_t> {
     static constexpr int LOGKMAX = 9;
     static constexpr int BI = 16;
     static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 192, 256, 384, 512};  // measured: C3 block sort -7 %
+    static constexpr int TABLE_CLASS = kNumClasses;  // no table sort
     static constexpr int TARGET_DIV = 4;
     static constexpr int LAST_NUM = 3, LAST_DEN = 4;  // measured: C4 block sort -4 %, C3 unchanged
     static constexpr int ST = 512, SI = 16;
@@ -138,6 +146,7 @@ struct Tune<Rec32> {
     static constexpr int LOGKMAX = 8;
     static constexpr int BI = 8;
     static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512};
+    static constexpr int TABLE_CLASS = kNumClasses;
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 2;  // measured: C5 block sort 2.55 -> 2.32 ms
     static constexpr int ST = 512, SI = 8;
@@ -170,6 +179,7 @@ struct Ledger {
     uint64_t alg_bytes = 0;
     uint32_t launches = 0, syncs = 0, levels = 0, merge_passes = 0, resplits = 0;
     uint64_t sample_keys = 0;
+    uint32_t table_buckets = 0;
     uint64_t ph_bytes[QMSORT_NUM_PHASES] = {};
     uint32_t ph_launches[QMSORT_NUM_PHASES] = {};
     bool prof = false;
@@ -427,6 +437,12 @@ static int launch_class(const SortTask* tasks, uint32_t count, K* A, const K* B,
     constexpr int T = TU::CLS_T[C];
     using BS = BlockSorter<K, T, TU::BI>;
     if (count == 0) return QMSORT_OK;
+    if constexpr (std::is_same<K, uint32_t>::value && C == TU::TABLE_CLASS) {
+        QCK(allow_smem((const void*)tablesort_tasks_kernel, TableSort::kSmemBytes));
+        QLAUNCH(led, kPhBlocksort, 0,
+                tablesort_tasks_kernel<<<count, TableSort::T, TableSort::kSmemBytes, st>>>(tasks, A, B, xf));
+        return QMSORT_OK;
+    }
     auto fn = blocksort_tasks_kernel<K, T, TU::BI>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
     QLAUNCH(led, kPhBlocksort, 0, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, A, B, xf));
@@ -563,6 +579,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     p.pivot = (uint32_t)std::max(0, cfg.pivot);
     const double dl = std::min(1.0, std::max(1.0 / 65536.0, cfg.delta > 0 ? cfg.delta : 1.0 / 16.0));
     p.delta_q16 = (uint32_t)(dl * 65536.0);
+    p.table_class = (uint32_t)TU::TABLE_CLASS;
 
     LevelBufs lv[2];
     K* tree[2];
@@ -737,6 +754,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     for (int c = 0; c < kNumClasses; ++c)
         if (nt[c] > L.task_cap) return fail(QMSORT_EINTERNAL, "block-sort task list capacity exceeded");
     QTRY((launch_classes_from<K, 0>(tasks, L.task_cap, nt, A, B, st, led, xf)));
+    if (TU::TABLE_CLASS < kNumClasses) led.table_buckets += nt[TU::TABLE_CLASS < kNumClasses ? TU::TABLE_CLASS : 0];
     if (hc[kCntSlots - 1].nfill || hc[kCntSlots - 1].nfill_big)
         QLAUNCH(led, kPhFill, 0,
                 fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, &tot->nfill_big, L.fill_cap, A, xf));
@@ -872,6 +890,7 @@ static void fill_metrics(qmsort_gpu_metrics* m, Ledger& led, float ms) {
     m->host_syncs = led.syncs + 1;
     m->resplits = led.resplits;
     m->sample_keys = led.sample_keys;
+    m->table_buckets = led.table_buckets;
     for (int i = 0; i < QMSORT_NUM_PHASES; ++i) {
         m->phase_bytes[i] = led.ph_bytes[i];
         m->phase_launches[i] = led.ph_launches[i];

@@ -98,6 +98,9 @@ struct SortTask {  // one bucket for the block sorter
     uint64_t off;
     uint32_t len;
     uint32_t in_a;  // the bucket was scattered into A (else into B); it is sorted into A
+    // integer keys: every key of the bucket lies in [klo, khi] (the splitters
+    // around it within the parent segment's range) -- the table sort's span
+    uint64_t klo, khi;
 };
 
 constexpr uint64_t kFillWarp = 4096;  // fills up to this many keys get a warp each
@@ -175,7 +178,16 @@ struct PlanParams {
     int dst_is_a;           // this level's scatter writes the caller's buffer
     uint32_t pivot;         // PivotStrategy (sort.hpp:19): 2 mom_of_thirds, 3 hybrid
     uint32_t delta_q16;     // SortConfig::delta in 1/65536 (hybrid skew band)
+    uint32_t table_class;   // task list of the table sort (tablesort.cuh); >= kNumClasses: off
 };
+
+// Table-sort eligibility of a bucket of len keys within [klo, khi]
+// (TableSort::eligible, tablesort.cuh -- restated here for the plan).
+__host__ __device__ inline bool table_sort_eligible(uint32_t len, uint64_t klo, uint64_t khi) {
+    if (khi < klo || len > 4096u || len < 256u) return false;
+    const uint64_t span = khi - klo;
+    return span < 65536ull && span >= 4ull * len && span <= 64ull * len;
+}
 
 __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
     uint32_t r = 0;
@@ -738,6 +750,21 @@ __global__ void __launch_bounds__(512) colsum_kernel(const SegDesc* __restrict__
     }
 }
 
+// Key bounds of bin b of segment d (integer keys): bucket j holds the keys in
+// (splitter j-1, splitter j] within the segment's [lo, hi]; with equality
+// bins the splitter itself went to bin 2j+1.
+template <class K>
+__device__ __forceinline__ void bucket_bounds(const SegDesc& d, const K* __restrict__ sp, uint32_t b,
+                                              uint64_t& klo, uint64_t& khi) {
+    klo = d.lo;
+    khi = d.hi;
+    if constexpr (KeyTraits<K>::kLut) {
+        const uint32_t j = d.eq ? (b >> 1) : b;
+        if (j > 0) klo = (uint64_t)KeyTraits<K>::bits(sp[j - 1]) + 1;
+        if (j < d.m) khi = (uint64_t)KeyTraits<K>::bits(sp[j]) - (d.eq ? 1u : 0u);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3b: per segment: bucket starts and child work.
 // ---------------------------------------------------------------------------
@@ -781,6 +808,11 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
         if (len != 0 && !(d.eq && (b & 1)) && len <= p.cap && !(len == 1 && p.dst_is_a && !p.xf_fix)) {
             uint32_t cls = 0;
             while (cls < kNumClasses - 1 && len > p.class_cap[cls]) ++cls;
+            if (KeyTraits<K>::kLut && p.table_class < (uint32_t)kNumClasses) {
+                uint64_t klo, khi;
+                bucket_bounds<K>(d, sorted_store + d.sp, b, klo, khi);
+                if (table_sort_eligible(len, klo, khi)) cls = p.table_class;
+            }
             sl = (cls << 28) | atomicAdd(&cls_count[cls], 1u);
             atomicAdd(&cls_keys, (unsigned long long)len);
         }
@@ -826,6 +858,7 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 st.off = off;
                 st.len = len;
                 st.in_a = p.dst_is_a ? 1u : 0u;
+                bucket_bounds<K>(d, sorted_store + d.sp, b, st.klo, st.khi);
                 tasks[(size_t)cls * p.task_cap + t] = st;
             } else {
                 atomicExch(&cur_cnt->overflow, 1u);

@@ -249,3 +249,66 @@ def test_skewed_window(oracle, dt, n):
     a = raw.astype(np.uint32) if dt == DT_U32 else (raw.view(np.int64) if dt == DT_I64 else raw)
     got, _ = gpu_sort(a)
     np.testing.assert_array_equal(got, oracle.sort(dt, a))
+
+
+def dense_u32(rng, n, density_inv, base=0):
+    """n uint32 keys uniform over n * density_inv values starting at base."""
+    return (rng.integers(0, n * density_inv, size=n, dtype=np.uint64) + np.uint64(base)).astype(np.uint32)
+
+
+@pytest.mark.parametrize("density_inv", [3, 4, 5, 16, 33, 64, 65, 200])
+@pytest.mark.parametrize("n", [1 << 20, 3000001])
+@pytest.mark.parametrize("dt", [DT_U32, DT_I32])
+def test_table_sort_dense_keys(oracle, dt, density_inv, n):
+    """Dense uint32 / int32 key sets: the last level's buckets span a few 10^4
+    values and go through the comparison-free table sort (K5t) when the span
+    is between 4 and 64 values per key; denser and sparser buckets keep the
+    network.  Both orders, keys touching both ends of the key space."""
+    rng = np.random.default_rng(n + density_inv)
+    for base in (0, (1 << 32) - n * density_inv, 0x7FFFFFFF - n * density_inv // 2):
+        a = dense_u32(rng, n, density_inv, base)
+        if dt == DT_I32:
+            a = a.view(np.int32)
+        got, m = gpu_sort(a)
+        np.testing.assert_array_equal(got, np.sort(a))
+        if 5 <= density_inv <= 16:  # (33 values per key: only buckets under 2000 keys fit 2^16 values)
+            assert m.table_buckets > 0
+        if density_inv <= 3 or density_inv >= 200:
+            assert m.table_buckets == 0
+        got, _ = gpu_sort(a, less="greater")
+        np.testing.assert_array_equal(got, np.sort(a)[::-1])
+
+
+@pytest.mark.parametrize("copies", [2, 3, 4, 5, 9])
+@pytest.mark.parametrize("hot", [1, 40, 2000, 40000])
+def test_table_sort_repeated_values(oracle, copies, hot):
+    """Table sort with second, third, fourth and later copies of a value:
+    `hot` values of a dense key set appear `copies` times (planes 1 and 2, the
+    overflow list, and -- 40000 x 5 and up -- more fourth copies per bucket
+    than the list holds, which sends the bucket back to the network)."""
+    n = 1 << 20
+    rng = np.random.default_rng(copies * 1000 + hot)
+    a = dense_u32(rng, n, 16, 123456)
+    idx = rng.choice(n, size=hot, replace=False)
+    for c in range(1, copies):
+        a[(idx + c * 7919) % n] = a[idx]
+    got, m = gpu_sort(a)
+    np.testing.assert_array_equal(got, np.sort(a))
+    assert m.table_buckets > 0
+    got, _ = gpu_sort(a, less="greater")
+    np.testing.assert_array_equal(got, np.sort(a)[::-1])
+
+
+def test_table_sort_clustered_buckets(oracle):
+    """Buckets whose keys crowd one end of their splitter range (a staircase of
+    dense clusters separated by gaps) and buckets made of a few long runs."""
+    n = 1 << 21
+    rng = np.random.default_rng(5)
+    steps = rng.integers(0, 1 << 12, size=n // 4096, dtype=np.uint64).cumsum() * np.uint64(4096)
+    a = (np.repeat(steps, 4096)[:n] + rng.integers(0, 9000, size=n, dtype=np.uint64)).astype(np.uint32)
+    got, m = gpu_sort(a)
+    np.testing.assert_array_equal(got, np.sort(a))
+    b = np.repeat(rng.integers(0, 1 << 24, size=n // 3, dtype=np.uint64), 3)[:n].astype(np.uint32)
+    rng.shuffle(b)
+    got, m = gpu_sort(b)
+    np.testing.assert_array_equal(got, np.sort(b))
