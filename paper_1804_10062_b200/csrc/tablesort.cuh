@@ -8,11 +8,12 @@
 // bottom merge levels (merge.hpp:103-119), like K5, for the buckets the plan
 // marks eligible (TableSort::eligible):
 //   1. a bit table of the span lives in shared memory; every key sets its bit
-//      in plane 0 (atomicOr).  A key that finds it set is a second copy and
-//      sets the same bit of plane 1, a third copy that of plane 2; fourth and
-//      later copies go to a short overflow list;
+//      (atomicOr).  A key that finds it set is a second copy: it bumps its
+//      word's copy count and sets the same bit of a second plane, a third
+//      copy that of a third plane; fourth and later copies go to a short
+//      overflow list;
 //   2. one scan over the table's words gives every word the number of keys
-//      below it (bits of the three planes + overflow entries);
+//      below it (set bits + copy count);
 //   3. a key's rank = its word's prefix + the set bits below its own bit
 //      (+ its copy number): it is stored at that position of a 16-bit staging
 //      tile (key - klo), which goes out with coalesced stores.
@@ -34,12 +35,9 @@ __device__ __forceinline__ uint32_t smem_atom_or(uint32_t addr, uint32_t v) {
     asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(v) : "memory");
     return old;
 }
-__device__ __forceinline__ uint4 smem_ld128(uint32_t addr) {
-    uint4 r;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "r"(addr)
-                 : "memory");
+__device__ __forceinline__ uint2 smem_ld64(uint32_t addr) {
+    uint2 r;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "r"(addr) : "memory");
     return r;
 }
 __device__ __forceinline__ void smem_st32(uint32_t addr, uint32_t v) {
@@ -54,22 +52,25 @@ struct TableSort {
     static constexpr int kWords = 2048;                          // 2^16 values, one bit each
     static constexpr int kWpt = kWords / T;                      // table words per thread in the scan
     static constexpr int kOvfCap = 128;
-    static constexpr uint32_t kHasOvf = 1u << 31;  // cell.w: the word has overflow entries
     static_assert(kWpt == 8, "the cell swizzle assumes 8 words per thread");
 
     struct Smem {
-        // One 16-byte cell per table word (32 values): x, y, z = the bits of
-        // the first, second and third copy of each value, w = keys below the
-        // word | kHasOvf.  Word w lives in cell w ^ ((w >> 3) & 7): the
-        // scan's per-thread walks over 8 consecutive words are conflict-free.
-        alignas(16) uint4 cell[kWords];
+        // One 8-byte cell per table word (32 values): x = the values present,
+        // y = keys below the word (low half, written by the scan) | second and
+        // later copies among the word's keys (high half, counted by the
+        // insert).  Word w lives in cell w ^ ((w >> 4) & 7): the scan's
+        // per-thread walks over 8 consecutive words are conflict-free.
+        alignas(16) uint2 cell[kWords];
+        // bit b of y2[w] / y3[w]: value 32 w + b has a second / third copy
+        // (same swizzle; read only for words whose copy count is not zero)
+        uint32_t y2[kWords], y3[kWords];
         alignas(16) uint16_t out[kCap];
         uint32_t ovf[kOvfCap];  // fourth and later copies (key - klo)
         uint32_t warp_sums[T / 32];
         uint32_t novf;
     };
     using Net = BlockSorter<uint32_t, T, ITEMS>;  // fallback, in the table's memory
-    static_assert(Net::kSmemBytes <= sizeof(uint4) * kWords, "fallback tile");
+    static_assert(Net::kSmemBytes <= (sizeof(uint2) + 2 * sizeof(uint32_t)) * kWords, "fallback tile");
     static constexpr size_t kSmemBytes = sizeof(Smem);
 
     // Buckets the plan sends here: at most kCap keys, bounds spanning fewer
@@ -79,26 +80,19 @@ struct TableSort {
         return table_sort_eligible(len, klo, khi);
     }
 
-    __device__ __forceinline__ static uint32_t cell_of(uint32_t w) { return w ^ ((w >> 3) & 7u); }
+    __device__ __forceinline__ static uint32_t cell_of(uint32_t w) { return w ^ ((w >> 4) & 7u); }
 
     // The rare paths are kept out of line: the unrolled per-key code stays
     // small (inlined, the kernel stalled on instruction fetch).
     // A key that found its first-copy bit set: returns its copy number (1, 2,
     // or 3 = on the overflow list).
     __device__ __noinline__ static uint32_t later_copy(Smem& sm, uint32_t a, uint32_t bit, uint32_t v) {
-        if (!(atomicOr(&sm.cell[a].y, bit) & bit)) return 1u;
-        if (!(atomicOr(&sm.cell[a].z, bit) & bit)) return 2u;
+        atomicAdd(&sm.cell[a].y, 0x10000u);
+        if (!(atomicOr(&sm.y2[a], bit) & bit)) return 1u;
+        if (!(atomicOr(&sm.y3[a], bit) & bit)) return 2u;
         const uint32_t i = atomicAdd(&sm.novf, 1u);
         if (i < (uint32_t)kOvfCap) sm.ovf[i] = v;
-        atomicOr(&sm.cell[a].w, kHasOvf);
         return 3u;
-    }
-    // overflow entries in table word w
-    __device__ __noinline__ static uint32_t ovf_in_word(const Smem& sm, uint32_t w, uint32_t L) {
-        uint32_t n = 0;
-#pragma unroll 1
-        for (uint32_t i = 0; i < L; ++i) n += (sm.ovf[i] >> 5) == w ? 1u : 0u;
-        return n;
     }
     // overflow entries below v in v's word
     __device__ __noinline__ static uint32_t ovf_below(const Smem& sm, uint32_t v, uint32_t L) {
@@ -108,6 +102,13 @@ struct TableSort {
             const uint32_t o = sm.ovf[i];
             n += ((o >> 5) == (v >> 5) && o < v) ? 1u : 0u;
         }
+        return n;
+    }
+    // later copies of smaller values in the word of cell a
+    __device__ __forceinline__ static uint32_t copies_below(const Smem& sm, uint32_t a, uint32_t below, uint32_t v,
+                                                            uint32_t L) {
+        uint32_t n = (uint32_t)__popc(sm.y2[a] & below) + (uint32_t)__popc(sm.y3[a] & below);
+        if (L) n += ovf_below(sm, v, L);
         return n;
     }
 
@@ -128,7 +129,11 @@ struct TableSort {
 #pragma unroll
             for (int u = 0; u < ITEMS; ++u) k[u] = u * T + tid < m ? p[u * T] : klo;
         }
-        for (uint32_t i = tid; i < Wc; i += T) sm.cell[i] = make_uint4(0, 0, 0, 0);
+        for (uint32_t i = tid; i < Wc; i += T) {
+            sm.cell[i] = make_uint2(0, 0);
+            sm.y2[i] = 0;
+            sm.y3[i] = 0;
+        }
         if (tid == 0) sm.novf = 0;
         __syncthreads();
         // 1. insert; k[u] becomes (key - klo) | copy number << 16, or ~0 for
@@ -144,7 +149,7 @@ struct TableSort {
                 const uint32_t a = cell_of(v >> 5);
                 const uint32_t bit = valid ? 1u << (v & 31u) : 0u;
                 k[u] = valid ? v : 0xFFFFFFFFu;
-                if (smem_atom_or(cells + a * 16u, bit) & bit) {
+                if (smem_atom_or(cells + a * 8u, bit) & bit) {
                     const uint32_t c = later_copy(sm, a, bit, v);
                     k[u] = c == 3u ? 0xFFFFFFFFu : (v | (c << 16));
                 }
@@ -159,13 +164,12 @@ struct TableSort {
         const uint32_t w0 = (uint32_t)tid * kWpt;
         const bool owner = w0 < Wc;
         // cell of word w0 + j (w0 is a multiple of 8: the swizzle only permutes the thread's own 8 cells)
-        auto own = [&](int j) -> uint32_t { return cells + (w0 | (((uint32_t)tid & 7u) ^ (uint32_t)j)) * 16u; };
+        auto own = [&](int j) -> uint32_t { return cells + (w0 | ((((uint32_t)tid >> 1) & 7u) ^ (uint32_t)j)) * 8u; };
         if (owner) {
 #pragma unroll
             for (int j = 0; j < kWpt; ++j) {
-                const uint4 c = smem_ld128(own(j));
-                nk[j] = (uint32_t)__popc(c.x) + (uint32_t)__popc(c.y) + (uint32_t)__popc(c.z);
-                if (c.w) nk[j] += ovf_in_word(sm, w0 + j, L);
+                const uint2 c = smem_ld64(own(j));
+                nk[j] = (uint32_t)__popc(c.x) + (c.y >> 16);
                 cnt += nk[j];
             }
         }
@@ -184,8 +188,8 @@ struct TableSort {
             for (int i = 0; i < T / 32; ++i) run += (uint32_t)i < wid ? sm.warp_sums[i] : 0u;
 #pragma unroll
             for (int j = 0; j < kWpt; ++j) {
-                // the flag bit was set by the insert phase: keep it (prefix < 2^13)
-                asm volatile("red.shared.or.b32 [%0], %1;" : : "r"(own(j) + 12u), "r"(run) : "memory");
+                // the copy count in the high half stays (prefix < 2^13)
+                asm volatile("red.shared.or.b32 [%0], %1;" : : "r"(own(j) + 4u), "r"(run) : "memory");
                 run += nk[j];
             }
         }
@@ -197,21 +201,20 @@ struct TableSort {
             if (u < rows) {
                 const uint32_t v = k[u] & 0xFFFFu;
                 const uint32_t a = cell_of(v >> 5);
-                const uint4 c = smem_ld128(cells + a * 16u);
-                const uint32_t above = 0xFFFFFFFFu << (v & 31u);
-                uint32_t pos = (c.w & 0xFFFFu) + (uint32_t)__popc(c.x & ~above) + (uint32_t)__popc(c.y & ~above) +
-                               (uint32_t)__popc(c.z & ~above) + ((k[u] >> 16) & 3u);
-                if (c.w & kHasOvf) pos += ovf_below(sm, v, L);
+                const uint2 c = smem_ld64(cells + a * 8u);
+                const uint32_t below = ~(0xFFFFFFFFu << (v & 31u));
+                uint32_t pos = (c.y & 0xFFFFu) + (uint32_t)__popc(c.x & below);
+                if (c.y >> 16) pos += copies_below(sm, a, below, v, L) + ((k[u] >> 16) & 3u);
                 QCHECK(k[u] == 0xFFFFFFFFu || pos < (uint32_t)m, pos, m);
                 if (k[u] != 0xFFFFFFFFu) smem_st16(outs + pos * 2u, v);
             }
         }
         for (uint32_t i = tid; i < L; i += T) {  // fourth and later copies
             const uint32_t v = sm.ovf[i];
-            const uint4 c = sm.cell[cell_of(v >> 5)];
+            const uint32_t a = cell_of(v >> 5);
+            const uint2 c = sm.cell[a];
             const uint32_t below = (1u << (v & 31u)) - 1u;
-            uint32_t pos = (c.w & 0xFFFFu) + (uint32_t)__popc(c.x & below) + (uint32_t)__popc(c.y & below) +
-                           (uint32_t)__popc(c.z & below) + ovf_below(sm, v, L) + 3u;
+            uint32_t pos = (c.y & 0xFFFFu) + (uint32_t)__popc(c.x & below) + copies_below(sm, a, below, v, L) + 3u;
 #pragma unroll 1
             for (uint32_t j = 0; j < i; ++j) pos += sm.ovf[j] == v ? 1u : 0u;
             QCHECK(pos < (uint32_t)m, pos, m);

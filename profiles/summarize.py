@@ -109,7 +109,7 @@ def main() -> None:
         name = family(d["Kernel Name"]) + ("<" + d["Kernel Name"].split("<")[1].split(">")[0] + ">"
                                            if "<" in d["Kernel Name"] else "")
         lines.append(f"{name} | " + " | ".join(vals))
-        f = family(d["Kernel Name"]).replace("_kernel", "").replace("blocksort_tasks", "blocksort")
+        f = family(d["Kernel Name"]).replace("_kernel", "").replace("blocksort_tasks", "blocksort").replace("tablesort_tasks", "blocksort")
         try:
             b = (float(d["dram__bytes_read.sum"]) + float(d["dram__bytes_write.sum"])) * 1e9
         except ValueError:
