@@ -102,17 +102,27 @@ struct Tune<uint32_t> {
     static constexpr int BI = 32;                                 // block sort keys / thread
     // block sort classes (96: tiles just over 2048 keys keep all three warps
     // busy; trailing repeats are never chosen -- kNumClasses is the widest list)
-    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512};
+    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512, 512, 512};
     // task list 5 (a repeat the size rule never picks): the buckets the plan
     // finds eligible for the table sort (tablesort.cuh)
 #ifndef QMSORT_TABLE_SORT
 #define QMSORT_TABLE_SORT 1
 #endif
     static constexpr int TABLE_CLASS = QMSORT_TABLE_SORT ? 5 : kNumClasses;
+    // task list 6: buckets for the wide-span table sort (CellSort)
+#ifndef QMSORT_CELL_SORT
+#define QMSORT_CELL_SORT 1
+#endif
+    static constexpr int CELL_CLASS = QMSORT_CELL_SORT ? 6 : kNumClasses;
+    static constexpr int CELL_BIG_CLASS = kNumClasses;  // (none)
     static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     // last level: 3/4 of the target, so most tiles stay inside the packed
     // 16-bit block sort's span (measured: block sort 1817 -> 1716 us on C2)
-    static constexpr int LAST_NUM = 3, LAST_DEN = 4;
+#ifndef QMSORT_U32_LAST_NUM
+#define QMSORT_U32_LAST_NUM 3
+#define QMSORT_U32_LAST_DEN 4
+#endif
+    static constexpr int LAST_NUM = QMSORT_U32_LAST_NUM, LAST_DEN = QMSORT_U32_LAST_DEN;
 #ifndef QMSORT_U32_SAMPLE_THREADS
 #define QMSORT_U32_SAMPLE_THREADS 512
 #endif
@@ -130,8 +140,10 @@ template <>
 struct Tune<uint64_t> {
     static constexpr int LOGKMAX = 9;
     static constexpr int BI = 16;
-    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 192, 256, 384, 512};  // measured: C3 block sort -7 %
-    static constexpr int TABLE_CLASS = kNumClasses;  // no table sort
+    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 192, 256, 384, 512, 512, 512};  // measured: C3 block sort -7 %
+    static constexpr int TABLE_CLASS = kNumClasses;  // no dense table sort
+    static constexpr int CELL_CLASS = QMSORT_CELL_SORT ? 7 : kNumClasses;
+    static constexpr int CELL_BIG_CLASS = QMSORT_CELL_SORT ? 8 : kNumClasses;  // buckets beyond 2048 keys
     static constexpr int TARGET_DIV = 4;
     static constexpr int LAST_NUM = 3, LAST_DEN = 4;  // measured: C4 block sort -4 %, C3 unchanged
     static constexpr int ST = 512, SI = 16;
@@ -145,8 +157,8 @@ template <>
 struct Tune<Rec32> {
     static constexpr int LOGKMAX = 8;
     static constexpr int BI = 8;
-    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512};
-    static constexpr int TABLE_CLASS = kNumClasses;
+    static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512, 512, 512};
+    static constexpr int TABLE_CLASS = kNumClasses, CELL_CLASS = kNumClasses, CELL_BIG_CLASS = kNumClasses;
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 2;  // measured: C5 block sort 2.55 -> 2.32 ms
     static constexpr int ST = 512, SI = 8;
@@ -443,6 +455,14 @@ static int launch_class(const SortTask* tasks, uint32_t count, K* A, const K* B,
                 tablesort_tasks_kernel<<<count, TableSort::T, TableSort::kSmemBytes, st>>>(tasks, A, B, xf));
         return QMSORT_OK;
     }
+    if constexpr (KeyTraits<K>::kLut && (C == TU::CELL_CLASS || C == TU::CELL_BIG_CLASS)) {
+        constexpr bool BIG = C == TU::CELL_BIG_CLASS;
+        using CS = CellSort<K, BIG>;
+        auto fn = cellsort_tasks_kernel<K, BIG>;
+        QCK(allow_smem((const void*)fn, CS::kSmemBytes));
+        QLAUNCH(led, kPhBlocksort, 0, fn<<<count, CS::T, CS::kSmemBytes, st>>>(tasks, A, B, xf));
+        return QMSORT_OK;
+    }
     auto fn = blocksort_tasks_kernel<K, T, TU::BI>;
     QCK(allow_smem((const void*)fn, BS::kSmemBytes));
     QLAUNCH(led, kPhBlocksort, 0, fn<<<count, T, BS::kSmemBytes, st>>>(tasks, A, B, xf));
@@ -580,6 +600,16 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
     const double dl = std::min(1.0, std::max(1.0 / 65536.0, cfg.delta > 0 ? cfg.delta : 1.0 / 16.0));
     p.delta_q16 = (uint32_t)(dl * 65536.0);
     p.table_class = (uint32_t)TU::TABLE_CLASS;
+    p.cell_class = (uint32_t)TU::CELL_CLASS;
+    if constexpr (KeyTraits<K>::kLut) {
+        p.cell_cap = (uint32_t)CellSort<K>::kCap;
+        p.cell_bits = (uint32_t)CellSort<K>::kCellBits;
+        p.cell_big_cap = (uint32_t)CellSort<K, true>::kCap;
+        p.cell_big_bits = (uint32_t)CellSort<K, true>::kCellBits;
+    } else {
+        p.cell_cap = p.cell_bits = p.cell_big_cap = p.cell_big_bits = 0;
+    }
+    p.cell_big_class = (uint32_t)TU::CELL_BIG_CLASS;
 
     LevelBufs lv[2];
     K* tree[2];
@@ -755,6 +785,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         if (nt[c] > L.task_cap) return fail(QMSORT_EINTERNAL, "block-sort task list capacity exceeded");
     QTRY((launch_classes_from<K, 0>(tasks, L.task_cap, nt, A, B, st, led, xf)));
     if (TU::TABLE_CLASS < kNumClasses) led.table_buckets += nt[TU::TABLE_CLASS < kNumClasses ? TU::TABLE_CLASS : 0];
+    if (TU::CELL_CLASS < kNumClasses) led.table_buckets += nt[TU::CELL_CLASS < kNumClasses ? TU::CELL_CLASS : 0];
+    if (TU::CELL_BIG_CLASS < kNumClasses)
+        led.table_buckets += nt[TU::CELL_BIG_CLASS < kNumClasses ? TU::CELL_BIG_CLASS : 0];
     if (hc[kCntSlots - 1].nfill || hc[kCntSlots - 1].nfill_big)
         QLAUNCH(led, kPhFill, 0,
                 fill_kernel<K><<<1184, 256, 0, st>>>(fills, &tot->nfill, &tot->nfill_big, L.fill_cap, A, xf));

@@ -41,7 +41,7 @@
 
 namespace qmsort_b200 {
 
-constexpr int kNumClasses = 7;  // block-sort size classes (Tune<K>::CLS_T)
+constexpr int kNumClasses = 9;  // block-sort size classes (Tune<K>::CLS_T)
 constexpr int kLutMaxBits = 12;
 constexpr int kLutPerSplitter = 16;  // LUT words reserved per splitter slot
 
@@ -179,6 +179,9 @@ struct PlanParams {
     uint32_t pivot;         // PivotStrategy (sort.hpp:19): 2 mom_of_thirds, 3 hybrid
     uint32_t delta_q16;     // SortConfig::delta in 1/65536 (hybrid skew band)
     uint32_t table_class;   // task list of the table sort (tablesort.cuh); >= kNumClasses: off
+    uint32_t cell_class;    // task list of the wide-span table sort (CellSort); >= kNumClasses: off
+    uint32_t cell_cap, cell_bits;  // CellSort<K>: keys per bucket, log2 of its cells
+    uint32_t cell_big_class, cell_big_cap, cell_big_bits;  // CellSort<K, true> for the buckets beyond cell_cap
 };
 
 // Table-sort eligibility of a bucket of len keys within [klo, khi]
@@ -187,6 +190,30 @@ __host__ __device__ inline bool table_sort_eligible(uint32_t len, uint64_t klo, 
     if (khi < klo || len > 4096u || len < 256u) return false;
     const uint64_t span = khi - klo;
     return span < 65536ull && span >= 4ull * len && span <= 64ull * len;
+}
+
+// Cell width of a bucket of len keys spanning span + 1 values: the smallest
+// shift that leaves at most min(2^max_bits, 16 len rounded up to a power of
+// two) cells.
+__host__ __device__ inline uint32_t cell_shift(uint32_t len, uint64_t span, uint32_t max_bits) {
+#ifdef __CUDA_ARCH__
+    const uint32_t bits = 64u - (uint32_t)__clzll((long long)span);  // bit length of span
+    const uint32_t tb = min(max_bits, 32u - (uint32_t)__clz((int)(16u * len - 1u)));
+#else
+    uint32_t bits = 0;
+    while (bits < 64 && (span >> bits)) ++bits;
+    uint32_t tb = 0;
+    while (tb < max_bits && (1u << tb) < 16u * len) ++tb;
+#endif
+    return bits > tb ? bits - tb : 0u;
+}
+// Buckets the plan sends to the cell sort (CellSort<K>: cap keys, 2^max_bits
+// cells): at least 4 cells per key (else most cells hold several keys).
+__host__ __device__ inline bool cell_sort_eligible(uint32_t len, uint64_t klo, uint64_t khi, uint32_t cap,
+                                                   uint32_t max_bits) {
+    if (khi < klo || len > cap || len < 256u) return false;
+    const uint64_t span = khi - klo;
+    return (span >> cell_shift(len, span, max_bits)) >= 4ull * len;
 }
 
 __host__ __device__ inline uint32_t ceil_log2_u64(uint64_t x) {
@@ -808,10 +835,13 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
         if (len != 0 && !(d.eq && (b & 1)) && len <= p.cap && !(len == 1 && p.dst_is_a && !p.xf_fix)) {
             uint32_t cls = 0;
             while (cls < kNumClasses - 1 && len > p.class_cap[cls]) ++cls;
-            if (KeyTraits<K>::kLut && p.table_class < (uint32_t)kNumClasses) {
+            if (KeyTraits<K>::kLut && (p.table_class < (uint32_t)kNumClasses || p.cell_class < (uint32_t)kNumClasses)) {
                 uint64_t klo, khi;
                 bucket_bounds<K>(d, sorted_store + d.sp, b, klo, khi);
-                if (table_sort_eligible(len, klo, khi)) cls = p.table_class;
+                if (p.table_class < (uint32_t)kNumClasses && table_sort_eligible(len, klo, khi)) cls = p.table_class;
+                else if (p.cell_class < (uint32_t)kNumClasses && cell_sort_eligible(len, klo, khi, p.cell_cap, p.cell_bits)) cls = p.cell_class;
+                else if (p.cell_big_class < (uint32_t)kNumClasses && len > p.cell_cap &&
+                         cell_sort_eligible(len, klo, khi, p.cell_big_cap, p.cell_big_bits)) cls = p.cell_big_class;
             }
             sl = (cls << 28) | atomicAdd(&cls_count[cls], 1u);
             atomicAdd(&cls_keys, (unsigned long long)len);

@@ -262,8 +262,8 @@ def dense_u32(rng, n, density_inv, base=0):
 def test_table_sort_dense_keys(oracle, dt, density_inv, n):
     """Dense uint32 / int32 key sets: the last level's buckets span a few 10^4
     values and go through the comparison-free table sort (K5t) when the span
-    is between 4 and 64 values per key; denser and sparser buckets keep the
-    network.  Both orders, keys touching both ends of the key space."""
+    is between 4 and 64 values per key; sparser buckets go through the
+    wide-span table sort (K5c), denser ones keep the network.  Both orders, keys touching both ends of the key space."""
     rng = np.random.default_rng(n + density_inv)
     for base in (0, (1 << 32) - n * density_inv, 0x7FFFFFFF - n * density_inv // 2):
         a = dense_u32(rng, n, density_inv, base)
@@ -271,10 +271,10 @@ def test_table_sort_dense_keys(oracle, dt, density_inv, n):
             a = a.view(np.int32)
         got, m = gpu_sort(a)
         np.testing.assert_array_equal(got, np.sort(a))
-        if 5 <= density_inv <= 16:  # (33 values per key: only buckets under 2000 keys fit 2^16 values)
+        if 5 <= density_inv <= 16:
             assert m.table_buckets > 0
-        if density_inv <= 3 or density_inv >= 200:
-            assert m.table_buckets == 0
+        if density_inv <= 3:  # too dense for either table sort (a segment's end buckets aside)
+            assert m.table_buckets <= 4
         got, _ = gpu_sort(a, less="greater")
         np.testing.assert_array_equal(got, np.sort(a)[::-1])
 
@@ -312,3 +312,91 @@ def test_table_sort_clustered_buckets(oracle):
     rng.shuffle(b)
     got, m = gpu_sort(b)
     np.testing.assert_array_equal(got, np.sort(b))
+
+
+def _as_dtype(raw, dt):
+    """uint64 bit patterns -> an array of dt (float64: finite, no NaN / -0.0)."""
+    if dt == DT_U64:
+        return raw.astype(np.uint64)
+    if dt == DT_I64:
+        return raw.astype(np.uint64).view(np.int64)
+    if dt == DT_U32:
+        return (raw & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    if dt == DT_I32:
+        return (raw & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.int32)
+    raise ValueError(dt)
+
+
+@pytest.mark.parametrize("n", [1 << 18, 1 << 20, (1 << 21) + 12345, 1 << 22])
+@pytest.mark.parametrize("dt", [DT_U64, DT_I64, DT_F64, DT_U32])
+def test_cell_sort_wide_span_keys(oracle, dt, n):
+    """Sparse keys (64-bit keys, uint32 keys over the full range at small n):
+    the last level's buckets span far more than 2^16 values and go through
+    the wide-span table sort (K5c: cells of 2^sh values, in-cell ordering).
+    2^20 8-byte keys leave buckets of about 2048 keys (small shape), 2^21 of
+    about 4096 (big shape).  Both orders."""
+    a = rand_input(dt, n, seed=n + dt)
+    got, m = gpu_sort(a)
+    np.testing.assert_array_equal(got, np.sort(a))
+    assert m.table_buckets > 0
+    got, _ = gpu_sort(a, less="greater")
+    np.testing.assert_array_equal(got, np.sort(a)[::-1])
+
+
+@pytest.mark.parametrize("dist", ["gaussian", "exponential", "near_zero", "binades", "lattice"])
+def test_cell_sort_float_shapes(oracle, dist):
+    """float64 shapes whose bit patterns are far from uniform inside a bucket:
+    a bucket that straddles zero or many binades crowds its keys into a few
+    cells (overflow list / fix list full -> the network sorts it)."""
+    n = 1 << 21
+    rng = np.random.default_rng(11)
+    if dist == "gaussian":
+        x = rng.standard_normal(n)
+    elif dist == "exponential":
+        x = rng.exponential(1.0, n) * rng.choice([-1.0, 1.0], n)
+    elif dist == "near_zero":
+        x = rng.standard_normal(n) * 10.0 ** rng.integers(-300, -280, n)
+    elif dist == "binades":
+        x = np.ldexp(rng.random(n) + 0.5, rng.integers(-40, 40, n)) * rng.choice([-1.0, 1.0], n)
+    else:  # values on a coarse lattice: a few thousand distinct doubles, each many times
+        x = rng.integers(-3000, 3000, n).astype(np.float64) * 0.37
+    x[x == 0] = 0.0
+    got, _ = gpu_sort(x)
+    np.testing.assert_array_equal(got, np.sort(x))
+    got, _ = gpu_sort(x, less="greater")
+    np.testing.assert_array_equal(got, np.sort(x)[::-1])
+
+
+@pytest.mark.parametrize("dt", [DT_U64, DT_I64, DT_U32])
+@pytest.mark.parametrize("shape", ["pairs", "triples", "quads", "runs9", "clusters", "two_scales", "hot_cell"])
+def test_cell_sort_crowded_cells(oracle, dt, shape):
+    """Cells holding several keys: exact duplicates (2, 3, 4, 9 copies of every
+    value: planes, overflow list), tight clusters (distinct keys that share a
+    cell and must be ordered inside it), two scales in one bucket, and one
+    cell that takes a large share of its bucket (fallback to the network)."""
+    n = 1 << 20
+    rng = np.random.default_rng(dt * 100 + len(shape))
+    wide = rng.integers(0, 2**63, size=n, dtype=np.uint64) * np.uint64(2)
+    if shape in ("pairs", "triples", "quads", "runs9"):
+        c = {"pairs": 2, "triples": 3, "quads": 4, "runs9": 9}[shape]
+        raw = np.repeat(wide[: n // c + 1], c)[:n].copy()
+        rng.shuffle(raw)
+    elif shape == "clusters":  # 2..6 distinct keys a few values apart around every centre
+        raw = wide.copy()
+        k = n // 4
+        for j in range(1, 4):
+            raw[j * k:(j + 1) * k] = raw[:k] + rng.integers(1, 50, size=k, dtype=np.uint64)
+    elif shape == "two_scales":  # half the keys spread out, half within 2^20 values of 64 centres
+        raw = wide.copy()
+        centres = rng.integers(0, 2**63, size=64, dtype=np.uint64)
+        raw[: n // 2] = centres[rng.integers(0, 64, n // 2)] + rng.integers(0, 1 << 20, size=n // 2, dtype=np.uint64)
+    else:  # hot_cell: 30 % of the keys within 1000 consecutive values
+        raw = wide.copy()
+        raw[: n * 3 // 10] = np.uint64(1 << 61) + rng.integers(0, 1000, size=n * 3 // 10, dtype=np.uint64)
+    if dt in (DT_U32, DT_I32):
+        raw = raw >> np.uint64(32)
+    a = _as_dtype(raw, dt)
+    got, m = gpu_sort(a)
+    np.testing.assert_array_equal(got, np.sort(a))
+    got, _ = gpu_sort(a, less="greater")
+    np.testing.assert_array_equal(got, np.sort(a)[::-1])
