@@ -115,6 +115,12 @@ struct Tune<uint32_t> {
 #endif
     static constexpr int CELL_CLASS = QMSORT_CELL_SORT ? 6 : kNumClasses;
     static constexpr int CELL_BIG_CLASS = kNumClasses;  // (none)
+    // even splitters at a last level: ranges of about EVEN_TARGET keys and at
+    // most EVEN_SPAN values -- table-sort buckets filling 15 of its 16 rows
+#ifndef QMSORT_U32_EVEN_TARGET
+#define QMSORT_U32_EVEN_TARGET 3700
+#endif
+    static constexpr int EVEN_TARGET = QMSORT_TABLE_SORT ? QMSORT_U32_EVEN_TARGET : 0, EVEN_SPAN = 65535;
     static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     // last level: 3/4 of the target, so most tiles stay inside the packed
     // 16-bit block sort's span (measured: block sort 1817 -> 1716 us on C2)
@@ -144,8 +150,13 @@ struct Tune<uint64_t> {
     static constexpr int TABLE_CLASS = kNumClasses;  // no dense table sort
     static constexpr int CELL_CLASS = QMSORT_CELL_SORT ? 7 : kNumClasses;
     static constexpr int CELL_BIG_CLASS = QMSORT_CELL_SORT ? 8 : kNumClasses;  // buckets beyond 2048 keys
+    static constexpr int EVEN_TARGET = 0, EVEN_SPAN = 0;  // even splitters: K ranges
     static constexpr int TARGET_DIV = 4;
-    static constexpr int LAST_NUM = 3, LAST_DEN = 4;  // measured: C4 block sort -4 %, C3 unchanged
+#ifndef QMSORT_U64_LAST_NUM
+#define QMSORT_U64_LAST_NUM 1
+#define QMSORT_U64_LAST_DEN 1
+#endif
+    static constexpr int LAST_NUM = QMSORT_U64_LAST_NUM, LAST_DEN = QMSORT_U64_LAST_DEN;  // measured with the cell sort: 1/1 (C4a +1.5 %, C4d +2.7 %, C3 +0.4 % over 3/4)
     static constexpr int ST = 512, SI = 16;
     static constexpr int XT = 512, XI = 12;  // measured: C3 scatter 14.8 -> 13.7 ms, C4a 2.55 -> 2.17 ms (was 256 x 16)
     static constexpr int CT = 256, CU = 8;
@@ -159,6 +170,7 @@ struct Tune<Rec32> {
     static constexpr int BI = 8;
     static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512, 512, 512};
     static constexpr int TABLE_CLASS = kNumClasses, CELL_CLASS = kNumClasses, CELL_BIG_CLASS = kNumClasses;
+    static constexpr int EVEN_TARGET = 0, EVEN_SPAN = 0;
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 2;  // measured: C5 block sort 2.55 -> 2.32 ms
     static constexpr int ST = 512, SI = 8;
@@ -735,7 +747,8 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
             QLAUNCH(led, kPhSample, 0,
                     (level == 0 && fused ? sample_xf_fn : sample_fn)<<<sample_grid, TU::ST, BSS::kSmemBytes, st>>>(
                         lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u, lxf,
-                        level == 0 ? presorted : nullptr, level == 0 ? presorted_n : 0u));
+                        level == 0 ? presorted : nullptr, level == 0 ? presorted_n : 0u,
+                        (uint32_t)TU::EVEN_TARGET, (uint32_t)TU::EVEN_SPAN));
             QLAUNCH(led, kPhCount, 0,
                     count_fn<<<count_grid, TU::CT, 0, st>>>(lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks,
                                                             &c->work_count, src, tree[cur], sorted[cur],
@@ -1079,7 +1092,7 @@ __global__ void given_splitters_kernel(const K* __restrict__ spl, uint32_t nspli
         d.shift = shift;
         d.lutbits = lutbits;
         d.sampler = kSampleRandom;
-        d.pad[0] = d.pad[1] = 0;
+        d.arith = d.scale = 0;
         *seg = d;
     }
 }

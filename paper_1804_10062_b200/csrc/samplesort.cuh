@@ -43,6 +43,9 @@ namespace qmsort_b200 {
 
 constexpr int kNumClasses = 9;  // block-sort size classes (Tune<K>::CLS_T)
 constexpr int kLutMaxBits = 12;
+#ifndef QMSORT_EVEN_SPLITTERS
+#define QMSORT_EVEN_SPLITTERS 1
+#endif
 constexpr int kLutPerSplitter = 16;  // LUT words reserved per splitter slot
 
 struct SegDesc {
@@ -60,7 +63,12 @@ struct SegDesc {
     uint32_t shift;        // LUT cell = (key - lo) >> shift
     uint32_t lutbits;      // 2^lutbits LUT cells
     uint32_t sampler;      // kSampleRandom or kSampleTriples (worst-case policy, f1)
-    uint32_t pad[2];
+    // Even splitters (integer keys, set by sample_kernel when the sample says
+    // the keys are spread evenly over [lo, hi]): splitter j is the largest key
+    // with ((key - lo) >> shift) * scale >> 32 <= j, so a key's bucket is that
+    // product -- no table, no splitter read.
+    uint32_t arith;
+    uint32_t scale;
 };
 
 // K1 sampling rules.  kSampleRandom: seeded random
@@ -285,7 +293,7 @@ __device__ inline bool emit_segment(const LevelBufs& nb, uint64_t off, uint64_t 
     while (bl < 64 && (span >> bl) != 0) ++bl;  // bit length of span
     d.shift = bl > d.lutbits ? bl - d.lutbits : 0;
     d.sampler = sampler;
-    d.pad[0] = d.pad[1] = 0;
+    d.arith = d.scale = 0;
     nb.segs[s] = d;
     atomicAdd(&nb.cnt->nkeys, (unsigned long long)len);
     for (uint32_t i = 0; write_chunks && i < nch; ++i) {
@@ -355,7 +363,8 @@ __device__ __forceinline__ void load_classifier(ClassifierSmem<K, LOG_KMAX>& c, 
     if constexpr (KeyTraits<K>::kLut) {
         const uint32_t nc = 1u << d.lutbits;
         const uint32_t* src = lut_store + (size_t)d.sp * kLutPerSplitter;
-        for (uint32_t i = threadIdx.x; i < nc; i += T) c.lut[i] = src[i];
+        if (!d.arith)  // even splitters need no table
+            for (uint32_t i = threadIdx.x; i < nc; i += T) c.lut[i] = src[i];
     } else {
         for (uint32_t i = threadIdx.x; i < K_; i += T) {
             const K t = tree_store[d.sp + i];
@@ -395,6 +404,14 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
         const uint32_t shift = d.shift;
         const UI cmax = (UI)((1u << d.lutbits) - 1);
         uint32_t wide = 0;  // keys whose cell straddles two or more splitters
+        if (d.arith) {  // even splitters: the bucket is a product (uniform per segment)
+            const uint32_t scale = d.scale, jm = d.m;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const UI rel = KT::bits(key[u]) - lo;
+                j[u] = min(__umulhi((uint32_t)(rel >> shift), scale), jm);  // (padding keys clamp)
+            }
+        } else
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const UI rel = KT::bits(key[u]) - lo;
@@ -467,7 +484,8 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
                                                uint32_t* lut_store, uint64_t seed,
                                                uint32_t oversample, const Xf& xf,
                                                const K* __restrict__ presorted, uint32_t presorted_n,
-                                               unsigned long long* sample_keys) {
+                                               unsigned long long* sample_keys, uint32_t even_target,
+                                               uint32_t even_span) {
     using BS = BlockSorter<K, T, ITEMS>;
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
@@ -531,6 +549,75 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
         const uint64_t w0a = at(0).w[0], w0b = at(S - 1).w[0];
         pbase = w0a;
         psh = w0b > w0a ? (uint32_t)__clzll((long long)(w0b - w0a)) : 64u;
+    }
+
+    // Even splitters (integer keys): cut [lo, hi] into K equal ranges when
+    // the sorted sample says no range would take more than about twice its
+    // share -- uniform keys then need no lookup table and no splitter compare
+    // in K2 / K4 (a bucket is still #{splitters < key}; the splitters are the
+    // ranges' upper ends).  Anything else keeps the sample's quantiles.
+    if constexpr (KT::kLut) {
+        const uint64_t span = d.hi - d.lo;
+        if (QMSORT_EVEN_SPLITTERS && span >= 2ull * K_ - 1) {
+            const uint32_t bl = 64u - (uint32_t)__clzll((long long)span);
+            const uint32_t psh = bl > 32 ? bl - 32 : 0;
+            const uint32_t span32 = (uint32_t)(span >> psh);
+            // ranges: K, or -- a last level -- as few as leave buckets of
+            // even_target keys spanning at most even_span values (the table
+            // sort's tile and table, tablesort.cuh)
+            uint32_t nr = K_;
+            if (even_target) {
+                uint64_t want = (d.len + even_target - 1) / even_target;
+                if (even_span) want = max(want, span / even_span + 1);
+                nr = (uint32_t)min((uint64_t)K_, max(want, (uint64_t)2));
+            }
+            const uint32_t scale = (uint32_t)(((uint64_t)nr << 32) / ((uint64_t)span32 + 1));
+            const uint32_t m_ar = __umulhi(span32, scale);  // the last key's bucket = splitters
+            // upper end of range j (j < m_ar) as a key
+            auto upper = [&](uint32_t j) -> uint64_t {
+                const uint64_t r = ((((uint64_t)(j + 1)) << 32) - 1) / scale;
+                return d.lo + ((r + 1) << psh) - 1;
+            };
+            __shared__ uint32_t ar_max;
+            if (threadIdx.x == 0) ar_max = 0;
+            // flags[j] = sample keys <= upper(j)
+            for (uint32_t j = threadIdx.x; j <= m_ar; j += T) {
+                uint32_t c = (uint32_t)S;
+                if (j < m_ar) {
+                    const uint64_t v = upper(j);
+                    uint32_t lo2 = 0, cnt = (uint32_t)S;
+                    while (cnt > 0) {
+                        const uint32_t half = cnt >> 1;
+                        if ((uint64_t)KT::bits(at((int)(lo2 + half))) <= v) {
+                            lo2 += half + 1;
+                            cnt -= half + 1;
+                        } else {
+                            cnt = half;
+                        }
+                    }
+                    c = lo2;
+                }
+                flags[j] = c;
+            }
+            __syncthreads();
+            for (uint32_t j = threadIdx.x; j <= m_ar; j += T)
+                atomicMax(&ar_max, flags[j] - (j ? flags[j - 1] : 0u));
+            __syncthreads();
+            const bool even = m_ar >= 1 && (uint64_t)ar_max * (m_ar + 1) <= 2ull * (uint64_t)S + 8ull * (m_ar + 1);
+            __syncthreads();
+            if (even) {
+                K* sorted = sorted_store + d.sp;
+                for (uint32_t j = threadIdx.x; j < m_ar; j += T) sorted[j] = (K)upper(j);
+                if (threadIdx.x == 0) {
+                    segs[seg].m = m_ar;
+                    segs[seg].eq = 0;
+                    segs[seg].shift = psh;
+                    segs[seg].arith = 1;
+                    segs[seg].scale = scale;
+                }
+                return;
+            }
+        }
     }
 
     // candidate splitter j (0 <= j < K-1): sample quantile (j+1)/K
@@ -611,13 +698,15 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const uint32_t
                                                    K* sorted_store, uint32_t* lut_store,
                                                    uint64_t seed, uint32_t oversample,
                                                    Xf xf = Xf{0, 0}, const K* presorted = nullptr,
-                                                   uint32_t presorted_n = 0) {
+                                                   uint32_t presorted_n = 0, uint32_t even_target = 0,
+                                                   uint32_t even_span = 0) {
     if (QMSORT_LEVEL_OVERFLOWED(nsegs, nsegs)) return;
     const uint32_t ns = *nsegs;
     LevelCounters* lc = reinterpret_cast<LevelCounters*>(const_cast<uint32_t*>(nsegs));  // nsegs is its first member
     for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
         sample_segment<K, T, ITEMS, XF>(seg, segs, src, tree_store, sorted_store, lut_store, seed,
-                                        oversample, xf, presorted, presorted_n, &lc->sample_keys);
+                                        oversample, xf, presorted, presorted_n, &lc->sample_keys, even_target,
+                                        even_span);
         __syncthreads();  // shared memory is reused by the next segment
     }
 }
