@@ -541,21 +541,12 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
             if (XF) k[i] = xf_fwd(k[i], xf);
         }
     }
-    if (!pre) BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
-    auto at = [&](int q) -> K { return pre ? presorted[q] : s[P::idx(q)]; };
-    uint64_t pbase = 0;
-    uint32_t psh = 0;
-    if constexpr (std::is_same<K, Rec32>::value) {  // prefix window of the sampled w0 range
-        const uint64_t w0a = at(0).w[0], w0b = at(S - 1).w[0];
-        pbase = w0a;
-        psh = w0b > w0a ? (uint32_t)__clzll((long long)(w0b - w0a)) : 64u;
-    }
-
-    // Even splitters (integer keys): cut [lo, hi] into K equal ranges when
-    // the sorted sample says no range would take more than about twice its
-    // share -- uniform keys then need no lookup table and no splitter compare
-    // in K2 / K4 (a bucket is still #{splitters < key}; the splitters are the
-    // ranges' upper ends).  Anything else keeps the sample's quantiles.
+    // Even splitters (integer keys): cut [lo, hi] into equal ranges when the
+    // sample says no range would take more than about twice its share --
+    // uniform keys then need no lookup table and no splitter compare in K2 /
+    // K4 (a bucket is still #{splitters < key}; the splitters are the ranges'
+    // upper ends), and the sample is only tallied, not sorted.  Anything else
+    // keeps the sample's quantiles.
     if constexpr (KT::kLut) {
         const uint64_t span = d.hi - d.lo;
         if (QMSORT_EVEN_SPLITTERS && span >= 2ull * K_ - 1) {
@@ -572,42 +563,35 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
                 nr = (uint32_t)min((uint64_t)K_, max(want, (uint64_t)2));
             }
             const uint32_t scale = (uint32_t)(((uint64_t)nr << 32) / ((uint64_t)span32 + 1));
-            const uint32_t m_ar = __umulhi(span32, scale);  // the last key's bucket = splitters
-            // upper end of range j (j < m_ar) as a key
-            auto upper = [&](uint32_t j) -> uint64_t {
-                const uint64_t r = ((((uint64_t)(j + 1)) << 32) - 1) / scale;
-                return d.lo + ((r + 1) << psh) - 1;
-            };
+            const uint32_t m_ar = __umulhi(span32, scale);  // the last key's range = splitters
             __shared__ uint32_t ar_max;
+            for (uint32_t j = threadIdx.x; j <= m_ar; j += T) flags[j] = 0;
             if (threadIdx.x == 0) ar_max = 0;
-            // flags[j] = sample keys <= upper(j)
-            for (uint32_t j = threadIdx.x; j <= m_ar; j += T) {
-                uint32_t c = (uint32_t)S;
-                if (j < m_ar) {
-                    const uint64_t v = upper(j);
-                    uint32_t lo2 = 0, cnt = (uint32_t)S;
-                    while (cnt > 0) {
-                        const uint32_t half = cnt >> 1;
-                        if ((uint64_t)KT::bits(at((int)(lo2 + half))) <= v) {
-                            lo2 += half + 1;
-                            cnt -= half + 1;
-                        } else {
-                            cnt = half;
-                        }
-                    }
-                    c = lo2;
-                }
-                flags[j] = c;
+            __syncthreads();
+            auto tally = [&](const K& key) {
+                const uint64_t rel = (uint64_t)KT::bits(key) - d.lo;
+                atomicAdd(&flags[min(__umulhi((uint32_t)(rel >> psh), scale), m_ar)], 1u);
+            };
+            if (pre) {
+                for (int q = threadIdx.x; q < S; q += T) tally(presorted[q]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i)
+                    if ((int)threadIdx.x * ITEMS + i < S) tally(k[i]);
             }
             __syncthreads();
-            for (uint32_t j = threadIdx.x; j <= m_ar; j += T)
-                atomicMax(&ar_max, flags[j] - (j ? flags[j - 1] : 0u));
+            for (uint32_t j = threadIdx.x; j <= m_ar; j += T) atomicMax(&ar_max, flags[j]);
             __syncthreads();
             const bool even = m_ar >= 1 && (uint64_t)ar_max * (m_ar + 1) <= 2ull * (uint64_t)S + 8ull * (m_ar + 1);
             __syncthreads();
             if (even) {
+                // upper end of range j (j < m_ar): the largest key with
+                // ((key - lo) >> psh) * scale >> 32 <= j
                 K* sorted = sorted_store + d.sp;
-                for (uint32_t j = threadIdx.x; j < m_ar; j += T) sorted[j] = (K)upper(j);
+                for (uint32_t j = threadIdx.x; j < m_ar; j += T) {
+                    const uint64_t r = ((((uint64_t)(j + 1)) << 32) - 1) / scale;
+                    sorted[j] = (K)(d.lo + ((r + 1) << psh) - 1);
+                }
                 if (threadIdx.x == 0) {
                     segs[seg].m = m_ar;
                     segs[seg].eq = 0;
@@ -618,6 +602,15 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
                 return;
             }
         }
+    }
+    if (!pre) BS::sort(k, s, S);  // sorted sample of S keys in s (padded)
+    auto at = [&](int q) -> K { return pre ? presorted[q] : s[P::idx(q)]; };
+    uint64_t pbase = 0;
+    uint32_t psh = 0;
+    if constexpr (std::is_same<K, Rec32>::value) {  // prefix window of the sampled w0 range
+        const uint64_t w0a = at(0).w[0], w0b = at(S - 1).w[0];
+        pbase = w0a;
+        psh = w0b > w0a ? (uint32_t)__clzll((long long)(w0b - w0a)) : 64u;
     }
 
     // candidate splitter j (0 <= j < K-1): sample quantile (j+1)/K
@@ -1119,23 +1112,36 @@ struct PeerSink {
     __device__ __forceinline__ void store_bin(uint32_t, uint32_t v, const K& key) const { store(v, key); }
 };
 
+// The m keys of a tile into registers (striped: key u of thread t is p[u T + t]).
+template <class K, int T, int U, bool XF>
+__device__ __forceinline__ void load_tile(K (&k)[U], const K* __restrict__ p, uint32_t m, const Xf& xf) {
+    const uint32_t tid = threadIdx.x;
+    if (m == (uint32_t)(T * U)) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) k[u] = XF ? xf_fwd(p[u * T + tid], xf) : p[u * T + tid];
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t li = u * T + tid;
+            k[u] = li < m ? (XF ? xf_fwd(p[li], xf) : p[li]) : KeyTraits<K>::max_key();
+        }
+    }
+}
+
+// k: the tile's keys (load_tile); once they are staged the next tile of the
+// chunk (pnext, mnext keys; 0: none) is loaded into k, so its global loads
+// are in flight during the write-out.
 template <class K, int T, int U, int LOG_KMAX, bool FULL, bool XF, class Sink, bool RAW = false>
 __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm, const SegDesc& d,
                                              const K* __restrict__ p, uint32_t m,
                                              const Sink& out,
                                              uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT],
-                                             const Xf& xf) {
+                                             const Xf& xf, K (&k)[U], const K* __restrict__ pnext,
+                                             uint32_t mnext) {
     using SM = ScatterSmem<K, T, U, LOG_KMAX>;
     constexpr int BPT = SM::BPT;
     const uint32_t tid = threadIdx.x;
-    K k[U];
     uint32_t bin[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const uint32_t li = u * T + tid;
-        if (FULL) k[u] = XF ? xf_fwd(p[li], xf) : p[li];
-        else k[u] = li < m ? (XF ? xf_fwd(p[li], xf) : p[li]) : KeyTraits<K>::max_key();
-    }
     classify_keys<K, LOG_KMAX, U>(k, sm.cls, d, bin);
     // rank within the tile's bucket; pack (bin, rank) into one word
     if (((1u << d.logk) << d.eq) <= 64) {
@@ -1156,6 +1162,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
             // them with the fused transform); local levels store core keys
             if (v) out.store_bin(bin[u], base[bin[u]] + r, RAW && XF ? xf_inv(k[u], xf) : k[u]);
         }
+        if (mnext) load_tile<K, T, U, XF>(k, pnext, mnext, xf);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < BPT; ++i) {
@@ -1209,6 +1216,50 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         vec_store<BPT>(&sm.hist[tid * BPT], z);
     }
     __syncthreads();
+    if constexpr (KeyTraits<K>::kLut && QMSORT_SCATTER_BINREC) {
+        // Even splitters: a key's bin is a product of the key, so the staged
+        // record is the key alone (8-byte keys: its tile index) -- 4 bytes
+        // through shared memory instead of 8; the write-out recomputes the bin.
+        if (d.arith) {
+            using KT = KeyTraits<K>;
+            using UI = typename KT::UInt;
+            uint32_t* st4 = reinterpret_cast<uint32_t*>(sm.stage);
+            const uint32_t* binstart = reinterpret_cast<const uint32_t*>(sm.sd);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (FULL || u * T + tid < m) {
+                    const uint32_t pos = binstart[bin[u] >> 16] + (bin[u] & 0xFFFFu);
+                    QCHECK(pos < m, pos, m);
+                    if constexpr (SM::kStageIndex) st4[pos] = u * T + tid;
+                    else st4[pos] = (uint32_t)k[u];
+                }
+            }
+            if (mnext) load_tile<K, T, U, XF>(k, pnext, mnext, xf);
+            __syncthreads();
+            const UI lo = (UI)d.lo;
+            const uint32_t psh = d.shift, scale = d.scale, jm = d.m;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = u * T + tid;
+                if (FULL || i < m) {
+                    const uint32_t v = st4[i];
+                    K raw, core;
+                    if constexpr (SM::kStageIndex) {
+                        raw = p[v];
+                        core = XF ? xf_fwd(raw, xf) : raw;
+                    } else {
+                        core = (K)v;
+                        raw = XF ? xf_inv(core, xf) : core;
+                    }
+                    const uint32_t b = min(__umulhi((uint32_t)((UI)(KT::bits(core) - lo) >> psh), scale), jm);
+                    const uint32_t dest = binstart[SM::NB + b] + i;
+                    out.store(dest, RAW && XF ? raw : core);
+                }
+            }
+            __syncthreads();
+            return;
+        }
+    }
     typename SM::Rec* stage = sm.stage;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1231,6 +1282,7 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
             stage[pos] = r;
         }
     }
+    if (mnext) load_tile<K, T, U, XF>(k, pnext, mnext, xf);
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -1247,6 +1299,32 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         }
     }
     __syncthreads();
+    }
+}
+
+// The tiles of one chunk, software-pipelined: tile t+1's keys are loaded
+// while tile t is written out.
+template <class K, int T, int U, int LOG_KMAX, bool XF, class Sink, bool RAW>
+__device__ __forceinline__ void scatter_chunk(ScatterSmem<K, T, U, LOG_KMAX>& sm, const SegDesc& d,
+                                              const K* __restrict__ p, uint32_t len, const Sink& out,
+                                              uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT],
+                                              const Xf& xf) {
+    constexpr uint32_t TILE = (uint32_t)T * U;
+    // 4-byte keys only (measured: C2 scatter 1476 -> 1348 us; 8- and 32-byte
+    // keys, whose registers the write-out needs, lose 1-5 %)
+    constexpr bool kPrefetch = sizeof(K) == 4;
+    K k[U];
+    if (kPrefetch) load_tile<K, T, U, XF>(k, p, min(len, TILE), xf);
+    for (uint32_t t0 = 0; t0 < len;) {
+        const uint32_t m = min(TILE, len - t0);
+        const uint32_t nx = t0 + m;
+        const uint32_t mn = kPrefetch ? min(TILE, len - nx) : 0u;  // 0 after the last tile
+        if (!kPrefetch) load_tile<K, T, U, XF>(k, p + t0, m, xf);
+        if (m == TILE)
+            scatter_tile<K, T, U, LOG_KMAX, true, XF, Sink, RAW>(sm, d, p + t0, m, out, cursor, xf, k, p + nx, mn);
+        else
+            scatter_tile<K, T, U, LOG_KMAX, false, XF, Sink, RAW>(sm, d, p + t0, m, out, cursor, xf, k, p + nx, mn);
+        t0 = nx;
     }
 }
 
@@ -1306,35 +1384,20 @@ __global__ void __launch_bounds__(T, T >= 1024 ? 1 : T >= 512 ? 2 : (sizeof(K) >
 
         const K* p = src + c.begin;
         const uint32_t len = (uint32_t)(c.end - c.begin);
-        uint32_t t0 = 0;
         if constexpr (PEER) {
             const PeerSink<K> out{peer_dmv, peer_vb, peers.nranks};
-            if ((xf.a | xf.b) && peers.raw) {  // ship the caller's keys
-                for (; t0 + TILE <= len; t0 += TILE)
-                    scatter_tile<K, T, U, LOG_KMAX, true, true, PeerSink<K>, true>(sm, d, p + t0, TILE, out, cursor, xf);
-                if (t0 < len)
-                    scatter_tile<K, T, U, LOG_KMAX, false, true, PeerSink<K>, true>(sm, d, p + t0, len - t0, out, cursor, xf);
-            } else if (xf.a | xf.b) {  // ship core keys
-                for (; t0 + TILE <= len; t0 += TILE)
-                    scatter_tile<K, T, U, LOG_KMAX, true, true, PeerSink<K>, false>(sm, d, p + t0, TILE, out, cursor, xf);
-                if (t0 < len)
-                    scatter_tile<K, T, U, LOG_KMAX, false, true, PeerSink<K>, false>(sm, d, p + t0, len - t0, out, cursor, xf);
-            } else {
-                for (; t0 + TILE <= len; t0 += TILE)
-                    scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
-                if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
-            }
+            if ((xf.a | xf.b) && peers.raw)  // ship the caller's keys
+                scatter_chunk<K, T, U, LOG_KMAX, true, PeerSink<K>, true>(sm, d, p, len, out, cursor, xf);
+            else if (xf.a | xf.b)  // ship core keys
+                scatter_chunk<K, T, U, LOG_KMAX, true, PeerSink<K>, false>(sm, d, p, len, out, cursor, xf);
+            else
+                scatter_chunk<K, T, U, LOG_KMAX, false, PeerSink<K>, false>(sm, d, p, len, out, cursor, xf);
         } else {
             const LocalSink<K> out{dst + d.off, d.len};
-            if (xf.a | xf.b) {  // level 0 of a fused-transform sort
-                for (; t0 + TILE <= len; t0 += TILE)
-                    scatter_tile<K, T, U, LOG_KMAX, true, true>(sm, d, p + t0, TILE, out, cursor, xf);
-                if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, true>(sm, d, p + t0, len - t0, out, cursor, xf);
-            } else {
-                for (; t0 + TILE <= len; t0 += TILE)
-                    scatter_tile<K, T, U, LOG_KMAX, true, false>(sm, d, p + t0, TILE, out, cursor, xf);
-                if (t0 < len) scatter_tile<K, T, U, LOG_KMAX, false, false>(sm, d, p + t0, len - t0, out, cursor, xf);
-            }
+            if (xf.a | xf.b)  // level 0 of a fused-transform sort
+                scatter_chunk<K, T, U, LOG_KMAX, true, LocalSink<K>, false>(sm, d, p, len, out, cursor, xf);
+            else
+                scatter_chunk<K, T, U, LOG_KMAX, false, LocalSink<K>, false>(sm, d, p, len, out, cursor, xf);
         }
     }
 }
