@@ -107,8 +107,8 @@ typedef struct {
     uint64_t sample_keys; /* splitter-sample keys drawn over all levels (median_of_3:
                              32 K per segment; median_of_sqrt_n: 2 floor(sqrt(len)/2)+1,
                              the reference's s, partition.hpp:240-241) */
-    uint32_t table_buckets; /* uint32 buckets sorted by the comparison-free table sort
-                               (tablesort.cuh) instead of the network */
+    uint32_t table_buckets; /* integer-key buckets sent to the comparison-free table / cell
+                               sorts (tablesort.cuh) instead of the network */
     uint32_t reserved;
 } qmsort_gpu_metrics;
 

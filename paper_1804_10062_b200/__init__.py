@@ -163,7 +163,7 @@ class Metrics:
     phase_launches: list = dataclasses.field(default_factory=lambda: [0] * _lib.NUM_PHASES)
     resplits: int = 0  # hybrid pivot: buckets re-sampled with triple medians (f1)
     sample_keys: int = 0  # splitter-sample keys drawn (median_of_sqrt_n: the reference's s per segment)
-    table_buckets: int = 0  # uint32 buckets sorted by the comparison-free table sort (tablesort.cuh)
+    table_buckets: int = 0  # integer-key buckets sent to the comparison-free table / cell sorts (tablesort.cuh)
 
     @classmethod
     def from_c(cls, m: _lib.GpuMetrics) -> "Metrics":

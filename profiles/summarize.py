@@ -133,5 +133,35 @@ def main() -> None:
     print(json.dumps({k: (v / tot) for k, v in fam.items()}), tot)
 
 
+def configs(prefix: str, rnd: str) -> None:
+    """The other configs' bench lines (scripts/gpu_profile.sh: cfg_*, merge_*, sharded_*)
+    condensed into profiles/r<round>_configs.json."""
+    out = {}
+    for f in sorted(os.listdir(G)):
+        if not (f.startswith(prefix + "_") and f.endswith(".json")):
+            continue
+        tag = f[len(prefix) + 1:-5]
+        if not tag.startswith(("cfg_", "merge_", "sharded_")):
+            continue
+        try:
+            d = json.loads(open(os.path.join(G, f)).read().strip().splitlines()[-1])
+        except (ValueError, IndexError):
+            continue
+        e = {k: d[k] for k in ("value", "unit", "ms_per_step", "config") if k in d}
+        if "sort_roofline" in d:
+            e["sort_roofline_frac"] = d["sort_roofline"]["frac"]
+            e["phases_us"] = {k: v["us"] for k, v in d["sort_roofline"]["phases"].items()}
+            r = d.get("roofline", {})
+            e["dominant"] = {k: r.get(k) for k in ("kernel", "achieved", "frac", "avg_launch_us")}
+        else:
+            for k in ("verify", "roofline"):
+                if k in d:
+                    e[k] = d[k]
+        out[tag] = e
+    if out:
+        json.dump(out, open(os.path.join(P, f"r{rnd}_configs.json"), "w"), indent=1)
+
+
 if __name__ == "__main__":
     main()
+    configs(sys.argv[1], sys.argv[2])
