@@ -353,6 +353,41 @@ __device__ __forceinline__ uint64_t rec_prefix(const Rec32& r, uint64_t base, ui
     return (d0 << psh) | (r.w[1] >> (64 - psh));
 }
 
+// The largest record whose prefix (rec_prefix with base, psh) is p: the upper
+// end of an even range of record prefixes as a splitter record.
+__device__ __forceinline__ Rec32 rec_from_prefix(uint64_t p, uint64_t base, uint32_t psh) {
+    Rec32 r;
+    if (psh == 0) {
+        r.w[0] = base + p;
+        r.w[1] = ~0ull;
+    } else if (psh >= 64) {
+        r.w[0] = base;
+        r.w[1] = p;
+    } else {
+        r.w[0] = base + (p >> psh);
+        r.w[1] = (p << (64 - psh)) | ((1ull << (64 - psh)) - 1);
+    }
+    r.w[2] = r.w[3] = ~0ull;
+    return r;
+}
+
+// Bucket of a key in an even-splitter segment (SegDesc::arith): integers
+// ((key - lo) >> shift) * scale >> 32; records the same product of their
+// prefix's distance from the sample's smallest prefix (hi) >> lutbits.
+template <class K>
+__device__ __forceinline__ uint32_t even_bucket(const K& key, const SegDesc& d) {
+    using KT = KeyTraits<K>;
+    if constexpr (KT::kLut) {
+        using UI = typename KT::UInt;
+        const UI rel = KT::bits(key) - (UI)d.lo;
+        return min(__umulhi((uint32_t)(rel >> d.shift), d.scale), d.m);  // (padding keys clamp)
+    } else {
+        const uint64_t pk = rec_prefix(key, d.lo, d.shift);
+        const uint64_t rel = pk > d.hi ? pk - d.hi : 0;
+        return min(__umulhi((uint32_t)(rel >> d.lutbits), d.scale), d.m);
+    }
+}
+
 template <class K, int LOG_KMAX, int T>
 __device__ __forceinline__ void load_classifier(ClassifierSmem<K, LOG_KMAX>& c, const SegDesc& d,
                                                 const K* __restrict__ tree_store,
@@ -365,7 +400,7 @@ __device__ __forceinline__ void load_classifier(ClassifierSmem<K, LOG_KMAX>& c, 
         const uint32_t* src = lut_store + (size_t)d.sp * kLutPerSplitter;
         if (!d.arith)  // even splitters need no table
             for (uint32_t i = threadIdx.x; i < nc; i += T) c.lut[i] = src[i];
-    } else {
+    } else if (!d.arith) {
         for (uint32_t i = threadIdx.x; i < K_; i += T) {
             const K t = tree_store[d.sp + i];
             c.tree[i] = t;
@@ -405,12 +440,8 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
         const UI cmax = (UI)((1u << d.lutbits) - 1);
         uint32_t wide = 0;  // keys whose cell straddles two or more splitters
         if (d.arith) {  // even splitters: the bucket is a product (uniform per segment)
-            const uint32_t scale = d.scale, jm = d.m;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const UI rel = KT::bits(key[u]) - lo;
-                j[u] = min(__umulhi((uint32_t)(rel >> shift), scale), jm);  // (padding keys clamp)
-            }
+            for (int u = 0; u < U; ++u) j[u] = even_bucket<K>(key[u], d);
         } else
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -439,6 +470,9 @@ __device__ __forceinline__ void classify_keys(const K (&key)[U],
                 j[u] = jj;
             }
         }
+    } else if (d.arith) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) j[u] = even_bucket<K>(key[u], d);
     } else {
         // Eytzinger walk on the splitters' prefixes; the full record compare
         // only where a key's prefix equals the node's
@@ -600,6 +634,84 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
                     segs[seg].scale = scale;
                 }
                 return;
+            }
+        }
+    }
+    if constexpr (std::is_same<K, Rec32>::value) {
+        // Records: the same test on the sample's 64-bit prefixes, over the
+        // range [smallest, largest] sampled prefix; the splitters are the
+        // largest records of the even prefix ranges, a record's bucket the
+        // product of its prefix (records outside the sampled range clamp
+        // into the end buckets, which keeps the buckets monotone).
+        if (QMSORT_EVEN_SPLITTERS && !pre) {
+            __shared__ unsigned long long rmin, rmax;
+            __shared__ uint32_t rec_max;
+            auto minmax = [&](auto&& f) {
+                if (threadIdx.x == 0) {
+                    rmin = ~0ull;
+                    rmax = 0;
+                }
+                __syncthreads();
+                unsigned long long lo2 = ~0ull, hi2 = 0;
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i)
+                    if ((int)threadIdx.x * ITEMS + i < S) {
+                        const unsigned long long v = f(k[i]);
+                        lo2 = min(lo2, v);
+                        hi2 = max(hi2, v);
+                    }
+                if (lo2 <= hi2) {
+                    atomicMin(&rmin, lo2);
+                    atomicMax(&rmax, hi2);
+                }
+                __syncthreads();
+            };
+            minmax([](const Rec32& r) { return (unsigned long long)r.w[0]; });
+            const uint64_t base = rmin;
+            const uint32_t wsh = rmax > rmin ? (uint32_t)__clzll((long long)(rmax - rmin)) : 64u;
+            __syncthreads();
+            minmax([&](const Rec32& r) { return (unsigned long long)rec_prefix(r, base, wsh); });
+            const uint64_t plo = rmin, span = rmax - rmin;
+            __syncthreads();
+            if (span >= 2ull * K_ - 1) {
+                const uint32_t bl = 64u - (uint32_t)__clzll((long long)span);
+                const uint32_t psh2 = bl > 32 ? bl - 32 : 0;
+                const uint32_t span32 = (uint32_t)(span >> psh2);
+                const uint32_t scale = (uint32_t)(((uint64_t)K_ << 32) / ((uint64_t)span32 + 1));
+                const uint32_t m_ar = __umulhi(span32, scale);
+                for (uint32_t j = threadIdx.x; j <= m_ar; j += T) flags[j] = 0;
+                if (threadIdx.x == 0) rec_max = 0;
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < ITEMS; ++i)
+                    if ((int)threadIdx.x * ITEMS + i < S) {
+                        const uint64_t rel = rec_prefix(k[i], base, wsh) - plo;
+                        atomicAdd(&flags[min(__umulhi((uint32_t)(rel >> psh2), scale), m_ar)], 1u);
+                    }
+                __syncthreads();
+                for (uint32_t j = threadIdx.x; j <= m_ar; j += T) atomicMax(&rec_max, flags[j]);
+                __syncthreads();
+                const bool even =
+                    m_ar >= 1 && (uint64_t)rec_max * (m_ar + 1) <= 2ull * (uint64_t)S + 8ull * (m_ar + 1);
+                __syncthreads();
+                if (even) {
+                    K* sorted = sorted_store + d.sp;
+                    for (uint32_t j = threadIdx.x; j < m_ar; j += T) {
+                        const uint64_t r = ((((uint64_t)(j + 1)) << 32) - 1) / scale;
+                        sorted[j] = rec_from_prefix(plo + (((r + 1) << psh2) - 1), base, wsh);
+                    }
+                    if (threadIdx.x == 0) {
+                        segs[seg].m = m_ar;
+                        segs[seg].eq = 0;
+                        segs[seg].lo = base;
+                        segs[seg].shift = wsh;
+                        segs[seg].hi = plo;
+                        segs[seg].lutbits = psh2;
+                        segs[seg].arith = 1;
+                        segs[seg].scale = scale;
+                    }
+                    return;
+                }
             }
         }
     }
@@ -1216,13 +1328,11 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         vec_store<BPT>(&sm.hist[tid * BPT], z);
     }
     __syncthreads();
-    if constexpr (KeyTraits<K>::kLut && QMSORT_SCATTER_BINREC) {
+    if constexpr (QMSORT_SCATTER_BINREC) {
         // Even splitters: a key's bin is a product of the key, so the staged
         // record is the key alone (8-byte keys: its tile index) -- 4 bytes
         // through shared memory instead of 8; the write-out recomputes the bin.
         if (d.arith) {
-            using KT = KeyTraits<K>;
-            using UI = typename KT::UInt;
             uint32_t* st4 = reinterpret_cast<uint32_t*>(sm.stage);
             const uint32_t* binstart = reinterpret_cast<const uint32_t*>(sm.sd);
 #pragma unroll
@@ -1231,13 +1341,11 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
                     const uint32_t pos = binstart[bin[u] >> 16] + (bin[u] & 0xFFFFu);
                     QCHECK(pos < m, pos, m);
                     if constexpr (SM::kStageIndex) st4[pos] = u * T + tid;
-                    else st4[pos] = (uint32_t)k[u];
+                    else memcpy(&st4[pos], &k[u], 4);
                 }
             }
             if (mnext) load_tile<K, T, U, XF>(k, pnext, mnext, xf);
             __syncthreads();
-            const UI lo = (UI)d.lo;
-            const uint32_t psh = d.shift, scale = d.scale, jm = d.m;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint32_t i = u * T + tid;
@@ -1248,10 +1356,10 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
                         raw = p[v];
                         core = XF ? xf_fwd(raw, xf) : raw;
                     } else {
-                        core = (K)v;
+                        memcpy(&core, &v, 4);
                         raw = XF ? xf_inv(core, xf) : core;
                     }
-                    const uint32_t b = min(__umulhi((uint32_t)((UI)(KT::bits(core) - lo) >> psh), scale), jm);
+                    const uint32_t b = even_bucket<K>(core, d);
                     const uint32_t dest = binstart[SM::NB + b] + i;
                     out.store(dest, RAW && XF ? raw : core);
                 }
