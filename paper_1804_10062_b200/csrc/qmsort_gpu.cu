@@ -169,7 +169,12 @@ struct Tune<Rec32> {
     static constexpr int LOGKMAX = 8;
     static constexpr int BI = 8;
     static constexpr int CLS_T[kNumClasses] = {64, 96, 128, 256, 512, 512, 512, 512, 512};
-    static constexpr int TABLE_CLASS = kNumClasses, CELL_CLASS = kNumClasses, CELL_BIG_CLASS = kNumClasses;
+#ifndef QMSORT_REC_CELL_SORT
+#define QMSORT_REC_CELL_SORT 1
+#endif
+    // task list 7: buckets of 256..2048 records for the cell sort on record prefixes
+    static constexpr int TABLE_CLASS = kNumClasses, CELL_CLASS = QMSORT_REC_CELL_SORT ? 7 : kNumClasses,
+                         CELL_BIG_CLASS = kNumClasses;
     static constexpr int EVEN_TARGET = 0, EVEN_SPAN = 0;
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 2;  // measured: C5 block sort 2.55 -> 2.32 ms
@@ -467,7 +472,7 @@ static int launch_class(const SortTask* tasks, uint32_t count, K* A, const K* B,
                 tablesort_tasks_kernel<<<count, TableSort::T, TableSort::kSmemBytes, st>>>(tasks, A, B, xf));
         return QMSORT_OK;
     }
-    if constexpr (KeyTraits<K>::kLut && (C == TU::CELL_CLASS || C == TU::CELL_BIG_CLASS)) {
+    if constexpr (C == TU::CELL_CLASS || C == TU::CELL_BIG_CLASS) {
         constexpr bool BIG = C == TU::CELL_BIG_CLASS;
         using CS = CellSort<K, BIG>;
         auto fn = cellsort_tasks_kernel<K, BIG>;
@@ -619,7 +624,9 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
         p.cell_big_cap = (uint32_t)CellSort<K, true>::kCap;
         p.cell_big_bits = (uint32_t)CellSort<K, true>::kCellBits;
     } else {
-        p.cell_cap = p.cell_bits = p.cell_big_cap = p.cell_big_bits = 0;
+        p.cell_cap = (uint32_t)CellSort<K>::kCap;
+        p.cell_bits = (uint32_t)CellSort<K>::kCellBits;
+        p.cell_big_cap = p.cell_big_bits = 0;
     }
     p.cell_big_class = (uint32_t)TU::CELL_BIG_CLASS;
 

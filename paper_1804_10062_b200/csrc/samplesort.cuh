@@ -1037,6 +1037,9 @@ __global__ void __launch_bounds__(T) plan_kernel(const SegDesc* __restrict__ seg
                 else if (p.cell_big_class < (uint32_t)kNumClasses && len > p.cell_cap &&
                          cell_sort_eligible(len, klo, khi, p.cell_big_cap, p.cell_big_bits)) cls = p.cell_big_class;
             }
+            // records: the cell sort finds the bucket's prefix bounds itself
+            if (!KeyTraits<K>::kLut && p.cell_class < (uint32_t)kNumClasses && len >= 256u && len <= p.cell_cap)
+                cls = p.cell_class;
             sl = (cls << 28) | atomicAdd(&cls_count[cls], 1u);
             atomicAdd(&cls_keys, (unsigned long long)len);
         }

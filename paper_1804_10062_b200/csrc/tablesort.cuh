@@ -279,13 +279,82 @@ struct CellShape {
     static constexpr int T = BIG ? 512 : 256;
     static constexpr int ITEMS = sizeof(K) == 4 || BIG ? 16 : 8;
     static constexpr int kCellBits = sizeof(K) == 4 || BIG ? 16 : 15;
-    static constexpr int kMinCtas = BIG ? 2 : (sizeof(K) == 4 ? 4 : 5);
+    static constexpr int kMinCtas = BIG || sizeof(K) > 8 ? 2 : (sizeof(K) == 4 ? 4 : 5);
+};
+
+// What a key's cell is computed from: integer keys -- their bits, within the
+// bounds the plan passes with the task; records -- the 64-bit prefix of
+// (w0 - smallest w0, w1) (rec_prefix), within the bucket's smallest and
+// largest prefix, both found by the CTA once the bucket is in registers.
+template <class K>
+struct CellBounds {
+    using UI = typename KeyTraits<K>::UInt;
+    UI klo, span;
+    uint32_t sh;
+    template <int ITEMS, class SM>
+    __device__ __forceinline__ bool prepare(const K (&)[ITEMS], int, SM&, int, int) {
+        return true;
+    }
+    __device__ __forceinline__ UI proj(const K& k) const { return KeyTraits<K>::bits(k); }
+};
+template <>
+struct CellBounds<Rec32> {
+    using UI = uint64_t;
+    uint64_t klo, span;
+    uint32_t sh;
+    uint64_t base;
+    uint32_t wsh;
+    __device__ __forceinline__ uint64_t proj(const Rec32& r) const { return rec_prefix(r, base, wsh); }
+    // block-wide smallest / largest f(key) over the bucket's keys
+    template <int ITEMS, class SM, class F>
+    __device__ __forceinline__ void minmax(const Rec32 (&k)[ITEMS], int m, SM& sm, int T, F&& f, uint64_t& lo,
+                                           uint64_t& hi) {
+        if (threadIdx.x == 0) {
+            sm.red[0] = ~0ull;
+            sm.red[1] = 0;
+        }
+        __syncthreads();
+        unsigned long long a = ~0ull, b = 0;
+#pragma unroll
+        for (int u = 0; u < ITEMS; ++u)
+            if (u * T + (int)threadIdx.x < m) {
+                const unsigned long long v = f(k[u]);
+                a = min(a, v);
+                b = max(b, v);
+            }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if ((threadIdx.x & 31) == 0 && a <= b) {
+            atomicMin(&sm.red[0], a);
+            atomicMax(&sm.red[1], b);
+        }
+        __syncthreads();
+        lo = sm.red[0];
+        hi = sm.red[1];
+        __syncthreads();
+    }
+    template <int ITEMS, class SM>
+    __device__ __forceinline__ bool prepare(const Rec32 (&k)[ITEMS], int m, SM& sm, int T, int cell_bits) {
+        uint64_t lo, hi;
+        minmax(k, m, sm, T, [](const Rec32& r) { return (unsigned long long)r.w[0]; }, lo, hi);
+        base = lo;
+        wsh = hi > lo ? (uint32_t)__clzll((long long)(hi - lo)) : 64u;
+        minmax(k, m, sm, T, [&](const Rec32& r) { return (unsigned long long)rec_prefix(r, base, wsh); }, lo, hi);
+        klo = lo;
+        span = hi - lo;
+        sh = cell_shift((uint32_t)m, span, (uint32_t)cell_bits);
+        return (span >> sh) >= 4ull * (uint64_t)m;  // else most cells hold several records
+    }
 };
 
 template <class K, bool BIG = false>
 struct CellSort {
     using KT = KeyTraits<K>;
-    using UI = typename KT::UInt;
+    using BD = CellBounds<K>;
+    using UI = typename BD::UI;
     using SH = CellShape<K, BIG>;
     static constexpr int T = SH::T, ITEMS = SH::ITEMS, kCap = T * ITEMS;
     static constexpr int kPlanes = 3;
@@ -302,12 +371,12 @@ struct CellSort {
         uint32_t fix[kFixCap];  // first slot | keys << 16 of the cells holding several keys
         K ovfk[kOvfCap];        // fourth and later keys of a cell
         uint32_t ovf[kOvfCap];  // ... and their cells
+        unsigned long long red[2];
         uint32_t warp_sums[T / 32];
         uint32_t novf, nfix;
     };
     using Net = BlockSorter<K, T, ITEMS>;
-    static_assert(Net::kSmemBytes <= (sizeof(uint2) + 2 * sizeof(uint32_t)) * kWords + sizeof(K) * kCap,
-                  "fallback tile");
+    static_assert(Net::kSmemBytes <= sizeof(Smem), "fallback tile");
     static constexpr size_t kSmemBytes = sizeof(Smem);
 
     // Word w lives in cell w ^ s(w): the scan's per-thread walks over kWpt
@@ -318,16 +387,16 @@ struct CellSort {
         return kWpt == 8 ? w ^ ((w >> 4) & 7u) : w ^ ((w >> 4) & 3u);
     }
 
-    __device__ __noinline__ static uint32_t later_copy(Smem& sm, uint32_t a, uint32_t bit, uint32_t v, K key) {
+    // A key that found its cell's bit set: its copy number (1, 2), or 3 | the
+    // overflow-list slot reserved for it << 2 (the caller stores the key: it
+    // stays in registers).
+    __device__ __noinline__ static uint32_t later_copy(Smem& sm, uint32_t a, uint32_t bit, uint32_t v) {
         atomicAdd(&sm.cell[a].y, 0x10000u);
         if (!(atomicOr(&sm.y2[a], bit) & bit)) return 1u;
         if (!(atomicOr(&sm.y3[a], bit) & bit)) return 2u;
         const uint32_t i = atomicAdd(&sm.novf, 1u);
-        if (i < (uint32_t)kOvfCap) {
-            sm.ovf[i] = v;
-            sm.ovfk[i] = key;
-        }
-        return 3u;
+        if (i < (uint32_t)kOvfCap) sm.ovf[i] = v;
+        return 3u | (i << 2);
     }
     // overflow entries in cells below v of v's word / in cell v
     __device__ __noinline__ static uint32_t ovf_below(const Smem& sm, uint32_t v, uint32_t L) {
@@ -366,13 +435,10 @@ struct CellSort {
     // src may alias dst.  Returns false with nothing written when the bucket
     // has to be sorted by the network.
     __device__ __forceinline__ static bool sort(const K* __restrict__ src, K* __restrict__ dst, const int m, Smem& sm,
-                                                const UI klo, const UI span, const uint32_t sh, const Xf& xf) {
+                                                BD& bd, const Xf& xf) {
         const int tid = threadIdx.x;
         const uint32_t cells = (uint32_t)__cvta_generic_to_shared(sm.cell);
         const uint32_t outs = (uint32_t)__cvta_generic_to_shared(sm.out);
-        const uint32_t vspan = (uint32_t)(span >> sh);  // last cell
-        const uint32_t W = (vspan >> 5) + 1;
-        const uint32_t Wc = (W + (uint32_t)kWpt - 1u) & ~((uint32_t)kWpt - 1u);
         const int rows = (m + T - 1) / T;
         K k[ITEMS];
         {
@@ -381,6 +447,12 @@ struct CellSort {
             for (int u = 0; u < ITEMS; ++u)
                 if (u * T + tid < m) k[u] = p[u * T];
         }
+        if (!bd.prepare(k, m, sm, T, kCellBits)) return false;
+        const UI klo = bd.klo, span = bd.span;
+        const uint32_t sh = bd.sh;
+        const uint32_t vspan = (uint32_t)(span >> sh);  // last cell
+        const uint32_t W = (vspan >> 5) + 1;
+        const uint32_t Wc = (W + (uint32_t)kWpt - 1u) & ~((uint32_t)kWpt - 1u);
         for (uint32_t i = tid; i < Wc; i += T) {
             sm.cell[i] = make_uint2(0, 0);
             sm.y2[i] = 0;
@@ -397,12 +469,16 @@ struct CellSort {
 #pragma unroll
         for (int u = 0; u < ITEMS; ++u) {
             if (u < rows && u * T + tid < m) {
-                const UI rel = KT::bits(k[u]) - klo;
+                const UI rel = bd.proj(k[u]) - klo;
                 oob |= rel > span;
                 const uint32_t v = (uint32_t)(min(rel, span) >> sh);
                 const uint32_t a = cell_of(v >> 5);
                 const uint32_t bit = 1u << (v & 31u);
-                if (smem_atom_or(cells + a * 8u, bit) & bit) cp |= later_copy(sm, a, bit, v, k[u]) << (2 * u);
+                if (smem_atom_or(cells + a * 8u, bit) & bit) {
+                    const uint32_t c = later_copy(sm, a, bit, v);
+                    cp |= (c & 3u) << (2 * u);
+                    if ((c & 3u) == 3u && (c >> 2) < (uint32_t)kOvfCap) sm.ovfk[c >> 2] = k[u];
+                }
             }
         }
         const int bad = __syncthreads_or(oob ? 1 : 0);
@@ -447,14 +523,17 @@ struct CellSort {
         for (int u = 0; u < ITEMS; ++u) {
             if (u < rows && u * T + tid < m) {
                 const uint32_t copy = (cp >> (2 * u)) & 3u;
-                const uint32_t v = (uint32_t)((KT::bits(k[u]) - klo) >> sh);
+                const uint32_t v = (uint32_t)((bd.proj(k[u]) - klo) >> sh);
                 const uint32_t a = cell_of(v >> 5);
                 const uint2 c = smem_ld64(cells + a * 8u);
                 const uint32_t below = ~(0xFFFFFFFFu << (v & 31u));
                 uint32_t pos = (c.y & 0xFFFFu) + (uint32_t)__popc(c.x & below);
                 if (c.y >> 16) pos += slow_rank(sm, a, v, copy, pos, L);
                 QCHECK(copy == 3u || pos < (uint32_t)m, pos, m);
-                if (copy != 3u) smem_st_key(outs + pos * (uint32_t)sizeof(K), k[u]);
+                if (copy != 3u) {
+                    if constexpr (sizeof(K) <= 8) smem_st_key(outs + pos * (uint32_t)sizeof(K), k[u]);
+                    else sm.out[pos] = k[u];
+                }
             }
         }
         for (uint32_t i = tid; i < L; i += T) {  // fourth and later keys of a cell
@@ -504,10 +583,15 @@ __global__ void __launch_bounds__(CellShape<K, BIG>::T, CellShape<K, BIG>::kMinC
     const SortTask t = tasks[blockIdx.x];
     QCHECK(t.len <= (uint32_t)CS::kCap, t.len, CS::kCap);
     const K* src = (t.in_a ? A : B) + t.off;
-    using UI = typename CS::UI;
-    const uint64_t span = t.khi - t.klo;
-    if (CS::sort(src, A + t.off, (int)t.len, sm, (UI)t.klo, (UI)span, cell_shift(t.len, span, CS::kCellBits), xf))
-        return;
+    typename CS::BD bd;
+    if constexpr (KeyTraits<K>::kLut) {
+        using UI = typename CS::UI;
+        const uint64_t span = t.khi - t.klo;
+        bd.klo = (UI)t.klo;
+        bd.span = (UI)span;
+        bd.sh = cell_shift(t.len, span, CS::kCellBits);
+    }
+    if (CS::sort(src, A + t.off, (int)t.len, sm, bd, xf)) return;
     __syncthreads();
     CS::Net::sort_tile(src, A + t.off, (int)t.len, reinterpret_cast<K*>(smem_raw), xf);
 }

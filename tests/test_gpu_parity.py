@@ -401,3 +401,34 @@ def test_cell_sort_crowded_cells(oracle, dt, shape):
     np.testing.assert_array_equal(got, np.sort(a))
     got, _ = gpu_sort(a, less="greater")
     np.testing.assert_array_equal(got, np.sort(a)[::-1])
+
+
+@pytest.mark.parametrize("shape", ["c5", "const_w0", "wide_w0", "outliers", "two_w0", "dup_prefix"])
+@pytest.mark.parametrize("n", [1 << 18, (1 << 20) + 777])
+def test_record_even_splitters(oracle, shape, n):
+    """Records under even splitters (K1 cuts the sampled prefix range into
+    equal parts): the C5 shape (12-bit w0), one w0 for all records (the prefix
+    is w1), w0 over all 64 bits, a few records far outside the sampled prefix
+    range on both sides (they clamp into the end buckets), two distant w0
+    values (an uneven sample: quantile splitters), and records that agree on
+    the whole prefix and differ only in w2 / w3."""
+    rng = np.random.default_rng(n + len(shape))
+    r = rng.integers(0, 2**63, size=(n, 4), dtype=np.uint64) * np.uint64(2)
+    if shape == "c5":
+        r[:, 0] >>= np.uint64(52)
+    elif shape == "const_w0":
+        r[:, 0] = np.uint64(0xABCDEF)
+    elif shape == "outliers":
+        r[:, 0] = np.uint64(1 << 40) + (r[:, 0] >> np.uint64(44))
+        r[:3, 0] = np.uint64(5)
+        r[3:6, 0] = np.uint64(0xFFFFFFFFFFFFFF00)
+    elif shape == "two_w0":
+        r[:, 0] = np.where(rng.integers(0, 2, n) == 1, np.uint64(7), np.uint64(1 << 62))
+    elif shape == "dup_prefix":
+        r[:, 0] >>= np.uint64(56)
+        r[:, 1] = r[:, 0] * np.uint64(0x0101010101010101)
+    want = oracle.sort(DT_REC32, r)
+    got, _ = gpu_sort(r)
+    np.testing.assert_array_equal(got, want)
+    got, _ = gpu_sort(r, less="greater")
+    np.testing.assert_array_equal(got, want[::-1])
