@@ -380,11 +380,17 @@ __device__ __forceinline__ uint32_t even_bucket(const K& key, const SegDesc& d) 
     if constexpr (KT::kLut) {
         using UI = typename KT::UInt;
         const UI rel = KT::bits(key) - (UI)d.lo;
-        return min(__umulhi((uint32_t)(rel >> d.shift), d.scale), d.m);  // (padding keys clamp)
+        const UI r = rel >> d.shift;  // < 2^32 for keys within [lo, hi]; a tile's padding keys saturate
+        const uint32_t r32 = sizeof(UI) == 8 && r > (UI)0xFFFFFFFFu ? 0xFFFFFFFFu : (uint32_t)r;
+        return min(__umulhi(r32, d.scale), d.m);
     } else {
+        // records outside the sampled prefix range clamp into the end
+        // buckets: below it rel = 0; above it the 32-bit range index
+        // saturates (a truncated index would land in an arbitrary bucket)
         const uint64_t pk = rec_prefix(key, d.lo, d.shift);
         const uint64_t rel = pk > d.hi ? pk - d.hi : 0;
-        return min(__umulhi((uint32_t)(rel >> d.lutbits), d.scale), d.m);
+        const uint64_t r = rel >> d.lutbits;
+        return min(__umulhi(r > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)r, d.scale), d.m);
     }
 }
 

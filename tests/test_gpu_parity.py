@@ -403,13 +403,14 @@ def test_cell_sort_crowded_cells(oracle, dt, shape):
     np.testing.assert_array_equal(got, np.sort(a)[::-1])
 
 
-@pytest.mark.parametrize("shape", ["c5", "const_w0", "wide_w0", "outliers", "two_w0", "dup_prefix"])
+@pytest.mark.parametrize("shape", ["c5", "const_w0", "wide_w0", "outliers", "narrow_outliers", "two_w0", "dup_prefix"])
 @pytest.mark.parametrize("n", [1 << 18, (1 << 20) + 777])
 def test_record_even_splitters(oracle, shape, n):
     """Records under even splitters (K1 cuts the sampled prefix range into
     equal parts): the C5 shape (12-bit w0), one w0 for all records (the prefix
     is w1), w0 over all 64 bits, a few records far outside the sampled prefix
-    range on both sides (they clamp into the end buckets), two distant w0
+    range on both sides (they clamp into the end buckets; narrow_outliers: so
+    far outside that the 32-bit range index saturates), two distant w0
     values (an uneven sample: quantile splitters), and records that agree on
     the whole prefix and differ only in w2 / w3."""
     rng = np.random.default_rng(n + len(shape))
@@ -422,6 +423,14 @@ def test_record_even_splitters(oracle, shape, n):
         r[:, 0] = np.uint64(1 << 40) + (r[:, 0] >> np.uint64(44))
         r[:3, 0] = np.uint64(5)
         r[3:6, 0] = np.uint64(0xFFFFFFFFFFFFFF00)
+    elif shape == "narrow_outliers":
+        # one w0 and a narrow w1 range (a small prefix span), plus records the
+        # sample misses whose prefix lies 2^34 spans above / below the range
+        r[:, 0] = np.uint64(7)
+        r[:, 1] >>= np.uint64(34)
+        r[:5, 0] = np.uint64(8)
+        r[5:8, 0] = np.uint64(6)
+        r[8:11, 1] = np.array([(1 << 40) + (1 << 29), (1 << 50) + (1 << 28), (1 << 63) + 12345], dtype=np.uint64)
     elif shape == "two_w0":
         r[:, 0] = np.where(rng.integers(0, 2, n) == 1, np.uint64(7), np.uint64(1 << 62))
     elif shape == "dup_prefix":
