@@ -150,7 +150,10 @@ struct Tune<uint64_t> {
     static constexpr int TABLE_CLASS = kNumClasses;  // no dense table sort
     static constexpr int CELL_CLASS = QMSORT_CELL_SORT ? 7 : kNumClasses;
     static constexpr int CELL_BIG_CLASS = QMSORT_CELL_SORT ? 8 : kNumClasses;  // buckets beyond 2048 keys
-    static constexpr int EVEN_TARGET = 0, EVEN_SPAN = 0;  // even splitters: K ranges
+#ifndef QMSORT_U64_EVEN_TARGET
+#define QMSORT_U64_EVEN_TARGET 0
+#endif
+    static constexpr int EVEN_TARGET = QMSORT_U64_EVEN_TARGET, EVEN_SPAN = 0;  // even splitters: K ranges
     static constexpr int TARGET_DIV = 4;
 #ifndef QMSORT_U64_LAST_NUM
 #define QMSORT_U64_LAST_NUM 1
