@@ -120,7 +120,8 @@ struct Tune<uint32_t> {
 #ifndef QMSORT_U32_EVEN_TARGET
 #define QMSORT_U32_EVEN_TARGET 3700
 #endif
-    static constexpr int EVEN_TARGET = QMSORT_TABLE_SORT ? QMSORT_U32_EVEN_TARGET : 0, EVEN_SPAN = 65535;
+    static constexpr int EVEN_TARGET = QMSORT_TABLE_SORT ? QMSORT_U32_EVEN_TARGET : 0, EVEN_SPAN = 65535,
+                         EVEN_OVER = 0;
     static constexpr int TARGET_DIV = 4;                          // target bucket = cap / 4
     // last level: 3/4 of the target, so most tiles stay inside the packed
     // 16-bit block sort's span (measured: block sort 1817 -> 1716 us on C2)
@@ -151,9 +152,13 @@ struct Tune<uint64_t> {
     static constexpr int CELL_CLASS = QMSORT_CELL_SORT ? 7 : kNumClasses;
     static constexpr int CELL_BIG_CLASS = QMSORT_CELL_SORT ? 8 : kNumClasses;  // buckets beyond 2048 keys
 #ifndef QMSORT_U64_EVEN_TARGET
-#define QMSORT_U64_EVEN_TARGET 0
+#define QMSORT_U64_EVEN_TARGET 7600
 #endif
-    static constexpr int EVEN_TARGET = QMSORT_U64_EVEN_TARGET, EVEN_SPAN = 0;  // even splitters: K ranges
+    // even splitters: K ranges; a last level that K ranges would leave with
+    // buckets over the small cell-sort tile (2048 keys) takes ranges of 7600
+    // keys instead -- the big tile 15/16 full (measured: C3 42.6 -> 45.1 Gkeys/s;
+    // applied to every last level C4 loses 7 %)
+    static constexpr int EVEN_TARGET = QMSORT_U64_EVEN_TARGET, EVEN_SPAN = 0, EVEN_OVER = 2048;
     static constexpr int TARGET_DIV = 4;
 #ifndef QMSORT_U64_LAST_NUM
 #define QMSORT_U64_LAST_NUM 1
@@ -178,7 +183,7 @@ struct Tune<Rec32> {
     // task list 7: buckets of 256..2048 records for the cell sort on record prefixes
     static constexpr int TABLE_CLASS = kNumClasses, CELL_CLASS = QMSORT_REC_CELL_SORT ? 7 : kNumClasses,
                          CELL_BIG_CLASS = kNumClasses;
-    static constexpr int EVEN_TARGET = 0, EVEN_SPAN = 0;
+    static constexpr int EVEN_TARGET = 0, EVEN_SPAN = 0, EVEN_OVER = 0;
     static constexpr int TARGET_DIV = 2;
     static constexpr int LAST_NUM = 1, LAST_DEN = 2;  // measured: C5 block sort 2.55 -> 2.32 ms
     static constexpr int ST = 512, SI = 8;
@@ -758,7 +763,7 @@ static int samplesort(K* A, K* B, size_t n, const qmsort_gpu_config& cfg, unsign
                     (level == 0 && fused ? sample_xf_fn : sample_fn)<<<sample_grid, TU::ST, BSS::kSmemBytes, st>>>(
                         lv[cur].segs, &c->nsegs, src, tree[cur], sorted[cur], lut[cur], seed, 32u, lxf,
                         level == 0 ? presorted : nullptr, level == 0 ? presorted_n : 0u,
-                        (uint32_t)TU::EVEN_TARGET, (uint32_t)TU::EVEN_SPAN));
+                        (uint32_t)TU::EVEN_TARGET, (uint32_t)TU::EVEN_SPAN, (uint32_t)TU::EVEN_OVER));
             QLAUNCH(led, kPhCount, 0,
                     count_fn<<<count_grid, TU::CT, 0, st>>>(lv[cur].segs, lv[cur].chunks, 0u, &c->nchunks,
                                                             &c->work_count, src, tree[cur], sorted[cur],

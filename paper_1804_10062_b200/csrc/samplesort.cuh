@@ -525,7 +525,7 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
                                                uint32_t oversample, const Xf& xf,
                                                const K* __restrict__ presorted, uint32_t presorted_n,
                                                unsigned long long* sample_keys, uint32_t even_target,
-                                               uint32_t even_span) {
+                                               uint32_t even_span, uint32_t even_over) {
     using BS = BlockSorter<K, T, ITEMS>;
     using P = SmemPad<K>;
     using KT = KeyTraits<K>;
@@ -597,7 +597,9 @@ __device__ __forceinline__ void sample_segment(uint32_t seg, SegDesc* segs, cons
             // even_target keys spanning at most even_span values (the table
             // sort's tile and table, tablesort.cuh)
             uint32_t nr = K_;
-            if (even_target) {
+            // (8-byte keys: only where K ranges would leave buckets over
+            // even_over keys, the small cell-sort shape's tile, anyway)
+            if (even_target && d.len > (uint64_t)even_over * K_) {
                 uint64_t want = (d.len + even_target - 1) / even_target;
                 if (even_span) want = max(want, span / even_span + 1);
                 nr = (uint32_t)min((uint64_t)K_, max(want, (uint64_t)2));
@@ -810,14 +812,14 @@ __global__ void __launch_bounds__(T) sample_kernel(SegDesc* segs, const uint32_t
                                                    uint64_t seed, uint32_t oversample,
                                                    Xf xf = Xf{0, 0}, const K* presorted = nullptr,
                                                    uint32_t presorted_n = 0, uint32_t even_target = 0,
-                                                   uint32_t even_span = 0) {
+                                                   uint32_t even_span = 0, uint32_t even_over = 0) {
     if (QMSORT_LEVEL_OVERFLOWED(nsegs, nsegs)) return;
     const uint32_t ns = *nsegs;
     LevelCounters* lc = reinterpret_cast<LevelCounters*>(const_cast<uint32_t*>(nsegs));  // nsegs is its first member
     for (uint32_t seg = blockIdx.x; seg < ns; seg += gridDim.x) {
         sample_segment<K, T, ITEMS, XF>(seg, segs, src, tree_store, sorted_store, lut_store, seed,
                                         oversample, xf, presorted, presorted_n, &lc->sample_keys, even_target,
-                                        even_span);
+                                        even_span, even_over);
         __syncthreads();  // shared memory is reused by the next segment
     }
 }
