@@ -46,6 +46,12 @@ constexpr int kLutMaxBits = 12;
 #ifndef QMSORT_EVEN_SPLITTERS
 #define QMSORT_EVEN_SPLITTERS 1
 #endif
+#ifndef QMSORT_STAGE_KEY8
+#define QMSORT_STAGE_KEY8 1
+#endif
+#ifndef QMSORT_PREFETCH8
+#define QMSORT_PREFETCH8 1
+#endif
 constexpr int kLutPerSplitter = 16;  // LUT words reserved per splitter slot
 
 struct SegDesc {
@@ -1344,15 +1350,20 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
         // record is the key alone (8-byte keys: its tile index) -- 4 bytes
         // through shared memory instead of 8; the write-out recomputes the bin.
         if (d.arith) {
-            uint32_t* st4 = reinterpret_cast<uint32_t*>(sm.stage);
+            // 4- and 8-byte keys are staged themselves (QMSORT_STAGE_KEY8: 8-byte
+            // keys too -- 8 bytes through shared memory, no second read of the
+            // tile), records by their tile index
+            constexpr bool kKey = sizeof(K) == 4 || (sizeof(K) == 8 && QMSORT_STAGE_KEY8);
+            using SlotT = typename std::conditional<kKey && sizeof(K) == 8, uint64_t, uint32_t>::type;
+            SlotT* st = reinterpret_cast<SlotT*>(sm.stage);
             const uint32_t* binstart = reinterpret_cast<const uint32_t*>(sm.sd);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (FULL || u * T + tid < m) {
                     const uint32_t pos = binstart[bin[u] >> 16] + (bin[u] & 0xFFFFu);
                     QCHECK(pos < m, pos, m);
-                    if constexpr (SM::kStageIndex) st4[pos] = u * T + tid;
-                    else memcpy(&st4[pos], &k[u], 4);
+                    if constexpr (kKey) memcpy(&st[pos], &k[u], sizeof(SlotT));
+                    else st[pos] = u * T + tid;
                 }
             }
             if (mnext) load_tile<K, T, U, XF>(k, pnext, mnext, xf);
@@ -1361,14 +1372,14 @@ __device__ __forceinline__ void scatter_tile(ScatterSmem<K, T, U, LOG_KMAX>& sm,
             for (int u = 0; u < U; ++u) {
                 const uint32_t i = u * T + tid;
                 if (FULL || i < m) {
-                    const uint32_t v = st4[i];
+                    const SlotT v = st[i];
                     K raw, core;
-                    if constexpr (SM::kStageIndex) {
+                    if constexpr (kKey) {
+                        memcpy(&core, &v, sizeof(SlotT));
+                        raw = XF ? xf_inv(core, xf) : core;
+                    } else {
                         raw = p[v];
                         core = XF ? xf_fwd(raw, xf) : raw;
-                    } else {
-                        memcpy(&core, &v, 4);
-                        raw = XF ? xf_inv(core, xf) : core;
                     }
                     const uint32_t b = even_bucket<K>(core, d);
                     const uint32_t dest = binstart[SM::NB + b] + i;
@@ -1429,9 +1440,10 @@ __device__ __forceinline__ void scatter_chunk(ScatterSmem<K, T, U, LOG_KMAX>& sm
                                               uint32_t (&cursor)[ScatterSmem<K, T, U, LOG_KMAX>::BPT],
                                               const Xf& xf) {
     constexpr uint32_t TILE = (uint32_t)T * U;
-    // 4-byte keys only (measured: C2 scatter 1476 -> 1348 us; 8- and 32-byte
-    // keys, whose registers the write-out needs, lose 1-5 %)
-    constexpr bool kPrefetch = sizeof(K) == 4;
+    // 4- and 8-byte keys (measured: C2 scatter 1476 -> 1348 us; C3, with the
+    // keys themselves staged under even splitters, 11.5 -> 9.8 ms; records,
+    // whose registers the write-out needs, lose 5 %)
+    constexpr bool kPrefetch = sizeof(K) == 4 || (sizeof(K) == 8 && QMSORT_PREFETCH8);
     K k[U];
     if (kPrefetch) load_tile<K, T, U, XF>(k, p, min(len, TILE), xf);
     for (uint32_t t0 = 0; t0 < len;) {
