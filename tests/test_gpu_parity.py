@@ -441,3 +441,32 @@ def test_record_even_splitters(oracle, shape, n):
     np.testing.assert_array_equal(got, want)
     got, _ = gpu_sort(r, less="greater")
     np.testing.assert_array_equal(got, want[::-1])
+
+
+@pytest.mark.parametrize("dt", [DT_U32, DT_U64, DT_I64])
+@pytest.mark.parametrize("share", [0.08, 0.12, 0.15, 0.25, 0.6])
+def test_even_splitters_near_the_acceptance_threshold(oracle, dt, share):
+    """Mixtures around K1's even-splitter test: most keys uniform over the full
+    range plus `share` of them uniform over one eighth of it, so the ranges
+    inside that eighth hold 1.6 ... 5 times their share -- samples just under
+    the threshold are accepted (uneven buckets, deeper levels for the big
+    ones), samples over it keep the quantile splitters; and a last level whose
+    segments are dense in one half and empty in the other."""
+    n = 1 << 22
+    rng = np.random.default_rng(int(share * 100) + dt)
+    full = np.uint64(0xFFFFFFFF if dt == DT_U32 else 0xFFFFFFFFFFFFFFFF)
+    raw = rng.integers(0, 2**63, size=n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=n, dtype=np.uint64)
+    raw &= full
+    k = int(n * share)
+    raw[:k] = (raw[:k] >> np.uint64(3)) + (full >> np.uint64(2))
+    rng.shuffle(raw)
+    a = _as_dtype(raw, dt)
+    got, _ = gpu_sort(a)
+    np.testing.assert_array_equal(got, np.sort(a))
+    # every other 2^16-value stripe empty (uint32) / every other 2^40-value stripe (64-bit)
+    stripe = np.uint64(16 if dt == DT_U32 else 40)
+    b = _as_dtype(raw & ~(np.uint64(1) << stripe) & full, dt)
+    got, _ = gpu_sort(b)
+    np.testing.assert_array_equal(got, np.sort(b))
+    got, _ = gpu_sort(b, less="greater")
+    np.testing.assert_array_equal(got, np.sort(b)[::-1])
